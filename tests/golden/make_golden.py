@@ -1,0 +1,289 @@
+"""Generate the golden parity fixtures by running the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package `roboserve` from
+/root/reference/pkg/src, feeds it seeded synthetic inputs for every hot-path
+function (horizon.py:108-132, workload.py:461-496, core.py:31-47/157-166,
+waiting.py:46-100, scheduler.py:79-276, pkg/scratch_fig4.py) and stores the
+inputs together with the reference's outputs under tests/golden/.  The
+fixtures are what pins both the CPU oracle (oracle/) and the CUDA path; the
+GPU box never needs /root/reference.
+"""
+
+from __future__ import annotations
+
+import contextlib
+import io
+import json
+import os
+import runpy
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+REF_SRC = "/root/reference/pkg/src"
+REF_PKG = "/root/reference/pkg"
+sys.path.insert(0, REF_SRC)
+
+from roboserve import core, horizon, scheduler, waiting, workload  # noqa: E402
+from roboserve.core import Interval, LastExecInfo, PendingRequest, TaskState  # noqa: E402
+from roboserve.engines import EngineProfile  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+# --- step 1a: confidence horizon -------------------------------------------
+
+def gen_confidence(rng: np.random.Generator):
+    cases = []
+
+    def add(u, t, hmin):
+        mags = horizon.UpdateMagnitudes(u)
+        cfg = horizon.HorizonPolicyConfig.confidence(threshold=float(t), min_horizon=int(hmin))
+        cases.append((mags.u.copy(), float(t), int(hmin), horizon.decide_horizon(cfg, mags)))
+
+    # synthesized rounds: the reference's own magnitude model (workload.py:341-359)
+    for _ in range(700):
+        K = int(rng.integers(2, 11))
+        N = int(rng.choice([1, 2, 3, 7, 16, 31, 50, 64]))
+        spec = workload.SyntheticSpec(chunk_size=N, diffusion_steps=K,
+                                      uncertain_fraction=float(rng.uniform(0, 0.5)))
+        u = workload._synth_round_magnitudes(spec, rng).u
+        if rng.random() < 0.5:
+            u = u.astype(np.float32).astype(np.float64)   # fp32-storable
+        t = float(rng.choice([0.0, 0.2, 0.4, 0.8, 1.0, rng.uniform(0, 2)]))
+        add(u, t, int(rng.integers(1, 9)))
+    # bump == (1 + t) exactly: f = 1.8 * mean vs 1.8 * mean -> bit-level tie
+    for _ in range(100):
+        N = int(rng.integers(8, 65))
+        spec = workload.SyntheticSpec(chunk_size=N, diffusion_steps=6, uncertain_fraction=0.4)
+        add(workload._synth_round_magnitudes(spec, rng).u, 0.8, 1)
+    # wide dynamic range, zeros, ties, N == 1 with long pairwise sums
+    for _ in range(300):
+        K = int(rng.integers(2, 8))
+        N = int(rng.integers(1, 40))
+        u = rng.uniform(0, 1, (K, N)) * 10.0 ** rng.uniform(-6, 6, (K, N))
+        u[rng.random((K, N)) < 0.15] = 0.0
+        if rng.random() < 0.3:
+            u[-1] = u[:-1].mean(axis=0) * rng.choice([1.0, 1.4, 1.5])
+        add(u.astype(np.float32).astype(np.float64), float(rng.choice([0.0, 0.4, 0.5])),
+            int(rng.integers(1, 4)))
+    for K in list(range(2, 40)) + [64, 129, 130, 200, 300]:
+        u = rng.uniform(0, 1, (K, 1)) * 10.0 ** rng.uniform(-5, 5, (K, 1))
+        add(u, float(rng.uniform(0, 1)), 1)
+    return cases
+
+
+def save_confidence(cases):
+    shapes = np.array([c[0].shape for c in cases], np.int64)
+    offs = np.concatenate([[0], np.cumsum(shapes[:, 0] * shapes[:, 1])]).astype(np.int64)
+    np.savez_compressed(
+        OUT / "horizon_confidence.npz",
+        u=np.concatenate([c[0].ravel() for c in cases]), shapes=shapes, offsets=offs,
+        threshold=np.array([c[1] for c in cases]), min_horizon=np.array([c[2] for c in cases]),
+        expected=np.array([c[3] for c in cases], np.int64))
+
+
+# --- step 1b: divergence horizon + cosine scores ----------------------------
+
+def gen_divergence(rng: np.random.Generator):
+    cases = []
+    for ci in range(420):
+        D = int(rng.choice([1, 2, 3, 4, 7, 8, 12, 15, 16, 17, 20, 24, 31, 32, 33, 40, 48, 64]))
+        Lr = int(rng.integers(1, 41))
+        Lc = Lr if rng.random() < 0.7 else int(rng.integers(1, 41))
+        ref = rng.normal(0, 1, (Lr, D)) * 10.0 ** rng.uniform(-3, 3)
+        L = max(Lr, Lc)
+        noise = rng.normal(0, 1, (L, D)) * (0.3 * np.arange(1, L + 1)[:, None] / L)
+        cand = np.zeros((Lc, D))
+        m = min(Lr, Lc)
+        cand[:m] = ref[:m] + noise[:m] * np.abs(ref[:m]).mean()
+        if Lc > m:
+            cand[m:] = rng.normal(0, 1, (Lc - m, D))
+        if rng.random() < 0.1:
+            ref[rng.integers(0, Lr)] = 0.0
+        if rng.random() < 0.1:
+            cand[rng.integers(0, Lc)] = 0.0
+        if rng.random() < 0.5:
+            ref = ref.astype(np.float32).astype(np.float64)
+            cand = cand.astype(np.float32).astype(np.float64)
+        cos = np.array([workload._cosine(cand[i], ref[i]) for i in range(m)])
+        if ci % 5 == 0 and m > 1:
+            thr = float(cos[int(rng.integers(0, m))])     # exact tie: cos == thr passes
+            thr = min(1.0, max(thr, 1e-3)) if thr > 0 else 0.5
+        else:
+            thr = float(rng.choice([0.9, 0.95, 0.99, rng.uniform(0.05, 1.0), 1.0]))
+        h = workload.round_optimal_horizon(ref, cand, thr)
+        cases.append((ref, cand, thr, h, cos))
+    # reference test-suite shapes (tests/test_workload.py:211-229)
+    return cases
+
+
+def save_divergence(cases):
+    rs = np.array([c[0].shape for c in cases], np.int64)
+    cs = np.array([c[1].shape for c in cases], np.int64)
+    np.savez_compressed(
+        OUT / "divergence.npz",
+        ref=np.concatenate([c[0].ravel() for c in cases]),
+        cand=np.concatenate([c[1].ravel() for c in cases]),
+        ref_shapes=rs, cand_shapes=cs,
+        ref_off=np.concatenate([[0], np.cumsum(rs[:, 0] * rs[:, 1])]).astype(np.int64),
+        cand_off=np.concatenate([[0], np.cumsum(cs[:, 0] * cs[:, 1])]).astype(np.int64),
+        thr=np.array([c[2] for c in cases]), expected=np.array([c[3] for c in cases], np.int64),
+        cos=np.concatenate([c[4] for c in cases]),
+        cos_off=np.concatenate([[0], np.cumsum([len(c[4]) for c in cases])]).astype(np.int64))
+
+
+# --- step 2: time, ledger, ratio, bucket ------------------------------------
+
+def gen_time(rng):
+    rows = []
+    hzs = [1, 2, 3, 7.5, 10, 29.97, 30, 30.0, 50, 59.94, 100, 1000.0, 1 / 3, 0.1, 12.5, 240]
+    for hz in hzs:
+        for c in [0, 1, 2, 3, 9, 10, 29, 30, 48, 50, 64, 99, 1000, 12345, 10**6]:
+            rows.append({"count": c, "hz": hz, "us": core.us_from_actions(c, hz)})
+    for _ in range(300):
+        hz = float(rng.choice(hzs))
+        c = int(rng.integers(0, 5000))
+        rows.append({"count": c, "hz": hz, "us": core.us_from_actions(c, hz)})
+    return rows
+
+
+def random_state(rng, tid: str, now: int, max_rounds: int = 6, p_inflight: float = 0.4):
+    """A TaskState built through its own mutators (core.py:192-219)."""
+    t = int(now - rng.integers(500_000, 20_000_000))
+    st = TaskState(task_id=tid, t_start=t, accumulated_generation=int(rng.integers(0, 5_000_000)))
+    n = int(rng.integers(0, max_rounds + 1))
+    cur = t
+    for j in range(n):
+        gs = cur + int(rng.integers(0, 200_000))
+        ge = gs + int(rng.integers(100_000, 400_000))
+        es = ge + int(rng.integers(0, 50_000))
+        ee = es + core.exec_duration(int(rng.integers(10, 51)), 30)
+        st.begin_generation(j, gs)
+        st.finish_generation(j, ge)
+        st.record_execution(j, es, ee, 1)
+        cur = ee - int(rng.integers(0, 300_000))
+    if rng.random() < p_inflight:
+        st.begin_generation(n, cur + int(rng.integers(0, 200_000)))
+    return st
+
+
+def state_json(st: TaskState):
+    return {"task_id": st.task_id, "t_start": st.t_start, "skipped": st.skipped,
+            "accumulated_generation": st.accumulated_generation,
+            "gen_starts": list(st.gen_starts), "gen_ends": list(st.gen_ends),
+            "exec_intervals": [[iv.start, iv.end] for iv in st.exec_intervals],
+            "horizons": list(st.horizons)}
+
+
+def req_json(r: PendingRequest):
+    return {"task_id": r.task_id, "round_id": r.round_id, "issued_at": r.issued_at,
+            "obs_captured_at": r.obs_captured_at,
+            "last_exec_info": [r.last_exec_info.exec_start, r.last_exec_info.remaining_actions],
+            "payload_bytes": r.payload_bytes, "skipped": r.skipped}
+
+
+def gen_plan(rng):
+    instances = []
+    for ii in range(140):
+        now = 100_000_000
+        P = int(rng.choice([1, 2, 3, 5, 17, 64, 120]))
+        tie_heavy = ii % 4 == 0
+        id_style = rng.integers(0, 3)
+        if id_style == 0:
+            ids = [f"task-{i:04d}" for i in rng.choice(20000, P, replace=False)]
+        elif id_style == 1:
+            ids = [str(i) for i in rng.choice(100000, P, replace=False)]
+        else:
+            ids = ["".join(rng.choice(list("abAB09-_z"), int(rng.integers(1, 6)))) + f"#{i}"
+                   for i in range(P)]
+        states, pending = {}, []
+        for tid in ids:
+            st = random_state(rng, tid, now, max_rounds=2 if tie_heavy else 6)
+            if tie_heavy:
+                st.t_start = now - 1_000_000
+            states[tid] = st
+            skipped = int(rng.integers(0, 3 if tie_heavy else 13))
+            st.skipped = skipped
+            issued = now - int(rng.integers(0, 3 if tie_heavy else 1_000_000))
+            pending.append(PendingRequest(
+                task_id=tid, round_id=len(st.exec_intervals), issued_at=issued,
+                obs_captured_at=issued - int(rng.integers(0, 300_000)),
+                last_exec_info=LastExecInfo(issued - 1000, int(rng.integers(0, 40))),
+                payload_bytes=int(rng.integers(0, 400_000)), skipped=skipped))
+        policy = ["kairos", "fifo", "las"][ii % 3] if ii % 7 else "kairos"
+        B = int(rng.choice([1, 2, 5, 10, 16]))
+        A = int(rng.choice([1, 3, 5, 7]))
+        cfg = scheduler.SchedulerConfig(policy=policy, buckets=B, aging_interval=A,
+                                        stale_threshold=int(rng.choice([0, 150_000, 10**9])),
+                                        default_exec_estimate=int(rng.choice([166_667, 0, 10**6])))
+        cap = int(rng.integers(1, max(2, P + 3)))
+        in_flight = int(rng.integers(0, 3))
+        edge = EngineProfile(tier="edge", capacity=cap, max_batch=1, points=((1, 1000),))
+        before = {t: state_json(s) for t, s in states.items()}
+        # per-request intermediates through the reference functions
+        inter = {}
+        for r in pending:
+            s = states[r.task_id]
+            wr = waiting.current_wait_ratio(s, now)
+            inter[r.task_id] = {
+                "total_wait": waiting.ledger_from_history(s).total_wait, "wr": wr,
+                "bucket": scheduler.assign_bucket(wr, r.skipped, cfg),
+                "est": scheduler.estimate_exec_latency(s, cfg.default_exec_estimate),
+                "need_time": core.exec_end_from_piggyback(r, 30)}
+        order_in = list(pending)
+        rng.shuffle(order_in)
+        plan = scheduler.plan(order_in, states, edge, None, None, now, cfg,
+                              edge_in_flight=in_flight)
+        instances.append({
+            "now": now, "policy": policy, "buckets": B, "aging_interval": A,
+            "stale_threshold": cfg.stale_threshold,
+            "default_exec_estimate": cfg.default_exec_estimate,
+            "capacity": cap, "edge_in_flight": in_flight, "control_hz": 30,
+            "states": list(before.values()), "pending": [req_json(r) for r in order_in],
+            "intermediates": inter,
+            "expected": {
+                "edge": [r.task_id for r in plan.edge],
+                "deferred": [[r.task_id, r.skipped] for r in plan.deferred],
+                "refetch": sorted(plan.refetch_task_ids),
+                "skipped_after": {t: s.skipped for t, s in states.items()}}})
+    return instances
+
+
+def gen_fig4():
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        g = runpy.run_path(os.path.join(REF_PKG, "scratch_fig4.py"), run_name="scratch_fig4")
+    out = []
+    for durs, gen in g["candidates"]:
+        durs_us = [[d * g["MS"] for d in task] for task in durs]
+        kai = g["policy_order"](durs_us, gen * g["MS"], g["kairos_choose_factory"](durs_us, gen * g["MS"]))
+        fifo = g["policy_order"](durs_us, gen * g["MS"], g["fifo_choose"])
+        las = g["policy_order"](durs_us, gen * g["MS"], g["las_choose_factory"](gen * g["MS"]))
+        w_kai, w_fifo, w_las, w_opt = g["evaluate"](durs_us, gen * g["MS"])
+        out.append({"durs": durs, "gen": gen, "kairos": list(kai), "fifo": list(fifo),
+                    "las": list(las), "w_kai": w_kai, "w_fifo": w_fifo, "w_las": w_las,
+                    "w_opt": w_opt})
+    return {"stdout": buf.getvalue(), "candidates": out}
+
+
+def main():
+    rng = np.random.default_rng(20260517)
+    save_confidence(gen_confidence(rng))
+    save_divergence(gen_divergence(rng))
+    (OUT / "time.json").write_text(json.dumps(gen_time(rng)))
+    (OUT / "plan.json").write_text(json.dumps(gen_plan(rng), separators=(",", ":")))
+    (OUT / "fig4.json").write_text(json.dumps(gen_fig4(), indent=1))
+    for p in sorted(OUT.iterdir()):
+        if p.suffix in (".npz", ".json"):
+            print(f"{p.name:28s} {p.stat().st_size:>9d} B")
+
+
+if __name__ == "__main__":
+    main()

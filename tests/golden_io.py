@@ -1,0 +1,82 @@
+"""Loaders for the reference-generated fixtures in tests/golden/ (see make_golden.py)."""
+
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+import numpy as np
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def confidence_cases():
+    z = np.load(GOLDEN / "horizon_confidence.npz")
+    out = []
+    for i, (k, n) in enumerate(z["shapes"]):
+        u = z["u"][z["offsets"][i]:z["offsets"][i + 1]].reshape(k, n)
+        out.append((u, float(z["threshold"][i]), int(z["min_horizon"][i]), int(z["expected"][i])))
+    return out
+
+
+def divergence_cases():
+    z = np.load(GOLDEN / "divergence.npz")
+    out = []
+    for i in range(len(z["thr"])):
+        ref = z["ref"][z["ref_off"][i]:z["ref_off"][i + 1]].reshape(z["ref_shapes"][i])
+        cand = z["cand"][z["cand_off"][i]:z["cand_off"][i + 1]].reshape(z["cand_shapes"][i])
+        cos = z["cos"][z["cos_off"][i]:z["cos_off"][i + 1]]
+        out.append((ref, cand, float(z["thr"][i]), int(z["expected"][i]), cos))
+    return out
+
+
+def time_rows():
+    return json.loads((GOLDEN / "time.json").read_text())
+
+
+def plan_instances():
+    return json.loads((GOLDEN / "plan.json").read_text())
+
+
+def fig4():
+    return json.loads((GOLDEN / "fig4.json").read_text())
+
+
+def build_objects(inst, mod):
+    """Rebuild TaskState / PendingRequest objects of module `mod` (any package
+    exposing the reference's core types) from a plan fixture."""
+    states = {}
+    for s in inst["states"]:
+        st = mod.TaskState(task_id=s["task_id"], t_start=s["t_start"], skipped=s["skipped"],
+                           accumulated_generation=s["accumulated_generation"])
+        for j, gs in enumerate(s["gen_starts"]):
+            st.begin_generation(j, gs)
+            if s["gen_ends"][j] is not None:
+                st.finish_generation(j, s["gen_ends"][j])
+        for j, (es, ee) in enumerate(s["exec_intervals"]):
+            st.record_execution(j, es, ee, s["horizons"][j])
+        states[st.task_id] = st
+    pending = [mod.PendingRequest(task_id=r["task_id"], round_id=r["round_id"],
+                                  issued_at=r["issued_at"], obs_captured_at=r["obs_captured_at"],
+                                  last_exec_info=mod.LastExecInfo(*r["last_exec_info"]),
+                                  payload_bytes=r["payload_bytes"], skipped=r["skipped"])
+               for r in inst["pending"]]
+    return states, pending
+
+
+def ns_objects(inst):
+    """Duck-typed stand-ins (SimpleNamespace) for the fixture's states / requests."""
+    from types import SimpleNamespace as NS
+    states = {}
+    for s in inst["states"]:
+        states[s["task_id"]] = NS(
+            task_id=s["task_id"], t_start=s["t_start"], skipped=s["skipped"],
+            accumulated_generation=s["accumulated_generation"],
+            gen_starts=list(s["gen_starts"]), gen_ends=list(s["gen_ends"]),
+            exec_intervals=[NS(start=a, end=b) for a, b in s["exec_intervals"]])
+    pending = [NS(task_id=r["task_id"], issued_at=r["issued_at"],
+                  obs_captured_at=r["obs_captured_at"], skipped=r["skipped"],
+                  last_exec_info=NS(exec_start=r["last_exec_info"][0],
+                                    remaining_actions=r["last_exec_info"][1]))
+               for r in inst["pending"]]
+    return states, pending

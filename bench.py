@@ -1,0 +1,376 @@
+"""Benchmark: robot-rounds/s of the Kairos decision core (horizon + urgency +
+top-k admission) on B200, per BASELINE.json.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Workload (BASELINE.json configs[4], one GPU's share; weak scaling): each GPU
+owns R = 2^20 pending robots.  A step is one decision round over the whole
+fleet: divergence horizon of the new 50x7 fp32 chunk against the unexecuted
+overlap of the previous chunk (offset U[0,10], threshold 0.9), urgency keys
+from 0-5-round histories, and edge admission of the global top k = 8192 (NCCL
+all-gather of per-shard candidates when N > 1).  Inputs (2.9 GB per GPU) are
+larger than L2, so no flush is needed between steps.
+
+`value` is device-timed (CUDA events, barrier + synchronize both sides, max
+over ranks) with inputs resident in HBM; `e2e` runs the same round through the
+C ABI from pinned host buffers with the host->device copies of every input and
+the device->host read of every output inside the timed region.
+`--impl reference` times the CPU restatement of the reference path
+(oracle/, all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "robot-rounds/sec for horizon+schedule decisions"
+UNIT = "robot-rounds/s"
+R_DEFAULT = 1 << 20
+K_DEFAULT = 8192
+LP = LC = 50
+D = 7
+THR = 0.9
+# algorithmic bytes per robot-round of the dominant kernel (kr_horizon_divergence):
+# prev row block + candidate row block (fp32) + offset (int32) in, horizon (int32) out
+DIV_BYTES = (LP + LC) * D * 4 + 4 + 4
+
+
+def workload_config(args, world):
+    return {
+        "workload": "configs[4] per-GPU share: 2^20 pending robots/GPU, divergence horizon "
+                    "(prev/new chunk 50x7 fp32, overlap offset U[0,10], thr 0.9) + urgency "
+                    "(0-5 round histories) + global top-k=8192 admission",
+        "robots_per_gpu": args.robots, "global_k": args.k, "chunk": [LP, D], "samples": 1,
+        "policy": "kairos B=10 A=5", "parallelism": f"robot-sharded x{world}",
+        "l2": "inputs 2.9 GB/GPU > 126 MB L2 (no flush needed)",
+    }
+
+
+# --------------------------------------------------------------------------
+# clocks (NVML, sampled during the timed region)
+# --------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("kr_horizon_divergence_bytes_per_launch"), d.get("source")
+    return None, None
+
+
+# --------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle port on the host cores
+# --------------------------------------------------------------------------
+def cpu_round(R: int, seed: int, nthreads: int):
+    """One bounded CPU decision round of R robots with the oracle port:
+    returns (seconds, nthreads)."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2605_11381_b200 import synthetic
+    soa = synthetic.fleet_soa(R, seed=seed)
+    prev, cand, off = synthetic.chunks(R, seed=seed + 1, device="cpu")
+    prev, cand, off = prev.numpy(), cand.numpy(), off.numpy()
+    t0 = time.perf_counter()
+    orc.divergence_batch(prev, cand, THR, off, nthreads=nthreads)
+    orc.plan_soa(soa, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, min(K_DEFAULT, R))
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(target_s: float = 10.0):
+    from oracle import oracle as orc
+    nthreads = orc.nthreads_default()
+    t_small = cpu_round(8192, 5, nthreads)
+    R = int(min(R_DEFAULT, max(8192, 8192 * target_s / max(t_small, 1e-6) / 3)))
+    times = [cpu_round(R, 7 + i, nthreads) for i in range(3)]
+    t = statistics.median(times)
+    return {"value": R / t, "unit": UNIT, "cores": nthreads, "kind": "port",
+            "sample": f"{R} robots x 3 rounds (median), oracle/ C port: OpenMP divergence "
+                      f"horizon ({nthreads} threads) + serial plan() sort/admission"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    nthreads = orc.nthreads_default()
+    R = args.ref_robots
+    for i in range(args.warmup):
+        cpu_round(R, 100 + i, nthreads)
+    times = [cpu_round(R, 200 + i, nthreads) for i in range(args.steps)]
+    total = sum(times)
+    value = R * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": f"{R} robots per step (bounded sample of the per-GPU "
+                                   f"workload), oracle/ C restatement of the reference path"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_ours(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_11381_b200 import _lib, fleet as fl, rounds, synthetic
+
+    torch.cuda.set_device(local_rank)
+    lib = _lib.load()
+    R = args.robots
+    soa = synthetic.fleet_soa(R, seed=1000 + rank, rank_offset=rank * R)
+    fleet = fl.DeviceFleet.from_host(soa)
+    prev, cand, off = synthetic.chunks(R, seed=2000 + rank)
+    base = synthetic.NOW - (1 << 39)
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, base)
+    if world > 1:
+        rnd = rounds.ShardedDecisionRound(R, args.k, sched)
+    else:
+        rnd = rounds.DecisionRound(R, args.k, sched)
+    inputs = rounds.DivergenceInputs(prev, cand, THR, offset=off)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        rnd.run(fleet, inputs)
+    barrier()
+
+    # timed region: K whole rounds; divergence kernel bracketed by events
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = lib.kr_launch_count()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            rnd.horizons(inputs)
+            ev[i][1].record(stream)
+            rnd.urgency(fleet)
+            rnd.admit(fleet)
+        end.record(stream)
+        barrier()
+    launches = lib.kr_launch_count() - n0
+    elapsed = start.elapsed_time(end) / 1e3
+    div_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    value = R * world * args.steps / elapsed
+
+    # kernel breakdown of one extra round (events between the three steps)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    e[0].record(stream); rnd.horizons(inputs); e[1].record(stream)
+    rnd.urgency(fleet); e[2].record(stream); rnd.admit(fleet); e[3].record(stream)
+    torch.cuda.synchronize()
+    breakdown = {"horizon_divergence_ms": e[0].elapsed_time(e[1]),
+                 "urgency_ms": e[1].elapsed_time(e[2]), "admission_ms": e[2].elapsed_time(e[3])}
+
+    e2e = run_e2e(args, world, soa, prev, cand, off, sched) if not args.no_e2e else None
+
+    if rank != 0:
+        return
+    peak, peak_src = hbm_peak()
+    div_avg_s = statistics.mean(div_ms) / 1e3
+    achieved = DIV_BYTES * R / div_avg_s / 1e9
+    traffic, traffic_src = ncu_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded: fleet histories + N(0,1) action chunks, SURVEY.md 8d)",
+        "config": workload_config(args, world),
+        "roofline": {"bound": "hbm", "kernel": "kr_horizon_divergence", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_robot_round": DIV_BYTES,
+                     "launch_ms_mean": statistics.mean(div_ms),
+                     "traffic_source": traffic_src},
+        "kernels": breakdown,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, world, soa, prev, cand, off, sched):
+    """Same round through the C ABI from pinned host buffers (copies timed)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_11381_b200 import fleet as fl, rounds
+
+    R = args.robots
+    h_prev = prev.cpu().pin_memory()
+    h_cand = cand.cpu().pin_memory()
+    h_off = off.cpu().pin_memory()
+    h_soa = {k: torch.from_numpy(np.ascontiguousarray(soa[k])).pin_memory()
+             for k in fl.INT_FIELDS64 + fl.INT_FIELDS32 + ("slots",)}
+    d_prev, d_cand, d_off = torch.empty_like(prev), torch.empty_like(cand), torch.empty_like(off)
+    d_soa = {k: torch.empty(v.shape, dtype=v.dtype, device="cuda") for k, v in h_soa.items()}
+    fleet = fl.DeviceFleet.from_tensors(d_soa)
+    rnd = (rounds.ShardedDecisionRound(R, args.k, sched) if world > 1
+           else rounds.DecisionRound(R, args.k, sched))
+    outs = {"H": torch.empty(R, dtype=torch.int32).pin_memory(),
+            "need": torch.empty(R, dtype=torch.int64).pin_memory(),
+            "adm": torch.empty(R, dtype=torch.uint8).pin_memory(),
+            "ref": torch.empty(R, dtype=torch.uint8).pin_memory(),
+            "skip": torch.empty(R, dtype=torch.int32).pin_memory(),
+            "edge": torch.empty((max(rnd.k, 1), 2), dtype=torch.int64).pin_memory()}
+    h2d = sum(t.numel() * t.element_size() for t in [h_prev, h_cand, h_off, *h_soa.values()])
+    d2h = sum(t.numel() * t.element_size() for t in outs.values())
+
+    def step():
+        d_prev.copy_(h_prev, non_blocking=True)
+        d_cand.copy_(h_cand, non_blocking=True)
+        d_off.copy_(h_off, non_blocking=True)
+        for k, v in h_soa.items():
+            d_soa[k].copy_(v, non_blocking=True)
+        o = rnd.run(fleet, rounds.DivergenceInputs(d_prev, d_cand, THR, offset=d_off))
+        outs["H"].copy_(o.horizon, non_blocking=True)
+        outs["need"].copy_(o.need_time, non_blocking=True)
+        outs["adm"].copy_(o.admitted, non_blocking=True)
+        outs["ref"].copy_(o.refetch, non_blocking=True)
+        outs["skip"].copy_(fleet.t["skipped"], non_blocking=True)
+        outs["edge"][: o.edge_keys.shape[0]].copy_(o.edge_keys, non_blocking=True)
+
+    steps = max(1, min(args.steps, args.e2e_steps))
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    el = torch.tensor([s.elapsed_time(e) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    t = float(el.item())
+    return {"value": R * world * steps / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": 1e3 * t / steps,
+            "path": "pinned host buffers -> H2D -> decision round (C ABI) -> D2H of horizons, "
+                    "need times, masks, skip counters, ordered S_e"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--robots", type=int, default=R_DEFAULT)
+    ap.add_argument("--k", type=int, default=K_DEFAULT)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-robots", type=int, default=16384)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, world, rank, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * kairos_b200.h -- C ABI of the B200-native Kairos decision core.
+ *
+ * One shared library, libkairos_b200.so (built from
+ * paper_2605_11381_b200/csrc/ for sm_100a), exports exactly these entry points.
+ * They replace the reference's pure-Python hot path (paths relative to
+ * /root/reference/pkg/src/roboserve/):
+ *
+ *   kr_horizon_confidence   horizon.py:108-132   decide_horizon (confidence branch)
+ *   kr_horizon_static       horizon.py:121-122   decide_horizon (static branch)
+ *   kr_horizon_divergence   workload.py:461-496  _cosine + round_optimal_horizon
+ *   kr_us_from_actions      core.py:24-47,157-166 us_from_actions / exec_end_from_piggyback
+ *   kr_wait_ratio           waiting.py:62-66,96-100 wait_ratio / current_wait_ratio
+ *   kr_assign_bucket        scheduler.py:79-88   assign_bucket
+ *   kr_urgency              waiting.py:69-93 + scheduler.py:79-140,143-157
+ *                           ledger, wait ratio, bucket, exec estimate, sort key
+ *   kr_topk_select          scheduler.py:204-207 edge prefix S_e = order[:k]
+ *   kr_admit                scheduler.py:223-234 refetch + skip counters
+ *   kr_sort_keys            scheduler.py:130-140 the total order itself
+ *
+ * Conventions: every pointer argument that names device data is a device
+ * pointer; kr_fleet / kr_sched structs themselves live in host memory.  All
+ * calls are asynchronous on `stream` (a cudaStream_t, NULL = legacy default),
+ * never allocate, never synchronise (except where documented), and return a
+ * kr_status.  Data-dependent validation (non-finite magnitudes, key-field
+ * overflow) is reported through a caller-owned device word `flags` that the
+ * kernels atomically OR; the host shim raises the reference's ValueError.
+ * No C++ exception crosses this boundary.  Stream-ordered and re-entrant per
+ * stream; no global mutable state.
+ */
+#ifndef KAIROS_B200_H
+#define KAIROS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KR_API __attribute__((visibility("default")))
+#else
+#define KR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KR_OK = 0,
+    KR_EINVAL = 1,     /* bad shape / argument (host-side check) */
+    KR_ECUDA = 2,      /* CUDA launch / runtime error */
+    KR_ENOSPACE = 3,   /* workspace too small */
+} kr_status;
+
+enum { KR_F32 = 0, KR_F64 = 1 };
+enum { KR_KAIROS = 0, KR_FIFO = 1, KR_LAS = 2 };
+
+/* Device validation flags (OR-ed into *flags). */
+#define KR_FLAG_NONFINITE  0x1u  /* horizon.py:47-48  "update magnitudes must be finite" */
+#define KR_FLAG_NEGATIVE   0x2u  /* horizon.py:49-50  "update magnitudes must be >= 0"   */
+#define KR_FLAG_KEY_RANGE  0x4u  /* packed sort-key field out of range */
+#define KR_FLAG_TIME_RANGE 0x8u  /* core.py:38-41 negative action count / overflow       */
+#define KR_FLAG_RATIO      0x10u /* wait-ratio operand beyond 2^53 (inexact double)      */
+
+/* 128-bit composite sort key (ascending = reference order). */
+typedef struct kr_key {
+    uint64_t hi;
+    uint64_t lo;
+} kr_key;
+
+/* Fleet structure-of-arrays: one entry per pending request. */
+typedef struct kr_fleet {
+    int64_t n;
+    const int64_t* t_start;          /* TaskState.t_start                     core.py:187 */
+    const int64_t* issued_at;        /* PendingRequest.issued_at              core.py:147 */
+    const int64_t* obs_captured_at;  /* PendingRequest.obs_captured_at        core.py:148 */
+    const int64_t* accum_gen;        /* TaskState.accumulated_generation      core.py:189 */
+    const int32_t* remaining;        /* LastExecInfo.remaining_actions        core.py:127 */
+    const int32_t* lexrank;          /* position of task_id in sorted(task ids)          */
+    int32_t* skipped;                /* PendingRequest.skipped in, TaskState.skipped out  */
+    const int64_t* hist_off;         /* CSR slot offset per request                      */
+    const int32_t* n_exec;           /* len(TaskState.exec_intervals)                    */
+    const int32_t* n_gen;            /* len(TaskState.gen_starts)                        */
+    const int64_t* slots;            /* [*][4] gen_start, gen_end, exec_start, exec_end  */
+} kr_fleet;
+
+/* SchedulerConfig (scheduler.py:38-56) plus the round's scalars. */
+typedef struct kr_sched {
+    int32_t policy;                  /* KR_KAIROS / KR_FIFO / KR_LAS */
+    int32_t buckets;                 /* B, 1..256 */
+    int32_t aging_interval;          /* A >= 1 */
+    int32_t pad_;
+    int64_t stale_threshold;         /* µs */
+    int64_t default_exec_estimate;   /* µs */
+    int64_t now;                     /* µs */
+    int64_t hz_num, hz_den;          /* control_hz == hz_num / hz_den exactly */
+    int64_t issued_base;             /* key origin: issued_at - issued_base in [0, 2^40) */
+} kr_sched;
+
+KR_API const char* kr_version(void);
+KR_API const char* kr_status_string(int status);
+/* Last CUDA error string recorded by a failing call on this thread. */
+KR_API const char* kr_last_error(void);
+/* Kernels launched by this library so far in this process (diagnostic). */
+KR_API unsigned long long kr_launch_count(void);
+
+/* ---- step 1: execution-horizon selection ------------------------------ */
+
+/* U: [R][K][N] fp32 (dtype KR_F32) or fp64, row-major.  H[r] = decide_horizon.
+ * one_plus_t = 1.0 + threshold computed on the host in fp64 (horizon.py:127). */
+KR_API int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_t K, int32_t N,
+                          double one_plus_t, int32_t min_horizon, int32_t* H,
+                          uint32_t* flags, void* stream);
+KR_API int kr_horizon_static(int64_t R, int32_t N, int32_t static_h, int32_t* H, void* stream);
+
+/* prev: [R][Lp][D], cand: [R][S][Lc][D] (same dtype).  For robot r the
+ * reference trajectory is prev[r][off_r : len_prev_r] (the unexecuted overlap
+ * of the previous chunk), the candidates cand[r][s][0 : len_cand_r].
+ * H[r] = min_s round_optimal_horizon(ref_r, cand_{r,s}, thr).  offset /
+ * len_prev / len_cand may be NULL (0 / Lp / Lc).  cos (nullable) receives the
+ * fp64 cosine of every (r, s, i < limit_r), NaN beyond the limit. */
+KR_API int kr_horizon_divergence(const void* prev, const void* cand, int dtype, int64_t R,
+                          int32_t S, int32_t Lp, int32_t Lc, int32_t D,
+                          const int32_t* offset, const int32_t* len_prev,
+                          const int32_t* len_cand, double thr, int32_t* H, double* cos,
+                          void* stream);
+
+/* ---- step 2: execution-aware urgency ---------------------------------- */
+
+/* out[i] = (base ? base[i] : 0) + us_from_actions(count[i], hz_num/hz_den). */
+KR_API int kr_us_from_actions(const int64_t* count, const int64_t* base, int64_t n, int64_t hz_num,
+                       int64_t hz_den, int64_t* out, uint32_t* flags, void* stream);
+/* wr[i] = current_wait_ratio semantics: 0 if now <= t_start[i]. */
+KR_API int kr_wait_ratio(const int64_t* total_wait, const int64_t* t_start, int64_t n, int64_t now,
+                  double* wr, uint32_t* flags, void* stream);
+KR_API int kr_assign_bucket(const double* wr, const int32_t* skipped, int64_t n, int32_t buckets,
+                     int32_t aging_interval, int32_t* bucket, void* stream);
+/* Fused per-request pass: ledger -> wait ratio -> bucket -> exec estimate ->
+ * aged estimate -> packed key (+ next-need time).  Optional outputs nullable;
+ * slot_wait[hist_off + j] receives round j's recorded wait, or -1 where the
+ * ledger records none (WaitLedger.waits, waiting.py:82-92). */
+KR_API int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys, int64_t* need_time,
+               int64_t* total_wait, double* wr, int32_t* bucket, int64_t* est,
+               int64_t* slot_wait, uint32_t* flags, void* stream);
+
+/* ---- step 3: priority ordering + top-k admission ---------------------- */
+
+/* Bytes of scratch needed by kr_topk_select / kr_sort_keys for n keys. */
+KR_API size_t kr_workspace_bytes(int64_t n);
+/* Device-side k-th smallest key (MSD radix select).  *kth is undefined for
+ * k == 0; for k >= n it is the all-ones key. */
+KR_API int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth, void* workspace,
+                   size_t workspace_bytes, void* stream);
+/* Admission pass over n keys (scheduler.py:204-207, 223-234):
+ *   admitted[i] = k > 0 && (kth == NULL || key_i <= *kth)
+ * (kth NULL with k > 0 admits everything, i.e. k >= n), refetch[i] = admitted
+ * && now - obs_captured_at > stale_threshold, skip counters updated in place
+ * (admitted -> 0, deferred -> skipped + 1).  With edge_idx / edge_keys the
+ * admitted (key, index) pairs -- exactly min(k, n) of them when kth is the
+ * k-th smallest key -- are gathered and sorted, so edge_idx is S_e in
+ * reference order.  admitted / refetch / edge outputs nullable; fleet / cfg
+ * may be NULL when neither refetch nor skip counters are wanted. */
+KR_API int kr_admit(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
+             const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
+             int32_t* edge_idx, kr_key* edge_keys, void* workspace, size_t workspace_bytes,
+             void* stream);
+/* Full argsort of n unique keys (ascending).  Synchronises `stream` once
+ * when n exceeds the single-CTA limit (pass plan read back to the host). */
+KR_API int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_key* sorted_keys,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,124 @@
+"""ctypes binding of libkairos_b200.so (include/kairos_b200.h).
+
+The decision core has no CPU fallback: if the library is missing, or no CUDA
+device is visible, every compute entry point raises instead of silently
+computing on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import torch
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libkairos_b200.so"
+
+KR_OK, KR_EINVAL, KR_ECUDA, KR_ENOSPACE = 0, 1, 2, 3
+KR_F32, KR_F64 = 0, 1
+KR_KAIROS, KR_FIFO, KR_LAS = 0, 1, 2
+
+FLAG_NONFINITE = 0x1
+FLAG_NEGATIVE = 0x2
+FLAG_KEY_RANGE = 0x4
+FLAG_TIME_RANGE = 0x8
+FLAG_RATIO = 0x10
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_f64 = ctypes.c_double
+
+
+class KrFleet(ctypes.Structure):
+    """kr_fleet: device pointers of the fleet structure-of-arrays."""
+
+    _fields_ = [("n", _i64)] + [(name, _vp) for name in (
+        "t_start", "issued_at", "obs_captured_at", "accum_gen", "remaining", "lexrank",
+        "skipped", "hist_off", "n_exec", "n_gen", "slots")]
+
+
+class KrSched(ctypes.Structure):
+    """kr_sched: SchedulerConfig plus the round's scalars."""
+
+    _fields_ = [("policy", _i32), ("buckets", _i32), ("aging_interval", _i32), ("pad_", _i32),
+                ("stale_threshold", _i64), ("default_exec_estimate", _i64), ("now", _i64),
+                ("hz_num", _i64), ("hz_den", _i64), ("issued_base", _i64)]
+
+
+_SIGNATURES = {
+    "kr_version": (ctypes.c_char_p, []),
+    "kr_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "kr_last_error": (ctypes.c_char_p, []),
+    "kr_launch_count": (ctypes.c_ulonglong, []),
+    "kr_horizon_confidence": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _f64, _i32,
+                                             _vp, _vp, _vp]),
+    "kr_horizon_static": (ctypes.c_int, [_i64, _i32, _i32, _vp, _vp]),
+    "kr_horizon_divergence": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _i64, _i32, _i32, _i32,
+                                             _i32, _vp, _vp, _vp, _f64, _vp, _vp, _vp]),
+    "kr_us_from_actions": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "kr_wait_ratio": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "kr_assign_bucket": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "kr_urgency": (ctypes.c_int, [ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _vp, _vp,
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "kr_workspace_bytes": (ctypes.c_size_t, [_i64]),
+    "kr_topk_select": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
+    "kr_admit": (ctypes.c_int, [_vp, _i64, _i64, _vp, ctypes.POINTER(KrFleet),
+                                ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp, _vp,
+                                ctypes.c_size_t, _vp]),
+    "kr_sort_keys": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_LIB = None
+
+
+class KairosError(RuntimeError):
+    """A C-ABI call failed (bad argument or CUDA error)."""
+
+
+def load(path: os.PathLike | None = None) -> ctypes.CDLL:
+    """Load the in-tree library; raise loudly if it has not been built."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise ImportError(
+            f"{p} is missing: the B200 decision core has no CPU fallback. Build it with "
+            "`python -m paper_2605_11381_b200.build_lib` (nvcc, sm_100a).")
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("a CUDA device (B200, sm_100a) is required: the Kairos decision core "
+                           "runs only as CUDA kernels and has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def check(status: int, what: str) -> None:
+    if status != KR_OK:
+        lib = load()
+        msg = lib.kr_status_string(status).decode()
+        detail = lib.kr_last_error().decode() if status == KR_ECUDA else ""
+        raise KairosError(f"{what}: {msg}" + (f" ({detail})" if detail else ""))
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,328 @@
+// kr_common.cuh -- device-side building blocks shared by every kernel of the
+// Kairos decision core: bit-exact fp64 numerics that reproduce the reference's
+// numpy / OpenBLAS evaluation order, integer-microsecond time arithmetic, the
+// wait ledger, the packed composite sort key, and the sm_100a PTX wrappers for
+// TMA bulk copies and mbarriers.
+//
+// Everything here is compiled with -fmad=false and uses explicit _rn
+// intrinsics, so no fp64 operation is contracted or reassociated: the fused
+// multiply-adds below exist exactly where OpenBLAS 0.3.30 (SkylakeX kernel)
+// fuses (see oracle/kairos_oracle.c for the matching CPU restatement).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/kairos_b200.h"
+
+namespace kr {
+
+constexpr int kMaxThreads = 256;
+
+// ---------------------------------------------------------------------------
+// PTX: shared-memory addresses, mbarriers, 1-D TMA bulk copies
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "KR_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra KR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Global -> shared bulk copy through the TMA engine; completion is signalled
+// as transaction bytes on `bar`.  dst, src and bytes must be 16-byte aligned.
+// The evict-first L2 policy keeps the one-pass action-chunk stream from
+// displacing the (re-read) fleet state and sort keys.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Generic-proxy accesses to shared memory must be ordered before a
+// subsequent async-proxy (TMA) write to the same buffer.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// fp64 arithmetic with explicit rounding (never contracted)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T v) { return static_cast<double>(v); }
+
+// numpy DOUBLE_pairwise_sum (numpy 2.3, loops_utils.h.src): used by
+// `u[:-1].mean(axis=0)` when N == 1 (horizon.py:125).  The
+// recursion splits at a multiple of 8 until blocks of <= 128, which are
+// reduced with 8 accumulators.
+template <class F>
+__device__ double np_pairwise_block(F a, int64_t lo, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; i++) res = dadd(res, a(lo + i));
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a(lo + j);
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = dadd(r[j], a(lo + i + j));
+    }
+    double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])),
+                      dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+    for (; i < n; i++) res = dadd(res, a(lo + i));
+    return res;
+}
+
+template <class F>
+__device__ double np_pairwise_sum(F a, int64_t lo, int64_t n) {
+    if (n <= 128) return np_pairwise_block(a, lo, n);
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return dadd(np_pairwise_sum(a, lo, n2), np_pairwise_sum(a, lo + n2, n - n2));
+}
+
+// OpenBLAS 0.3.30 ddot, contiguous, SkylakeX micro-kernel order
+// (kernel/x86_64/ddot.c + ddot_microk_skylakex-2.c): n & -16 elements through
+// 4x8-lane FMA accumulators over 32-blocks, folded to 4x4 lanes, 4x4-lane FMA
+// over remaining 16-blocks, lane chain, (a0+a2)+(a1+a3); scalar FMA tail.
+template <class FX, class FY>
+__device__ __forceinline__ double ddot_skx(FX x, FY y, int n) {
+    int n1 = n & -16, n32 = n1 & ~31, i = 0;
+    double dot = 0.0;
+    if (n1) {
+        double acc[32];
+#pragma unroll
+        for (int e = 0; e < 32; e++) acc[e] = 0.0;
+        for (; i < n32; i += 32) {
+#pragma unroll
+            for (int e = 0; e < 32; e++) acc[e] = dfma(x(i + e), y(i + e), acc[e]);
+        }
+        double a4[16];
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int l = 0; l < 4; l++) a4[4 * j + l] = dadd(acc[8 * j + l], acc[8 * j + l + 4]);
+        for (; i < n1; i += 16) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) a4[e] = dfma(x(i + e), y(i + e), a4[e]);
+        }
+        double a[4];
+#pragma unroll
+        for (int l = 0; l < 4; l++) a[l] = dadd(dadd(dadd(a4[l], a4[4 + l]), a4[8 + l]), a4[12 + l]);
+        dot = dadd(dadd(a[0], a[2]), dadd(a[1], a[3]));
+    }
+    for (; i < n; i++) dot = dfma(y(i), x(i), dot);
+    return dot;
+}
+
+// workload.py:461-468 `_cosine(a, b)` with a = candidate action, b = reference
+// action.  For D < 16 the three OpenBLAS dots are plain FMA chains, evaluated
+// in one pass so each element is loaded once.
+template <typename T>
+__device__ __forceinline__ double cosine_skx(const T* a, const T* b, int D) {
+    double xx, yy, xy;
+    if (D < 16) {
+        xx = 0.0; yy = 0.0; xy = 0.0;
+        for (int i = 0; i < D; i++) {
+            double x = to_f64(a[i]), y = to_f64(b[i]);
+            xx = dfma(x, x, xx);
+            yy = dfma(y, y, yy);
+            xy = dfma(y, x, xy);
+        }
+    } else {
+        auto fa = [a](int i) { return to_f64(a[i]); };
+        auto fb = [b](int i) { return to_f64(b[i]); };
+        xx = ddot_skx(fa, fa, D);
+        yy = ddot_skx(fb, fb, D);
+        xy = ddot_skx(fa, fb, D);
+    }
+    double na = dsqrt(xx), nb = dsqrt(yy);
+    if (na == 0.0 && nb == 0.0) return 1.0;
+    if (na == 0.0 || nb == 0.0) return 0.0;
+    return ddiv(xy, dmul(na, nb));
+}
+
+// Compile-time-D variant for the hot shapes: fully unrolled, operands held in
+// registers after one pass over shared memory.
+template <int DC, typename T>
+__device__ __forceinline__ double cosine_skx_fixed(const T* a, const T* b) {
+    double x[DC], y[DC];
+#pragma unroll
+    for (int i = 0; i < DC; i++) {
+        x[i] = to_f64(a[i]);
+        y[i] = to_f64(b[i]);
+    }
+    double xx, yy, xy;
+    if constexpr (DC < 16) {
+        xx = 0.0; yy = 0.0; xy = 0.0;
+#pragma unroll
+        for (int i = 0; i < DC; i++) {
+            xx = dfma(x[i], x[i], xx);
+            yy = dfma(y[i], y[i], yy);
+            xy = dfma(y[i], x[i], xy);
+        }
+    } else {
+        auto fx = [&](int i) { return x[i]; };
+        auto fy = [&](int i) { return y[i]; };
+        xx = ddot_skx(fx, fx, DC);
+        yy = ddot_skx(fy, fy, DC);
+        xy = ddot_skx(fx, fy, DC);
+    }
+    double na = dsqrt(xx), nb = dsqrt(yy);
+    if (na == 0.0 && nb == 0.0) return 1.0;
+    if (na == 0.0 || nb == 0.0) return 0.0;
+    return ddiv(xy, dmul(na, nb));
+}
+
+// ---------------------------------------------------------------------------
+// Integer-microsecond time (core.py:24-47)
+// ---------------------------------------------------------------------------
+// us_from_actions(count, hz_num/hz_den) = floor(count*1e6*den/num + 1/2)
+//   = (2*count*1e6*den + num) div (2*num).
+__device__ __forceinline__ int64_t us_from_actions(int64_t count, int64_t hz_num, int64_t hz_den,
+                                                   uint32_t* flag_bits) {
+    if (count < 0) {
+        *flag_bits |= KR_FLAG_TIME_RANGE;
+        return 0;
+    }
+    if (hz_den == 1 && count < (int64_t(1) << 40) && hz_num < (int64_t(1) << 40)) {
+        int64_t X = count * 1000000;
+        return (2 * X + hz_num) / (2 * hz_num);
+    }
+    unsigned __int128 X = (unsigned __int128)count * 1000000u * (unsigned __int128)hz_den;
+    unsigned __int128 Y = (unsigned __int128)hz_num;
+    unsigned __int128 q = (2 * X + Y) / (2 * Y);
+    if (q > (unsigned __int128)INT64_MAX) *flag_bits |= KR_FLAG_TIME_RANGE;
+    return (int64_t)q;
+}
+
+// ---------------------------------------------------------------------------
+// Wait ledger (waiting.py:69-93), wait ratio (waiting.py:62-66, 96-100),
+// bucket (scheduler.py:79-88)
+// ---------------------------------------------------------------------------
+struct Slot {
+    int64_t gs, ge, es, ee;
+};
+__device__ __forceinline__ Slot load_slot(const int64_t* slots, int64_t j) {
+    const longlong2* p = reinterpret_cast<const longlong2*>(slots + 4 * j);
+    longlong2 a = __ldg(p), b = __ldg(p + 1);
+    return Slot{a.x, a.y, b.x, b.y};
+}
+
+// Per round j < n_exec: gen-dominated (|G_j| >= |E_j|) rounds accrue
+// max(0, G_{j+1}.start - G_j.end) once G_{j+1} has started (n_gen > j+1, the
+// successor may still be in flight); exec-dominated rounds accrue
+// max(0, E_{j+1}.start - E_j.end) once E_{j+1} exists; the last round none.
+__device__ __forceinline__ int64_t total_wait(const int64_t* slots, int32_t n_exec,
+                                              int32_t n_gen) {
+    int64_t total = 0;
+    if (n_exec <= 0) return 0;
+    Slot cur = load_slot(slots, 0);
+    for (int32_t j = 0; j < n_exec; j++) {
+        bool has_next = (j + 1 < n_exec) || (n_gen > j + 1);
+        Slot nxt = has_next ? load_slot(slots, j + 1) : Slot{0, 0, 0, 0};
+        if (cur.ge - cur.gs >= cur.ee - cur.es) {
+            if (n_gen > j + 1) {
+                int64_t w = nxt.gs - cur.ge;
+                total += w > 0 ? w : 0;
+            }
+        } else if (j + 1 < n_exec) {
+            int64_t w = nxt.es - cur.ee;
+            total += w > 0 ? w : 0;
+        }
+        cur = nxt;
+    }
+    return total;
+}
+
+// Python `int / int` is the correctly rounded quotient; for |operands| < 2^53
+// both convert exactly and IEEE division gives the same double.
+__device__ __forceinline__ double wait_ratio(int64_t total, int64_t t_start, int64_t now,
+                                             uint32_t* flag_bits) {
+    if (now <= t_start) return 0.0;
+    int64_t life = now - t_start;
+    const int64_t lim = int64_t(1) << 53;
+    if (total >= lim || total <= -lim || life >= lim) *flag_bits |= KR_FLAG_RATIO;
+    double r = ddiv(static_cast<double>(total), static_cast<double>(life));
+    r = r > 0.0 ? r : 0.0;
+    return r < 1.0 ? r : 1.0;
+}
+
+__device__ __forceinline__ int32_t assign_bucket(double wr, int64_t skipped, int32_t B,
+                                                 int32_t A) {
+    int64_t b = static_cast<int64_t>(floor(dmul(wr, static_cast<double>(B))));
+    if (b > B - 1) b = B - 1;
+    if (skipped >= A) {
+        b = b + skipped / A;
+        if (b > B - 1) b = B - 1;
+    }
+    return static_cast<int32_t>(b);
+}
+
+// ---------------------------------------------------------------------------
+// Packed composite key (ascending order == reference order)
+//   kairos: hi = (B-1-b) << 56 | (2^56-1 - aged)      (scheduler.py:113-115,
+//           lo = (issued - base) << 24 | lexrank        buckets high -> low)
+//   fifo:   hi = issued ^ 2^63,  lo = lexrank          (scheduler.py:143-144)
+//   las:    hi = accum_gen ^ 2^63, lo = (issued - base) << 24 | lexrank
+// ---------------------------------------------------------------------------
+constexpr uint64_t kAgedMask = (uint64_t(1) << 56) - 1;
+constexpr int64_t kIssuedSpan = int64_t(1) << 40;
+constexpr int64_t kRankSpan = int64_t(1) << 24;
+
+__device__ __forceinline__ uint64_t issued_rank_word(int64_t issued, int64_t base, int32_t rank,
+                                                     uint32_t* flag_bits) {
+    int64_t d = issued - base;
+    if (d < 0 || d >= kIssuedSpan || rank < 0 || rank >= kRankSpan) *flag_bits |= KR_FLAG_KEY_RANGE;
+    return (static_cast<uint64_t>(d) << 24) | (static_cast<uint64_t>(rank) & 0xFFFFFFull);
+}
+
+__device__ __forceinline__ bool key_le(const kr_key& a, const kr_key& b) {
+    return a.hi < b.hi || (a.hi == b.hi && a.lo <= b.lo);
+}
+__device__ __forceinline__ bool key_lt(const kr_key& a, const kr_key& b) {
+    return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
+}
+
+// 128-bit logical right shift of (hi:lo) by s in [0, 127].
+__device__ __forceinline__ uint64_t shr128_lo(uint64_t hi, uint64_t lo, int s) {
+    if (s == 0) return lo;
+    if (s < 64) return (lo >> s) | (hi << (64 - s));
+    return hi >> (s - 64);
+}
+
+}  // namespace kr

@@ -1,0 +1,51 @@
+// kr_host.cuh -- host-side helpers shared by the C-ABI translation units:
+// error capture (no exceptions cross the ABI), device properties and the
+// launch-shape policy for the persistent streaming kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/kairos_b200.h"
+
+namespace kr {
+
+void set_last_error(const char* where, cudaError_t e);
+
+// Process-wide count of kernels launched by this library (diagnostic only).
+void count_launches(int n);
+
+inline int check_launch(const char* where, int launches = 1) {
+    count_launches(launches);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_last_error(where, e);
+        return KR_ECUDA;
+    }
+    return KR_OK;
+}
+
+#define KR_CUDA_TRY(expr)                                  \
+    do {                                                   \
+        cudaError_t kr_e_ = (expr);                        \
+        if (kr_e_ != cudaSuccess) {                        \
+            ::kr::set_last_error(#expr, kr_e_);            \
+            return KR_ECUDA;                               \
+        }                                                  \
+    } while (0)
+
+struct DeviceInfo {
+    int device = -1;
+    int sm_count = 0;
+    int max_smem_optin = 0;
+};
+// Properties of the current device (cached per device id).
+const DeviceInfo& device_info();
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace kr

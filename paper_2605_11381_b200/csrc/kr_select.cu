@@ -1,0 +1,746 @@
+// kr_select.cu -- step 3 of the decision core: priority ordering and top-k
+// batch admission under the edge budget (scheduler.py:130-140, 193-241).
+//
+// The reference sorts every pending request (Python `sorted`, bucket by
+// bucket) and slices the first k = capacity - in_flight as the edge batch.  On
+// the device the order is the ascending order of unique 128-bit keys
+// (kr_urgency), so admission is:
+//   1. MSD radix select of the k-th smallest key: each level histograms an
+//      11-bit digit taken just below the highest bit on which the surviving
+//      candidates still differ (OR ^ AND of the set), keeps only the boundary
+//      bin, and stops when the boundary bin holds one key.  Two grid-wide levels
+//      shrink 2^20 keys to a handful; one CTA finishes.
+//   2. One elementwise admission pass (key <= kth): admitted / refetch masks,
+//      skip counters (scheduler.py:223-234) and a gather of the k admitted
+//      (key, index) pairs.
+//   3. A sort of only those k pairs (single-CTA bitonic network in shared
+//      memory for k <= 8192, otherwise a stable multi-CTA LSD radix sort over
+//      the differing key bits), giving S_e in reference order.
+// Keys are unique (the lexrank tiebreak), so every step is deterministic.
+#include <climits>
+
+#include "kr_common.cuh"
+#include "kr_host.cuh"
+
+namespace kr {
+
+constexpr int kDigitBits = 11;
+constexpr int kBins = 1 << kDigitBits;
+constexpr int kBitonicMax = 8192;
+constexpr int kSortTile = 2048;  // LSD radix: elements per CTA tile (256 threads x 8)
+
+struct SelState {
+    unsigned long long st[2][4];  // [parity] {or_hi, or_lo, and_hi, and_lo}
+    unsigned int cnt[2];          // [parity] candidate count
+    long long need;               // 1-based rank of the target within candidates
+    unsigned int dstar;
+    unsigned int dcount;          // population of the boundary bin
+    int done;
+    int pad_;
+    kr_key kth;
+    unsigned int sel_count;       // admission gather count
+    unsigned int pad2_[3];
+    unsigned long long sst[4];    // OR/AND of the gathered (admitted) keys
+    unsigned int hist[kBins];
+};
+
+struct Workspace {
+    SelState* state;
+    kr_key* cand[2];
+    kr_key* skeys[2];
+    int32_t* sidx[2];
+    uint32_t* tile_hist;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static size_t sort_tiles(int64_t n) { return static_cast<size_t>((n + kSortTile - 1) / kSortTile); }
+
+static size_t workspace_bytes(int64_t n) {
+    size_t nn = static_cast<size_t>(n < 1 ? 1 : n);
+    size_t b = align256(sizeof(SelState));
+    b += 2 * align256(nn * sizeof(kr_key));      // select candidates
+    b += 2 * align256(nn * sizeof(kr_key));      // sort keys ping-pong
+    b += 2 * align256(nn * sizeof(int32_t));     // sort index ping-pong
+    b += align256(sort_tiles(n) * 256 * sizeof(uint32_t));
+    return b;
+}
+
+static Workspace carve(void* ws, int64_t n) {
+    size_t nn = static_cast<size_t>(n < 1 ? 1 : n);
+    unsigned char* p = static_cast<unsigned char*>(ws);
+    Workspace w;
+    w.state = reinterpret_cast<SelState*>(p);
+    p += align256(sizeof(SelState));
+    for (int i = 0; i < 2; i++) {
+        w.cand[i] = reinterpret_cast<kr_key*>(p);
+        p += align256(nn * sizeof(kr_key));
+    }
+    for (int i = 0; i < 2; i++) {
+        w.skeys[i] = reinterpret_cast<kr_key*>(p);
+        p += align256(nn * sizeof(kr_key));
+    }
+    for (int i = 0; i < 2; i++) {
+        w.sidx[i] = reinterpret_cast<int32_t*>(p);
+        p += align256(nn * sizeof(int32_t));
+    }
+    w.tile_hist = reinterpret_cast<uint32_t*>(p);
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+// block-level helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long warp_or(unsigned long long v) {
+    for (int o = 16; o; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_and(unsigned long long v) {
+    for (int o = 16; o; o >>= 1) v &= __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// OR / AND of keys, reduced per warp then atomically into dst[4].
+__device__ __forceinline__ void stats_accumulate(unsigned long long* dst, unsigned long long ohi,
+                                                 unsigned long long olo, unsigned long long ahi,
+                                                 unsigned long long alo) {
+    ohi = warp_or(ohi);
+    olo = warp_or(olo);
+    ahi = warp_and(ahi);
+    alo = warp_and(alo);
+    if ((threadIdx.x & 31) == 0) {
+        if (ohi) atomicOr(&dst[0], ohi);
+        if (olo) atomicOr(&dst[1], olo);
+        if (~ahi) atomicAnd(&dst[2], ahi);
+        if (~alo) atomicAnd(&dst[3], alo);
+    }
+}
+
+// Digit window just below the highest differing bit of the candidate set.
+struct Digit {
+    int shift, width;
+    bool any;
+};
+__device__ __forceinline__ Digit digit_of(const unsigned long long* s) {
+    unsigned long long xh = s[0] ^ s[2], xl = s[1] ^ s[3];
+    Digit d;
+    int h;
+    if (xh) h = 127 - __clzll(xh);
+    else if (xl) h = 63 - __clzll(xl);
+    else h = -1;
+    d.any = h >= 0;
+    d.width = h + 1 < kDigitBits ? h + 1 : kDigitBits;
+    d.shift = h - d.width + 1;
+    if (!d.any) { d.width = 1; d.shift = 0; }
+    return d;
+}
+__device__ __forceinline__ unsigned digit_val(const kr_key& k, const Digit& d) {
+    return static_cast<unsigned>(shr128_lo(k.hi, k.lo, d.shift) & ((1ull << d.width) - 1));
+}
+
+// ---------------------------------------------------------------------------
+// radix select
+// ---------------------------------------------------------------------------
+__global__ void k_sel_reset(SelState* s, int64_t n, int64_t k) {
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) s->hist[i] = 0;
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < 2; p++) {
+            s->st[p][0] = 0; s->st[p][1] = 0; s->st[p][2] = ~0ull; s->st[p][3] = ~0ull;
+        }
+        s->sst[0] = 0; s->sst[1] = 0; s->sst[2] = ~0ull; s->sst[3] = ~0ull;
+        s->cnt[0] = static_cast<unsigned>(n);
+        s->cnt[1] = 0;
+        s->need = k;
+        s->done = 0;
+        s->sel_count = 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sel_stats(const kr_key* __restrict__ keys, int64_t n,
+                                                   SelState* s) {
+    unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        kr_key k = keys[i];
+        oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
+    }
+    stats_accumulate(s->st[0], oh, ol, ah, al);
+}
+
+// level L reads candidates src (count cnt[L&1]) and histograms their digit.
+__global__ void __launch_bounds__(256) k_sel_hist(const kr_key* __restrict__ src, SelState* s,
+                                                  int level) {
+    __shared__ unsigned int h[kBins];
+    if (s->done) return;
+    const int p = level & 1;
+    Digit d = digit_of(s->st[p]);
+    const int64_t n = s->cnt[p];
+    const int bins = 1 << d.width;
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        atomicAdd(&h[digit_val(src[i], d)], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < bins; i += blockDim.x)
+        if (h[i]) atomicAdd(&s->hist[i], h[i]);
+}
+
+// One block: choose the boundary bin d* (cum_lt < need <= cum_le).
+__device__ void sel_pick_block(SelState* s, int level, const unsigned int* hist,
+                               const kr_key* src) {
+    __shared__ unsigned int part[1024];
+    __shared__ int found;
+    const int p = level & 1;
+    Digit d = digit_of(s->st[p]);
+    if (!d.any) {  // all candidates identical: unique keys => a single one
+        if (threadIdx.x == 0) {
+            s->kth = src[0];
+            s->done = 1;
+        }
+        return;
+    }
+    const int bins = 1 << d.width;
+    const int per = (bins + blockDim.x - 1) / blockDim.x;
+    unsigned int local = 0;
+    for (int q = 0; q < per; q++) {
+        int b = threadIdx.x * per + q;
+        if (b < bins) local += hist[b];
+    }
+    part[threadIdx.x] = local;
+    if (threadIdx.x == 0) found = 0;
+    __syncthreads();
+    // inclusive scan of part[] (Hillis-Steele)
+    for (int o = 1; o < blockDim.x; o <<= 1) {
+        unsigned int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    const long long need = s->need;
+    unsigned long long before = threadIdx.x ? part[threadIdx.x - 1] : 0;
+    if (static_cast<long long>(before) < need && need <= static_cast<long long>(part[threadIdx.x])) {
+        unsigned long long cum = before;
+        for (int q = 0; q < per; q++) {
+            int b = threadIdx.x * per + q;
+            if (b >= bins) break;
+            unsigned int c = hist[b];
+            if (static_cast<long long>(cum) < need && need <= static_cast<long long>(cum + c)) {
+                s->dstar = static_cast<unsigned>(b);
+                s->dcount = c;
+                s->need = need - static_cast<long long>(cum);
+                found = 1;
+                break;
+            }
+            cum += c;
+        }
+    }
+    __syncthreads();
+    (void)found;
+}
+
+__global__ void __launch_bounds__(1024) k_sel_pick(SelState* s, const kr_key* src, int level) {
+    if (s->done) return;
+    sel_pick_block(s, level, s->hist, src);
+    __syncthreads();
+    // reset for the next level
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) s->hist[i] = 0;
+    if (threadIdx.x == 0) {
+        const int q = (level + 1) & 1;
+        s->st[q][0] = 0; s->st[q][1] = 0; s->st[q][2] = ~0ull; s->st[q][3] = ~0ull;
+        s->cnt[q] = 0;
+    }
+}
+
+// Keep the boundary bin; if it holds one key that key is the answer.
+__global__ void __launch_bounds__(256) k_sel_scatter(const kr_key* __restrict__ src, kr_key* dst,
+                                                     SelState* s, int level) {
+    if (s->done) return;
+    const int p = level & 1, q = (level + 1) & 1;
+    Digit d = digit_of(s->st[p]);
+    const int64_t n = s->cnt[p];
+    const unsigned dstar = s->dstar;
+    const bool single = s->dcount == 1;
+    unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n; base += stride) {
+        int64_t i = base + threadIdx.x;
+        bool keep = false;
+        kr_key k{0, 0};
+        if (i < n) {
+            k = src[i];
+            keep = digit_val(k, d) == dstar;
+        }
+        if (single) {
+            if (keep) {
+                s->kth = k;
+                s->done = 1;
+            }
+            continue;
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, keep);
+        unsigned pos = 0;
+        if (mask) {
+            int lane = threadIdx.x & 31;
+            int leader = __ffs(mask) - 1;
+            unsigned basepos = 0;
+            if (lane == leader) basepos = atomicAdd(&s->cnt[q], __popc(mask));
+            basepos = __shfl_sync(0xffffffffu, basepos, leader);
+            pos = basepos + __popc(mask & ((1u << lane) - 1));
+        }
+        if (keep) {
+            dst[pos] = k;
+            oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
+        }
+    }
+    if (!single) stats_accumulate(s->st[q], oh, ol, ah, al);
+}
+
+// Single CTA: remaining levels over global ping-pong buffers.
+__global__ void __launch_bounds__(1024) k_sel_finish(SelState* s, kr_key* bufA, kr_key* bufB,
+                                                     int level) {
+    __shared__ unsigned int h[kBins];
+    __shared__ unsigned long long sst[4];
+    __shared__ unsigned int scnt;
+    if (s->done) return;
+    // bufA holds the candidates of `level` (the last grid-wide scatter's output)
+    kr_key* src = bufA;
+    kr_key* dst = bufB;
+    int p = level & 1;
+    for (int it = 0; it < 130; it++) {
+        const unsigned n = s->cnt[p];
+        Digit d = digit_of(s->st[p]);
+        if (!d.any || n <= 1) {
+            if (threadIdx.x == 0) {
+                s->kth = src[0];
+                s->done = 1;
+            }
+            return;
+        }
+        const int bins = 1 << d.width;
+        for (int i = threadIdx.x; i < bins; i += blockDim.x) h[i] = 0;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&h[digit_val(src[i], d)], 1u);
+        __syncthreads();
+        sel_pick_block(s, p, h, src);
+        __syncthreads();
+        const unsigned dstar = s->dstar;
+        const bool single = s->dcount == 1;
+        if (threadIdx.x < 4) sst[threadIdx.x] = threadIdx.x < 2 ? 0ull : ~0ull;
+        if (threadIdx.x == 0) scnt = 0;
+        __syncthreads();
+        unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+        for (unsigned base = 0; base < n; base += blockDim.x) {
+            unsigned i = base + threadIdx.x;
+            bool keep = false;
+            kr_key k{0, 0};
+            if (i < n) {
+                k = src[i];
+                keep = digit_val(k, d) == dstar;
+            }
+            if (single) {
+                if (keep) {
+                    s->kth = k;
+                    s->done = 1;
+                }
+                continue;
+            }
+            unsigned mask = __ballot_sync(0xffffffffu, keep);
+            unsigned pos = 0;
+            if (mask) {
+                int lane = threadIdx.x & 31;
+                int leader = __ffs(mask) - 1;
+                unsigned bp = 0;
+                if (lane == leader) bp = atomicAdd(&scnt, __popc(mask));
+                bp = __shfl_sync(0xffffffffu, bp, leader);
+                pos = bp + __popc(mask & ((1u << lane) - 1));
+            }
+            if (keep) {
+                dst[pos] = k;
+                oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
+            }
+        }
+        if (single) return;
+        oh = warp_or(oh); ol = warp_or(ol); ah = warp_and(ah); al = warp_and(al);
+        if ((threadIdx.x & 31) == 0) {
+            atomicOr(&sst[0], oh); atomicOr(&sst[1], ol);
+            atomicAnd(&sst[2], ah); atomicAnd(&sst[3], al);
+        }
+        __syncthreads();
+        const int q = p ^ 1;
+        if (threadIdx.x == 0) {
+            s->st[q][0] = sst[0]; s->st[q][1] = sst[1]; s->st[q][2] = sst[2]; s->st[q][3] = sst[3];
+            s->cnt[q] = scnt;
+        }
+        __syncthreads();
+        p = q;
+        kr_key* t = src; src = dst; dst = t;
+    }
+}
+
+__global__ void k_set_key(kr_key* dst, unsigned long long hi, unsigned long long lo) {
+    dst->hi = hi;
+    dst->lo = lo;
+}
+__global__ void k_copy_kth(const SelState* s, kr_key* dst) { *dst = s->kth; }
+
+// ---------------------------------------------------------------------------
+// admission pass (scheduler.py:204-207, 223-234)
+// ---------------------------------------------------------------------------
+struct AdmitArgs {
+    const kr_key* keys;
+    int64_t n;
+    int all;   // k >= n
+    int none;  // k == 0
+    const kr_key* kth;
+    const int64_t* obs;     // nullable
+    int32_t* skipped;       // nullable
+    uint8_t* admitted;      // nullable
+    uint8_t* refetch;       // nullable
+    int64_t now, stale;
+    kr_key* sel_keys;       // nullable (gather)
+    int32_t* sel_idx;
+    SelState* s;
+};
+
+__global__ void k_admit_init(SelState* s) {
+    if (threadIdx.x == 0) {
+        s->sel_count = 0;
+        s->sst[0] = 0; s->sst[1] = 0; s->sst[2] = ~0ull; s->sst[3] = ~0ull;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_admit(AdmitArgs a) {
+    kr_key kth{~0ull, ~0ull};
+    if (!a.all && !a.none) kth = *a.kth;
+    unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < a.n; base += stride) {
+        int64_t i = base + threadIdx.x;
+        bool in = false;
+        kr_key k{0, 0};
+        if (i < a.n) {
+            k = a.keys[i];
+            in = !a.none && (a.all || key_le(k, kth));
+            if (a.admitted) a.admitted[i] = in;
+            if (a.refetch) a.refetch[i] = in && (a.now - __ldg(a.obs + i) > a.stale);
+            if (a.skipped) a.skipped[i] = in ? 0 : a.skipped[i] + 1;
+        }
+        if (a.sel_keys) {
+            unsigned mask = __ballot_sync(0xffffffffu, in);
+            if (mask) {
+                int lane = threadIdx.x & 31;
+                int leader = __ffs(mask) - 1;
+                unsigned bp = 0;
+                if (lane == leader) bp = atomicAdd(&a.s->sel_count, __popc(mask));
+                bp = __shfl_sync(0xffffffffu, bp, leader);
+                if (in) {
+                    unsigned pos = bp + __popc(mask & ((1u << lane) - 1));
+                    a.sel_keys[pos] = k;
+                    a.sel_idx[pos] = static_cast<int32_t>(i);
+                    oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
+                }
+            }
+        }
+    }
+    if (a.sel_keys) stats_accumulate(a.s->sst, oh, ol, ah, al);
+}
+
+// ---------------------------------------------------------------------------
+// sorting the admitted set
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool pair_gt(const kr_key& a, int32_t ia, const kr_key& b, int32_t ib) {
+    if (a.hi != b.hi) return a.hi > b.hi;
+    if (a.lo != b.lo) return a.lo > b.lo;
+    return ia > ib;
+}
+
+// Single-CTA bitonic network over (key, idx), n <= kBitonicMax.
+__global__ void __launch_bounds__(1024) k_bitonic(const kr_key* keys, const int32_t* idx,
+                                                  const unsigned int* count_dev, int64_t count_host,
+                                                  int32_t* out_idx, kr_key* out_keys) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = count_dev ? static_cast<int>(*count_dev) : static_cast<int>(count_host);
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    kr_key* sk = reinterpret_cast<kr_key*>(smem);
+    int32_t* si = reinterpret_cast<int32_t*>(smem + sizeof(kr_key) * kBitonicMax);
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        if (i < n) {
+            sk[i] = keys[i];
+            si[i] = idx ? idx[i] : i;
+        } else {
+            sk[i] = kr_key{~0ull, ~0ull};
+            si[i] = INT_MAX;
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= np2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int pidx = threadIdx.x; pidx < np2 / 2; pidx += blockDim.x) {
+                int i = (pidx / j) * 2 * j + (pidx % j);
+                int l = i + j;
+                bool up = (i & k) == 0;
+                kr_key ka = sk[i], kb = sk[l];
+                int32_t ia = si[i], ib = si[l];
+                bool gt = pair_gt(ka, ia, kb, ib);
+                if (gt == up) {
+                    sk[i] = kb; sk[l] = ka;
+                    si[i] = ib; si[l] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (out_idx) out_idx[i] = si[i];
+        if (out_keys) out_keys[i] = sk[i];
+    }
+}
+
+// --- stable multi-CTA LSD radix sort over 8-bit windows ---------------------
+__global__ void __launch_bounds__(256) k_rs_hist(const kr_key* keys, int64_t n, int shift,
+                                                 int width, uint32_t* tile_hist, int64_t ntiles) {
+    __shared__ unsigned int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t t = blockIdx.x;
+    const int64_t lo = t * kSortTile, hi = lo + kSortTile < n ? lo + kSortTile : n;
+    const unsigned mask = (1u << width) - 1;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        kr_key k = keys[i];
+        atomicAdd(&h[shr128_lo(k.hi, k.lo, shift) & mask], 1u);
+    }
+    __syncthreads();
+    tile_hist[static_cast<int64_t>(threadIdx.x) * ntiles + t] = h[threadIdx.x];
+}
+
+// Exclusive scan of m entries in place, one CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* a, int64_t m) {
+    __shared__ unsigned int part[1024];
+    const int64_t per = (m + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = threadIdx.x * per, hi = lo + per < m ? lo + per : m;
+    unsigned int s = 0;
+    for (int64_t i = lo; i < hi; i++) s += a[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < blockDim.x; o <<= 1) {
+        unsigned int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    unsigned int run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+    for (int64_t i = lo; i < hi; i++) {
+        unsigned int v = a[i];
+        a[i] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rs_scatter(const kr_key* keys, const int32_t* idx,
+                                                    int64_t n, int shift, int width,
+                                                    const uint32_t* tile_off, int64_t ntiles,
+                                                    kr_key* okeys, int32_t* oidx) {
+    __shared__ unsigned int wc[8][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = blockIdx.x;
+    const int64_t lo = t * kSortTile;
+    const int per_warp = kSortTile / 8;
+    const int64_t wlo = lo + warp * per_warp;
+    const unsigned mask = (1u << width) - 1;
+    for (int d = lane; d < 256; d += 32) wc[warp][d] = 0;
+    __syncwarp();
+    for (int c = 0; c < per_warp; c += 32) {
+        int64_t i = wlo + c + lane;
+        if (i < n) {
+            kr_key k = keys[i];
+            atomicAdd(&wc[warp][shr128_lo(k.hi, k.lo, shift) & mask], 1u);
+        }
+    }
+    __syncthreads();
+    {
+        unsigned int d = threadIdx.x, run = 0;
+        for (int w = 0; w < 8; w++) {
+            unsigned int v = wc[w][d];
+            wc[w][d] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    for (int c = 0; c < per_warp; c += 32) {
+        int64_t i = wlo + c + lane;
+        bool valid = i < n;
+        kr_key k{0, 0};
+        unsigned d = 0xFFFFFFFFu;
+        if (valid) {
+            k = keys[i];
+            d = static_cast<unsigned>(shr128_lo(k.hi, k.lo, shift) & mask);
+        }
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned rank = __popc(peers & ((1u << lane) - 1));
+        unsigned basew = valid ? wc[warp][d] : 0;
+        __syncwarp();
+        if (valid) {
+            unsigned pos = tile_off[static_cast<int64_t>(d) * ntiles + t] + basew + rank;
+            okeys[pos] = k;
+            oidx[pos] = idx ? idx[i] : static_cast<int32_t>(i);
+            if (rank == 0) wc[warp][d] += __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+// Sorts (keys, idx) with n elements (keys/idx may alias workspace buffer 0).
+static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx,
+                      const unsigned int* count_dev, int64_t n, int32_t* out_idx, kr_key* out_keys,
+                      const unsigned long long* stats_dev, cudaStream_t st) {
+    if (n <= kBitonicMax) {
+        size_t smem = static_cast<size_t>(kBitonicMax) * (sizeof(kr_key) + sizeof(int32_t));
+        KR_CUDA_TRY(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+        k_bitonic<<<1, 1024, smem, st>>>(keys, idx, count_dev, n, out_idx, out_keys);
+        return check_launch("k_bitonic");
+    }
+    // window plan from OR ^ AND of the set (read back: one stream sync)
+    unsigned long long s4[4];
+    KR_CUDA_TRY(cudaMemcpyAsync(s4, stats_dev, sizeof(s4), cudaMemcpyDeviceToHost, st));
+    KR_CUDA_TRY(cudaStreamSynchronize(st));
+    unsigned long long x[2] = {s4[1] ^ s4[3], s4[0] ^ s4[2]};  // lo, hi
+    int shifts[32], widths[32], np = 0;
+    for (int b = 0; b < 128;) {
+        bool set = (x[b >> 6] >> (b & 63)) & 1ull;
+        if (!set) { b++; continue; }
+        shifts[np] = b;
+        widths[np] = 128 - b < 8 ? 128 - b : 8;
+        np++;
+        b += 8;
+    }
+    const int64_t ntiles = static_cast<int64_t>(sort_tiles(n));
+    const kr_key* ck = keys;
+    const int32_t* ci = idx;
+    if (np == 0) {  // all keys identical: one stable pass yields the identity order
+        shifts[0] = 0;
+        widths[0] = 8;
+        np = 1;
+    }
+    for (int p = 0; p < np; p++) {
+        kr_key* ok = w.skeys[p & 1];
+        int32_t* oi = w.sidx[p & 1];
+        if (ck == ok) { ok = w.skeys[(p + 1) & 1]; oi = w.sidx[(p + 1) & 1]; }
+        k_rs_hist<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(ck, n, shifts[p], widths[p],
+                                                                 w.tile_hist, ntiles);
+        k_rs_scan<<<1, 1024, 0, st>>>(w.tile_hist, ntiles * 256);
+        k_rs_scatter<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(
+            ck, ci, n, shifts[p], widths[p], w.tile_hist, ntiles, ok, oi);
+        int e = check_launch("radix pass", 3);
+        if (e) return e;
+        ck = ok;
+        ci = oi;
+    }
+    if (out_idx) {
+        if (ci)
+            KR_CUDA_TRY(cudaMemcpyAsync(out_idx, ci, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        else
+            return KR_EINVAL;
+    }
+    if (out_keys)
+        KR_CUDA_TRY(cudaMemcpyAsync(out_keys, ck, n * sizeof(kr_key), cudaMemcpyDeviceToDevice, st));
+    return KR_OK;
+}
+
+static unsigned grid_stream(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    int64_t cap = static_cast<int64_t>(device_info().sm_count) * 8;
+    if (b > cap) b = cap;
+    return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+}  // namespace kr
+
+using namespace kr;
+
+extern "C" size_t kr_workspace_bytes(int64_t n) { return workspace_bytes(n); }
+
+extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth, void* ws,
+                              size_t ws_bytes, void* stream) {
+    if (n < 0 || k < 0 || !kth) return KR_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    if (k == 0 || n == 0) return KR_OK;
+    if (k >= n) {
+        k_set_key<<<1, 1, 0, st>>>(kth, ~0ull, ~0ull);
+        return check_launch("kr_topk_select");
+    }
+    if (!ws || ws_bytes < workspace_bytes(n) || !keys) return KR_ENOSPACE;
+    Workspace w = carve(ws, n);
+    SelState* s = w.state;
+    k_sel_reset<<<1, 1024, 0, st>>>(s, n, k);
+    k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, s);
+    // level 0: all keys -> cand[0]; level 1: cand[0] -> cand[1]; finisher reads cand[1]
+    k_sel_hist<<<grid_stream(n), 256, 0, st>>>(keys, s, 0);
+    k_sel_pick<<<1, 1024, 0, st>>>(s, keys, 0);
+    k_sel_scatter<<<grid_stream(n), 256, 0, st>>>(keys, w.cand[0], s, 0);
+    k_sel_hist<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], s, 1);
+    k_sel_pick<<<1, 1024, 0, st>>>(s, w.cand[0], 1);
+    k_sel_scatter<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], w.cand[1], s, 1);
+    // finisher: level 2 reads parity 0 buffer == cand[1] (see k_sel_finish)
+    k_sel_finish<<<1, 1024, 0, st>>>(s, w.cand[1], w.cand[0], 2);
+    k_copy_kth<<<1, 1, 0, st>>>(s, kth);
+    return check_launch("kr_topk_select", 10);
+}
+
+extern "C" int kr_admit(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
+                        const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted,
+                        uint8_t* refetch, int32_t* edge_idx, kr_key* edge_keys, void* ws,
+                        size_t ws_bytes, void* stream) {
+    if (n < 0 || k < 0) return KR_EINVAL;
+    if (n == 0) return KR_OK;
+    if (!keys) return KR_EINVAL;
+    if ((refetch || (fleet && fleet->skipped)) && (!fleet || !cfg)) return KR_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    const bool gather = edge_idx || edge_keys;
+    Workspace w{};
+    if (gather) {
+        if (!ws || ws_bytes < workspace_bytes(n)) return KR_ENOSPACE;
+        w = carve(ws, n);
+        k_admit_init<<<1, 32, 0, st>>>(w.state);
+    }
+    AdmitArgs a{};
+    a.keys = keys;
+    a.n = n;
+    a.all = kth == nullptr;
+    a.none = k == 0;
+    a.kth = kth;
+    a.obs = fleet ? fleet->obs_captured_at : nullptr;
+    a.skipped = fleet ? fleet->skipped : nullptr;
+    a.admitted = admitted;
+    a.refetch = refetch;
+    a.now = cfg ? cfg->now : 0;
+    a.stale = cfg ? cfg->stale_threshold : 0;
+    a.sel_keys = gather ? w.skeys[0] : nullptr;
+    a.sel_idx = gather ? w.sidx[0] : nullptr;
+    a.s = w.state;
+    k_admit<<<grid_stream(n), 256, 0, st>>>(a);
+    int e = check_launch("k_admit", gather ? 2 : 1);
+    if (e || !gather) return e;
+    const int64_t m = k < n ? k : n;
+    if (m == 0) return KR_OK;
+    return sort_pairs(w, w.skeys[0], w.sidx[0], m <= kBitonicMax ? &w.state->sel_count : nullptr,
+                      m, edge_idx, edge_keys, w.state->sst, st);
+}
+
+extern "C" int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_key* sorted_keys,
+                            void* ws, size_t ws_bytes, void* stream) {
+    if (n < 0) return KR_EINVAL;
+    if (n == 0) return KR_OK;
+    if (!keys || !ws || ws_bytes < workspace_bytes(n)) return KR_ENOSPACE;
+    cudaStream_t st = as_stream(stream);
+    Workspace w = carve(ws, n);
+    if (n <= kBitonicMax)
+        return sort_pairs(w, keys, nullptr, nullptr, n, order, sorted_keys, nullptr, st);
+    k_sel_reset<<<1, 1024, 0, st>>>(w.state, n, 0);
+    k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, w.state);
+    int e = check_launch("kr_sort_keys", 2);
+    if (e) return e;
+    return sort_pairs(w, keys, nullptr, nullptr, n, order, sorted_keys, w.state->st[0], st);
+}

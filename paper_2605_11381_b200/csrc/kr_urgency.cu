@@ -1,0 +1,184 @@
+// kr_urgency.cu -- step 2 of the decision core: execution-aware urgency.
+//
+// One fused elementwise pass per pending request (thread per request):
+//   ledger_from_history   waiting.py:69-93  (CSR history slots, in-flight successor)
+//   current_wait_ratio    waiting.py:96-100, 62-66
+//   assign_bucket         scheduler.py:79-88 (wait-ratio bucket + skip aging)
+//   estimate_exec_latency scheduler.py:91-104 (last execution length = projected
+//                         execution duration of the next round)
+//   aged estimate + order scheduler.py:113-115, 130-140 (packed 128-bit key)
+//   next-need time        core.py:157-166 exec_end_from_piggyback: issue time plus
+//                         the remaining actions at the control rate
+// Integer-µs everywhere except the wait ratio (one fp64 division, correctly
+// rounded like Python's int / int) and its bucket multiply.
+#include "kr_common.cuh"
+#include "kr_host.cuh"
+
+namespace kr {
+
+__global__ void k_us_from_actions(const int64_t* count, const int64_t* base, int64_t n,
+                                  int64_t hz_num, int64_t hz_den, int64_t* out, uint32_t* flags) {
+    uint32_t fl = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t us = us_from_actions(count[i], hz_num, hz_den, &fl);
+        out[i] = (base ? base[i] : 0) + us;
+    }
+    if (fl && flags) atomicOr(flags, fl);
+}
+
+__global__ void k_wait_ratio(const int64_t* total, const int64_t* t_start, int64_t n, int64_t now,
+                             double* wr, uint32_t* flags) {
+    uint32_t fl = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        wr[i] = wait_ratio(total[i], t_start[i], now, &fl);
+    if (fl && flags) atomicOr(flags, fl);
+}
+
+__global__ void k_assign_bucket(const double* wr, const int32_t* skipped, int64_t n, int32_t B,
+                                int32_t A, int32_t* bucket) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        bucket[i] = assign_bucket(wr[i], skipped[i], B, A);
+}
+
+struct UrgencyOut {
+    kr_key* keys;
+    int64_t* need_time;
+    int64_t* total_wait;
+    double* wr;
+    int32_t* bucket;
+    int64_t* est;
+    int64_t* slot_wait;
+    uint32_t* flags;
+};
+
+// Per-round waits of one request (WaitLedger.waits), -1 where none recorded.
+__device__ __forceinline__ void slot_waits(const int64_t* slots, int32_t n_exec, int32_t n_gen,
+                                           int64_t* out) {
+    for (int32_t j = 0; j < n_exec; j++) {
+        Slot cur = load_slot(slots, j);
+        int64_t w = -1;
+        if (cur.ge - cur.gs >= cur.ee - cur.es) {
+            if (n_gen > j + 1) {
+                w = load_slot(slots, j + 1).gs - cur.ge;
+                w = w > 0 ? w : 0;
+            }
+        } else if (j + 1 < n_exec) {
+            w = load_slot(slots, j + 1).es - cur.ee;
+            w = w > 0 ? w : 0;
+        }
+        out[j] = w;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_urgency(kr_fleet f, kr_sched c, UrgencyOut o) {
+    uint32_t fl = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < f.n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t issued = __ldg(f.issued_at + i);
+        const int32_t rank = __ldg(f.lexrank + i);
+        if (o.need_time) {
+            int32_t rem = __ldg(f.remaining + i);
+            o.need_time[i] = issued + us_from_actions(rem, c.hz_num, c.hz_den, &fl);
+        }
+        kr_key key;
+        if (c.policy == KR_FIFO) {
+            key.hi = static_cast<uint64_t>(issued) ^ (uint64_t(1) << 63);
+            key.lo = static_cast<uint64_t>(static_cast<uint32_t>(rank));
+            if (rank < 0) fl |= KR_FLAG_KEY_RANGE;
+        } else if (c.policy == KR_LAS) {
+            key.hi = static_cast<uint64_t>(__ldg(f.accum_gen + i)) ^ (uint64_t(1) << 63);
+            key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
+        }
+        const bool need_hist =
+            c.policy == KR_KAIROS || o.total_wait || o.wr || o.bucket || o.est || o.slot_wait;
+        if (need_hist) {
+            const int64_t* slots = f.slots + 4 * __ldg(f.hist_off + i);
+            const int32_t ne = __ldg(f.n_exec + i), ng = __ldg(f.n_gen + i);
+            const int32_t skipped = f.skipped[i];
+            int64_t w = total_wait(slots, ne, ng);
+            double wr = wait_ratio(w, __ldg(f.t_start + i), c.now, &fl);
+            int32_t b = assign_bucket(wr, skipped, c.buckets, c.aging_interval);
+            int64_t est = c.default_exec_estimate;
+            if (ne > 0) {
+                Slot last = load_slot(slots, ne - 1);
+                est = last.ee - last.es;
+            }
+            if (o.total_wait) o.total_wait[i] = w;
+            if (o.wr) o.wr[i] = wr;
+            if (o.bucket) o.bucket[i] = b;
+            if (o.est) o.est[i] = est;
+            if (o.slot_wait) slot_waits(slots, ne, ng, o.slot_wait + __ldg(f.hist_off + i));
+            if (c.policy == KR_KAIROS) {
+                // aged = est * (1 + skipped), descending -> stored complemented
+                unsigned __int128 aged = static_cast<unsigned __int128>(est < 0 ? 0 : est) *
+                                         static_cast<unsigned __int128>(1 + (int64_t)skipped);
+                if (est < 0 || skipped < 0 || aged > kAgedMask) fl |= KR_FLAG_KEY_RANGE;
+                uint64_t a = aged > kAgedMask ? kAgedMask : static_cast<uint64_t>(aged);
+                key.hi = (static_cast<uint64_t>(c.buckets - 1 - b) << 56) | (kAgedMask - a);
+                key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
+            }
+        }
+        o.keys[i] = key;
+    }
+    if (fl && o.flags) atomicOr(o.flags, fl);
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    int64_t cap = static_cast<int64_t>(device_info().sm_count) * 8;
+    if (b > cap) b = cap;
+    return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+}  // namespace kr
+
+using namespace kr;
+
+extern "C" int kr_us_from_actions(const int64_t* count, const int64_t* base, int64_t n,
+                                  int64_t hz_num, int64_t hz_den, int64_t* out, uint32_t* flags,
+                                  void* stream) {
+    if (n < 0 || hz_num <= 0 || hz_den <= 0) return KR_EINVAL;
+    if (n == 0) return KR_OK;
+    if (!count || !out) return KR_EINVAL;
+    k_us_from_actions<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(count, base, n, hz_num,
+                                                                        hz_den, out, flags);
+    return check_launch("kr_us_from_actions");
+}
+
+extern "C" int kr_wait_ratio(const int64_t* total_wait, const int64_t* t_start, int64_t n,
+                             int64_t now, double* wr, uint32_t* flags, void* stream) {
+    if (n < 0) return KR_EINVAL;
+    if (n == 0) return KR_OK;
+    if (!total_wait || !t_start || !wr) return KR_EINVAL;
+    k_wait_ratio<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(total_wait, t_start, n, now, wr,
+                                                                   flags);
+    return check_launch("kr_wait_ratio");
+}
+
+extern "C" int kr_assign_bucket(const double* wr, const int32_t* skipped, int64_t n,
+                                int32_t buckets, int32_t aging_interval, int32_t* bucket,
+                                void* stream) {
+    if (n < 0 || buckets < 1 || aging_interval < 1) return KR_EINVAL;
+    if (n == 0) return KR_OK;
+    if (!wr || !skipped || !bucket) return KR_EINVAL;
+    k_assign_bucket<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(wr, skipped, n, buckets,
+                                                                      aging_interval, bucket);
+    return check_launch("kr_assign_bucket");
+}
+
+extern "C" int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys,
+                          int64_t* need_time, int64_t* total_wait, double* wr, int32_t* bucket,
+                          int64_t* est, int64_t* slot_wait, uint32_t* flags, void* stream) {
+    if (!fleet || !cfg || fleet->n < 0) return KR_EINVAL;
+    if (cfg->policy < KR_KAIROS || cfg->policy > KR_LAS || cfg->buckets < 1 ||
+        cfg->buckets > 256 || cfg->aging_interval < 1 || cfg->hz_num <= 0 || cfg->hz_den <= 0)
+        return KR_EINVAL;
+    if (fleet->n == 0) return KR_OK;
+    if (!keys) return KR_EINVAL;
+    UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, slot_wait, flags};
+    k_urgency<<<grid_for(fleet->n, 256), 256, 0, as_stream(stream)>>>(*fleet, *cfg, o);
+    return check_launch("kr_urgency");
+}

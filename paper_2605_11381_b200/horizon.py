@@ -1,0 +1,165 @@
+"""Step 1a: execution-horizon policies over refinement-update magnitudes.
+
+Drop-in for `roboserve.horizon` (reference horizon.py:1-151).  The policy
+objects keep the reference's fields, defaults and validation; every decision
+runs in the `kr_horizon_confidence` / `kr_horizon_static` CUDA kernels, in
+fp64 with the reference's numpy evaluation order, so results are bit-exact.
+`decide_horizon_batch` is the fleet-scale entry point over a device tensor
+U[R, K, N] (fp32 or fp64 storage).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as dev
+
+DEFAULT_THRESHOLD = 0.4
+DEFAULT_MIN_HORIZON = 5
+
+STATIC = "static"
+CONFIDENCE_THRESHOLD = "confidence_threshold"
+
+
+@dataclass(frozen=True, eq=False)
+class UpdateMagnitudes:
+    """K x N per-step, per-action update norms of one round (horizon.py:26-61)."""
+
+    u: np.ndarray
+
+    def __post_init__(self) -> None:
+        arr = np.asarray(self.u, dtype=np.float64)
+        if arr.ndim != 2:
+            raise ValueError(f"update magnitudes must be 2-D (K x N), got shape {arr.shape}")
+        k, n = arr.shape
+        if k < 2:
+            raise ValueError(f"need at least 2 refinement steps, got {k}")
+        if n < 1:
+            raise ValueError("chunk size must be >= 1")
+        if not np.isfinite(arr).all():
+            raise ValueError("update magnitudes must be finite")
+        if (arr < 0).any():
+            raise ValueError("update magnitudes must be >= 0")
+        frozen = arr.copy()
+        frozen.setflags(write=False)
+        object.__setattr__(self, "u", frozen)
+
+    @property
+    def steps(self) -> int:
+        return self.u.shape[0]
+
+    @property
+    def chunk_size(self) -> int:
+        return self.u.shape[1]
+
+
+@dataclass(frozen=True)
+class HorizonPolicyConfig:
+    """Static horizon or confidence threshold with a floor (horizon.py:64-105)."""
+
+    kind: str
+    static_h: int = 0
+    threshold: float = DEFAULT_THRESHOLD
+    min_horizon: int = DEFAULT_MIN_HORIZON
+
+    def __post_init__(self) -> None:
+        if self.kind not in (STATIC, CONFIDENCE_THRESHOLD):
+            raise ValueError(f"unknown horizon policy kind {self.kind!r}")
+        if self.kind == STATIC and self.static_h < 1:
+            raise ValueError(f"static horizon must be >= 1, got {self.static_h}")
+        if self.kind == CONFIDENCE_THRESHOLD:
+            if self.threshold < 0:
+                raise ValueError(f"threshold must be >= 0, got {self.threshold}")
+            if self.min_horizon < 1:
+                raise ValueError(f"min_horizon must be >= 1, got {self.min_horizon}")
+
+    @classmethod
+    def static(cls, horizon: int) -> "HorizonPolicyConfig":
+        return cls(kind=STATIC, static_h=horizon)
+
+    @classmethod
+    def confidence(cls, threshold: float = DEFAULT_THRESHOLD,
+                   min_horizon: int = DEFAULT_MIN_HORIZON) -> "HorizonPolicyConfig":
+        return cls(kind=CONFIDENCE_THRESHOLD, threshold=threshold, min_horizon=min_horizon)
+
+    @property
+    def floor(self) -> int:
+        return self.static_h if self.kind == STATIC else self.min_horizon
+
+
+def decide_horizon_batch(cfg: HorizonPolicyConfig, U: torch.Tensor,
+                         out: torch.Tensor | None = None, validate: bool = True) -> torch.Tensor:
+    """H[r] = decide_horizon(cfg, U[r]) for a device tensor U[R, K, N].
+
+    fp32 storage is upcast exactly; all arithmetic is fp64.  With
+    `validate`, non-finite or negative magnitudes raise the reference's
+    ValueError (one device->host read of the flag word); without it the call
+    is fully asynchronous on the current stream.
+    """
+    if U.dim() != 3:
+        raise ValueError(f"update magnitudes must be R x K x N, got shape {tuple(U.shape)}")
+    if U.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"U must be float32 or float64, got {U.dtype}")
+    R, K, N = U.shape
+    if K < 2:
+        raise ValueError(f"need at least 2 refinement steps, got {K}")
+    if N < 1:
+        raise ValueError("chunk size must be >= 1")
+    dev.device()
+    if not U.is_cuda:
+        U = U.to(dev.device())
+    U = U.contiguous()
+    if out is None:
+        out = torch.empty(R, dtype=torch.int32, device=U.device)
+    lib = _lib.load()
+    if cfg.kind == STATIC:
+        _lib.check(lib.kr_horizon_static(R, N, cfg.static_h, out.data_ptr(), dev.stream()),
+                   "kr_horizon_static")
+        return out
+    fl = dev.flags() if validate else None
+    dtype = _lib.KR_F64 if U.dtype == torch.float64 else _lib.KR_F32
+    _lib.check(lib.kr_horizon_confidence(U.data_ptr(), dtype, R, K, N, 1.0 + cfg.threshold,
+                                         cfg.min_horizon, out.data_ptr(), _lib.ptr(fl),
+                                         dev.stream()), "kr_horizon_confidence")
+    if validate:
+        f = dev.read_flags(fl)
+        if f & _lib.FLAG_NONFINITE:
+            raise ValueError("update magnitudes must be finite")
+        if f & _lib.FLAG_NEGATIVE:
+            raise ValueError("update magnitudes must be >= 0")
+    return out
+
+
+def decide_horizon(cfg: HorizonPolicyConfig, magnitudes: UpdateMagnitudes) -> int:
+    """One round's execution horizon (horizon.py:108-132), on the device."""
+    U = dev.tensor(magnitudes.u[None], torch.float64)
+    return int(decide_horizon_batch(cfg, U, validate=False).item())
+
+
+def sweep_thresholds(cfgs: Sequence[HorizonPolicyConfig],
+                     magnitude_sequence: Iterable[UpdateMagnitudes]) -> list[float]:
+    """Mean decided horizon of each config over the rounds (horizon.py:135-151).
+
+    Rounds of equal shape are stacked into one device tensor so each config is
+    a single kernel launch over all of them."""
+    seq = list(magnitude_sequence)
+    if not cfgs:
+        raise ValueError("no policy configurations given")
+    if not seq:
+        raise ValueError("no update-magnitude rounds given")
+    groups: dict[tuple, list[np.ndarray]] = {}
+    for m in seq:
+        groups.setdefault(m.u.shape, []).append(m.u)
+    stacks = [dev.tensor(np.stack(g), torch.float64) for g in groups.values()]
+    out = []
+    for cfg in cfgs:
+        total = 0
+        for U in stacks:
+            total += int(decide_horizon_batch(cfg, U, validate=False).to(torch.int64).sum().item())
+        out.append(total / len(seq))
+    return out

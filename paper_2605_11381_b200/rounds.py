@@ -1,0 +1,230 @@
+"""Fleet-scale decision round: the production hot path.
+
+One round = for every pending robot-round of the fleet
+  (1) divergence horizon of the new chunk against the unexecuted overlap of
+      the previous one (kr_horizon_divergence) -- or the confidence policy
+      over update magnitudes (kr_horizon_confidence);
+  (2) execution-aware urgency: next-need time and the packed priority key
+      (kr_urgency);
+  (3) top-k admission under the edge budget: device radix select of the k-th
+      key, the admission pass (masks + skip counters) and the ordered S_e
+      (kr_topk_select, kr_admit).
+Everything is stream-ordered on the current CUDA stream with no host sync, so
+a round can be captured in a CUDA graph.
+
+Sharding (`ShardedDecisionRound`): one process per GPU owns a contiguous
+range of robots.  Steps (1)-(2) are local.  Each rank selects its local top
+k' = min(k, R_local) keys, the k'-key candidate lists are exchanged with one
+NCCL all-gather over NVLink (the only cross-GPU traffic), and every rank runs
+the same device select over the gathered keys.  The global k-th key decides
+admission locally (key <= kth), which is exact because the global top k is a
+subset of the union of local top-k' sets and keys are unique.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from . import device as dev
+from . import fleet as fl
+
+ALL_ONES = -1  # int64 view of 0xFFFF...FFFF
+
+
+@dataclass
+class RoundOutputs:
+    horizon: torch.Tensor      # int32 [R]
+    need_time: torch.Tensor    # int64 [R]
+    keys: torch.Tensor         # int64 [R, 2] (kr_key)
+    admitted: torch.Tensor     # uint8 [R]
+    refetch: torch.Tensor      # uint8 [R]
+    edge_keys: torch.Tensor    # int64 [k, 2] S_e keys in order (global when sharded)
+    edge_idx: torch.Tensor | None = None  # int32 [k] local indices (single GPU)
+    kth: torch.Tensor | None = None
+
+
+@dataclass
+class DivergenceInputs:
+    prev: torch.Tensor                 # [R, Lp, D]
+    cand: torch.Tensor                 # [R, Lc, D] or [R, S, Lc, D]
+    threshold: float
+    offset: torch.Tensor | None = None
+    len_prev: torch.Tensor | None = None
+    len_cand: torch.Tensor | None = None
+
+
+class DecisionRound:
+    """Preallocated single-GPU decision round over R robots, budget k."""
+
+    def __init__(self, R: int, k: int, sched: _lib.KrSched):
+        self.R = R
+        self.k = min(k, R)
+        self.sched = sched
+        d = dev.device()
+        self.H = torch.empty(R, dtype=torch.int32, device=d)
+        self.need_time = torch.empty(R, dtype=torch.int64, device=d)
+        self.keys = fl.new_keys(R, d)
+        self.admitted = torch.empty(R, dtype=torch.uint8, device=d)
+        self.refetch = torch.empty(R, dtype=torch.uint8, device=d)
+        self.kth = fl.new_keys(1, d)
+        self.edge_idx = torch.empty(max(self.k, 1), dtype=torch.int32, device=d)
+        self.edge_keys = fl.new_keys(max(self.k, 1), d)
+        self.ws = fl.Workspace(R)
+        self.lib = _lib.load()
+
+    def horizons(self, h: DivergenceInputs) -> None:
+        prev, cand = h.prev, h.cand
+        if cand.dim() == 3:
+            cand = cand.unsqueeze(1)
+        R, Lp, D = prev.shape
+        S, Lc = cand.shape[1], cand.shape[2]
+        dtype = _lib.KR_F64 if prev.dtype == torch.float64 else _lib.KR_F32
+        _lib.check(self.lib.kr_horizon_divergence(
+            prev.data_ptr(), cand.data_ptr(), dtype, R, S, Lp, Lc, D, _lib.ptr(h.offset),
+            _lib.ptr(h.len_prev), _lib.ptr(h.len_cand), float(h.threshold), self.H.data_ptr(),
+            None, dev.stream()), "kr_horizon_divergence")
+
+    def urgency(self, fleet: fl.DeviceFleet) -> None:
+        fs = fleet.c_struct()
+        _lib.check(self.lib.kr_urgency(
+            ctypes.byref(fs), ctypes.byref(self.sched), self.keys.data_ptr(),
+            self.need_time.data_ptr(), None, None, None, None, None, None, dev.stream()),
+            "kr_urgency")
+
+    def admit(self, fleet: fl.DeviceFleet) -> None:
+        k, n = self.k, self.R
+        lib = self.lib
+        kth_ptr = None
+        if 0 < k < n:
+            _lib.check(lib.kr_topk_select(self.keys.data_ptr(), n, k, self.kth.data_ptr(),
+                                          self.ws.ptr(), self.ws.nbytes, dev.stream()),
+                       "kr_topk_select")
+            kth_ptr = self.kth.data_ptr()
+        fs = fleet.c_struct()
+        _lib.check(lib.kr_admit(
+            self.keys.data_ptr(), n, k, kth_ptr, ctypes.byref(fs), ctypes.byref(self.sched),
+            self.admitted.data_ptr(), self.refetch.data_ptr(), self.edge_idx.data_ptr(),
+            self.edge_keys.data_ptr(), self.ws.ptr(), self.ws.nbytes, dev.stream()), "kr_admit")
+
+    def run(self, fleet: fl.DeviceFleet, h: DivergenceInputs) -> RoundOutputs:
+        self.horizons(h)
+        self.urgency(fleet)
+        self.admit(fleet)
+        return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
+                            self.edge_keys[: self.k], self.edge_idx[: self.k], self.kth)
+
+
+def sharded_topk(keys, n_local: int, k: int, sizes: list, ops, group=None):
+    """Exact global top-k admission over robot-sharded keys (host protocol).
+
+    `ops` supplies the device primitives (product: `CudaShardOps`; the CPU
+    tests plug in a numpy twin to exercise this protocol under gloo):
+      local_candidates(keys, kl, kg) -> [kg, 2] local top-kl keys, sentinel-padded
+      all_gather(cand)               -> [W * kg, 2]
+      kth(keys, k)                   -> k-th smallest key (device handle)
+      sorted_leq(keys, k, kth)       -> the keys <= kth, ascending ([k, 2])
+      apply(keys, k, kth)            -> local admission (masks, skip counters)
+    Returns (k_global, global ordered S_e keys).
+    """
+    world = len(sizes)
+    kg = min(k, sum(sizes))
+    kl = min(kg, n_local)
+    cand = ops.local_candidates(keys, kl, kg)
+    gathered = ops.all_gather(cand)
+    m = kg * world
+    if world == 1:
+        kth = ops.kth(keys, kl) if 0 < kl < n_local else None
+    else:
+        kth = ops.kth(gathered, kg) if 0 < kg < m else None
+    edge = ops.sorted_leq(gathered, kg, kth) if kg > 0 else None
+    ops.apply(keys, kg, kth)
+    return kg, edge
+
+
+class CudaShardOps:
+    """sharded_topk primitives as C-ABI calls on preallocated device buffers."""
+
+    def __init__(self, rnd: "ShardedDecisionRound", fleet: fl.DeviceFleet):
+        self.r = rnd
+        self.fleet = fleet
+
+    def local_candidates(self, keys, kl, kg):
+        r, st = self.r, dev.stream()
+        r.cand.fill_(ALL_ONES)
+        if kl > 0:
+            kth_ptr = None
+            if kl < r.R:
+                _lib.check(r.lib.kr_topk_select(keys.data_ptr(), r.R, kl, r.kth_local.data_ptr(),
+                                                r.ws.ptr(), r.ws.nbytes, st), "kr_topk_select")
+                kth_ptr = r.kth_local.data_ptr()
+            _lib.check(r.lib.kr_admit(keys.data_ptr(), r.R, kl, kth_ptr, None, None, None, None,
+                                      None, r.cand.data_ptr(), r.ws.ptr(), r.ws.nbytes, st),
+                       "kr_admit(local candidates)")
+        return r.cand
+
+    def all_gather(self, cand):
+        # the only cross-GPU traffic of a round: W x k' x 16 B over NVLink
+        dist.all_gather_into_tensor(self.r.gathered, cand, group=self.r.group)
+        return self.r.gathered
+
+    def kth(self, keys, k):
+        r = self.r
+        ws = r.ws if keys is r.keys else r.ws_merge
+        out = r.kth_local if keys is r.keys else r.kth_global
+        _lib.check(r.lib.kr_topk_select(keys.data_ptr(), keys.shape[0], k, out.data_ptr(),
+                                        ws.ptr(), ws.nbytes, dev.stream()), "kr_topk_select")
+        return out
+
+    def sorted_leq(self, keys, k, kth):
+        r = self.r
+        _lib.check(r.lib.kr_admit(keys.data_ptr(), keys.shape[0], k, _lib.ptr(kth), None, None,
+                                  None, None, None, r.global_edge.data_ptr(), r.ws_merge.ptr(),
+                                  r.ws_merge.nbytes, dev.stream()), "kr_admit(merge)")
+        return r.global_edge[:k]
+
+    def apply(self, keys, k, kth):
+        r = self.r
+        fs = self.fleet.c_struct()
+        _lib.check(r.lib.kr_admit(keys.data_ptr(), r.R, k, _lib.ptr(kth), ctypes.byref(fs),
+                                  ctypes.byref(r.sched), r.admitted.data_ptr(),
+                                  r.refetch.data_ptr(), None, None, None, 0, dev.stream()),
+                   "kr_admit(apply)")
+
+
+class ShardedDecisionRound(DecisionRound):
+    """Robot-sharded round: local steps + one all-gather of top-k' candidates.
+
+    `k` is the global edge budget.  Requires torch.distributed (NCCL on GPUs)."""
+
+    def __init__(self, R_local: int, k: int, sched: _lib.KrSched, group=None):
+        super().__init__(R_local, k, sched)
+        self.group = group
+        self.world = dist.get_world_size(group)
+        sizes = torch.tensor([R_local], dtype=torch.int64, device=self.H.device)
+        allsz = [torch.zeros_like(sizes) for _ in range(self.world)]
+        dist.all_gather(allsz, sizes, group=group)
+        self.sizes = [int(s.item()) for s in allsz]
+        self.k_global = min(k, sum(self.sizes))
+        kg = max(self.k_global, 1)
+        d = self.H.device
+        self.cand = fl.new_keys(kg, d)
+        self.gathered = fl.new_keys(kg * self.world, d)
+        self.kth_local = fl.new_keys(1, d)
+        self.kth_global = fl.new_keys(1, d)
+        self.global_edge = fl.new_keys(kg, d)
+        self.ws_merge = fl.Workspace(kg * self.world)
+
+    def admit(self, fleet: fl.DeviceFleet) -> None:
+        sharded_topk(self.keys, self.R, self.k, self.sizes, CudaShardOps(self, fleet), self.group)
+
+    def run(self, fleet: fl.DeviceFleet, h: DivergenceInputs) -> RoundOutputs:
+        self.horizons(h)
+        self.urgency(fleet)
+        self.admit(fleet)
+        return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
+                            self.global_edge[: self.k_global], None, self.kth_global)

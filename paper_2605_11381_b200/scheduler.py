@@ -1,0 +1,211 @@
+"""Step 3: execution-aware priority ordering and top-k edge admission.
+
+Drop-in for `roboserve.scheduler` (reference scheduler.py:1-284).  Config and
+plan types keep the reference's fields and validation.  `plan` packs the
+pending set into the fleet layout, and three CUDA kernels make every decision:
+
+  kr_urgency    ledger -> wait ratio -> bucket (+aging) -> exec estimate ->
+                aged estimate -> one unique 128-bit key per request whose
+                ascending order is the reference's order (buckets high to low,
+                then (-aged, issued_at, task_id); FIFO / LAS keys likewise)
+  kr_sort_keys  the total order (needed for the ordered `deferred` tuple)
+  kr_admit      edge prefix of k = capacity - in_flight, stale-observation
+                refetch mask and the skip-counter side effect
+
+The host only builds the result objects and mirrors the skip counters into
+`states` as the reference does (scheduler.py:229-234).  The phase-3 cloud tier
+(scheduler.py:160-190, 210-221) is outside this build's decision core: a call
+that would consult it raises NotImplementedError rather than approximating.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+from typing import Iterable, Mapping, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as dev
+from . import fleet as fl
+from .core import Duration, PendingRequest, TaskState, TimePoint
+from .waiting import _state_fleet
+
+KAIROS = "kairos"
+FIFO = "fifo"
+LAS = "las"
+POLICIES = (KAIROS, FIFO, LAS)
+
+AGED_MAX = (1 << 56) - 1
+
+
+@dataclass(frozen=True)
+class SchedulerConfig:
+    """Scheduler knobs (scheduler.py:38-56)."""
+
+    policy: str = KAIROS
+    buckets: int = 10
+    aging_interval: int = 5
+    stale_threshold: Duration = 150_000
+    default_exec_estimate: Duration = 166_667
+
+    def __post_init__(self) -> None:
+        if self.policy not in POLICIES:
+            raise ValueError(f"policy must be one of {POLICIES}, got {self.policy!r}")
+        if self.buckets < 1:
+            raise ValueError(f"buckets must be >= 1, got {self.buckets}")
+        if self.aging_interval < 1:
+            raise ValueError(f"aging_interval must be >= 1, got {self.aging_interval}")
+        if self.stale_threshold < 0:
+            raise ValueError("stale_threshold must be >= 0")
+        if self.default_exec_estimate < 0:
+            raise ValueError("default_exec_estimate must be >= 0")
+
+
+@dataclass(frozen=True)
+class DispatchPlan:
+    """Per-tier dispatch lists plus deferred requests (scheduler.py:59-76)."""
+
+    edge: tuple
+    cloud: tuple
+    deferred: tuple
+    refetch_task_ids: frozenset
+
+    @property
+    def dispatched(self) -> tuple:
+        return self.edge + self.cloud
+
+
+def assign_bucket(wr: float, skipped: int, cfg: SchedulerConfig) -> int:
+    """Equal-width wait-ratio bucket with skip promotion (scheduler.py:79-88)."""
+    if not 0.0 <= wr <= 1.0:
+        raise ValueError(f"wait ratio must be in [0, 1], got {wr}")
+    if skipped < 0:
+        raise ValueError(f"skipped must be >= 0, got {skipped}")
+    if cfg.buckets > 256 or skipped >= (1 << 31):
+        raise ValueError("buckets must be <= 256 and skipped < 2^31 on the device path")
+    w = dev.tensor([float(wr)], torch.float64)
+    s = dev.tensor([int(skipped)], torch.int32)
+    b = torch.empty(1, dtype=torch.int32, device=w.device)
+    _lib.check(_lib.load().kr_assign_bucket(w.data_ptr(), s.data_ptr(), 1, cfg.buckets,
+                                            cfg.aging_interval, b.data_ptr(), dev.stream()),
+               "kr_assign_bucket")
+    return int(b.item())
+
+
+def estimate_exec_latency(state: TaskState, default: Optional[Duration] = None) -> Duration:
+    """Last execution length, else the default (scheduler.py:91-104)."""
+    sched = fl.sched_struct(FIFO, 1, 1, 0, default if default is not None else 0, 0, 1, 0)
+    out = fl.urgency(_state_fleet(state), sched, need_time=False, intermediates=True)
+    return int(out.est.item())
+
+
+def _issued_base(issued: np.ndarray) -> int:
+    if issued.size == 0:
+        return 0
+    lo, hi = int(issued.min()), int(issued.max())
+    if hi - lo >= fl.ISSUED_SPAN:
+        raise ValueError("pending issue times span more than 2^40 µs; the packed sort key "
+                         "cannot order them")
+    return lo
+
+
+def _ranks(ids: Sequence[str]) -> dict:
+    if len(set(ids)) != len(ids):
+        raise ValueError("pending set holds more than one request for a task")
+    if len(ids) >= fl.RANK_SPAN:
+        raise ValueError("more than 2^24 pending requests in one planning round")
+    return {t: i for i, t in enumerate(sorted(ids))}
+
+
+def order_within_bucket(requests: Sequence[PendingRequest], exec_estimates: Mapping[str, Duration],
+                        cfg: SchedulerConfig) -> list[PendingRequest]:
+    """Descending aged estimate, then arrival, then task id (scheduler.py:107-117).
+
+    Keys are packed on the host (hi = AGED_MAX - aged, lo = issued/rank word)
+    and ordered by the device sort."""
+    reqs = list(requests)
+    if not reqs:
+        return []
+    rank = _ranks([r.task_id for r in reqs])
+    issued = np.array([r.issued_at for r in reqs], np.int64)
+    base = _issued_base(issued)
+    keys = np.empty((len(reqs), 2), np.uint64)
+    for i, r in enumerate(reqs):
+        aged = exec_estimates[r.task_id] * (1 + r.skipped)
+        if not 0 <= aged <= AGED_MAX:
+            raise ValueError("aged execution estimate outside the packed key range")
+        keys[i, 0] = AGED_MAX - aged
+        keys[i, 1] = ((r.issued_at - base) << 24) | rank[r.task_id]
+    kt = dev.tensor(keys.view(np.int64), torch.int64)
+    ws = fl.Workspace(len(reqs))
+    order, _ = fl.sort_keys(kt, ws)
+    return [reqs[i] for i in order.cpu().tolist()]
+
+
+def _checked_pending(pending: Iterable[PendingRequest],
+                     states: Mapping[str, TaskState]) -> list[PendingRequest]:
+    reqs = sorted(pending, key=lambda r: (r.issued_at, r.task_id))
+    for req in reqs:
+        if req.task_id not in states:
+            raise ValueError(f"pending request references unknown task {req.task_id!r}")
+    return reqs
+
+
+def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edge, cloud, net,
+         now: TimePoint, cfg: SchedulerConfig, *, edge_in_flight: int = 0,
+         cloud_in_flight: int = 0) -> DispatchPlan:
+    """One planning round under the configured policy (scheduler.py:254-276)."""
+    reqs = _checked_pending(pending, states)
+    edge_avail = max(0, edge.capacity - edge_in_flight) if edge is not None else 0
+    cloud_avail = max(0, cloud.capacity - cloud_in_flight) if cloud is not None else 0
+    if cloud is not None and net is not None and cloud_avail > 0 and len(reqs) > edge_avail:
+        raise NotImplementedError(
+            "cloud-tier placement (scheduler.py:160-190, 210-221) is not part of the B200 "
+            "decision core; plan with cloud=None or net=None")
+    n = len(reqs)
+    if n == 0:
+        return DispatchPlan(edge=(), cloud=(), deferred=(), refetch_task_ids=frozenset())
+    if cfg.buckets > 256:
+        raise ValueError("the packed sort key supports at most 256 buckets")
+    rank = _ranks([r.task_id for r in reqs])
+    soa = fl.host_soa(reqs, states, rank)
+    base = _issued_base(soa["issued_at"])
+    fleet = fl.DeviceFleet.from_host(soa)
+    sched = fl.sched_struct(cfg.policy, cfg.buckets, cfg.aging_interval, cfg.stale_threshold,
+                            cfg.default_exec_estimate, int(now), 1, base)
+    flags = dev.flags()
+    u = fl.urgency(fleet, sched, need_time=False, flags=flags)
+    ws = fl.Workspace(n)
+    order, sorted_keys = fl.sort_keys(u.keys, ws)
+    k = min(edge_avail, n)
+    kth_ptr = sorted_keys.data_ptr() + (k - 1) * 16 if 0 < k < n else None
+    refetch = torch.empty(n, dtype=torch.uint8, device=u.keys.device)
+    fl.admit(u.keys, k, kth_ptr, fleet, sched, None, refetch=refetch)
+    f = dev.read_flags(flags)
+    if f & (_lib.FLAG_KEY_RANGE | _lib.FLAG_RATIO):
+        raise ValueError("a pending request falls outside the packed sort-key range "
+                         "(aged estimate >= 2^56 µs or lifetime >= 2^53 µs)")
+    order_h = order.cpu().numpy()
+    refetch_h = refetch.cpu().numpy()
+    skipped_h = fleet.t["skipped"].cpu().numpy()
+    s_edge = [reqs[i] for i in order_h[:k]]
+    deferred = []
+    for i in order_h[:k]:
+        states[reqs[i].task_id].skipped = int(skipped_h[i])
+    for i in order_h[k:]:
+        r = reqs[i]
+        states[r.task_id].skipped = int(skipped_h[i])
+        deferred.append(replace(r, skipped=int(skipped_h[i])))
+    refetch_ids = frozenset(reqs[i].task_id for i in np.nonzero(refetch_h)[0])
+    return DispatchPlan(edge=tuple(s_edge), cloud=(), deferred=tuple(deferred),
+                        refetch_task_ids=refetch_ids)
+
+
+def plan_fifo(pending, states, edge, cloud, net, now, cfg, **kw) -> DispatchPlan:
+    return plan(pending, states, edge, cloud, net, now, replace(cfg, policy=FIFO), **kw)
+
+
+def plan_las(pending, states, edge, cloud, net, now, cfg, **kw) -> DispatchPlan:
+    return plan(pending, states, edge, cloud, net, now, replace(cfg, policy=LAS), **kw)

@@ -1,0 +1,126 @@
+"""Step 1 on the GPU vs the reference's golden vectors and the CPU oracle:
+bit-exact horizons (and bit-exact fp64 cosine scores)."""
+
+from __future__ import annotations
+
+from collections import defaultdict
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kb():
+    import paper_2605_11381_b200 as kb
+    return kb
+
+
+def test_confidence_golden_scalar(kb):
+    cases = golden_io.confidence_cases()
+    bad = []
+    for i, (u, t, hmin, exp) in enumerate(cases[::7]):
+        cfg = kb.HorizonPolicyConfig.confidence(threshold=t, min_horizon=hmin)
+        if kb.decide_horizon(cfg, kb.UpdateMagnitudes(u)) != exp:
+            bad.append(i)
+    assert not bad
+
+
+@pytest.mark.parametrize("storage", [torch.float64, torch.float32])
+def test_confidence_golden_batched(kb, storage):
+    groups = defaultdict(list)
+    for u, t, hmin, exp in golden_io.confidence_cases():
+        if storage == torch.float32 and not np.array_equal(u.astype(np.float32).astype(np.float64), u):
+            continue
+        groups[(u.shape, t, hmin)].append((u, exp))
+    checked = 0
+    for (shape, t, hmin), items in groups.items():
+        U = torch.tensor(np.stack([u for u, _ in items]), dtype=storage, device="cuda")
+        H = kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(t, hmin), U)
+        assert H.cpu().tolist() == [e for _, e in items], (shape, t, hmin)
+        checked += len(items)
+    assert checked > 300
+
+
+@pytest.mark.parametrize("R,K,N", [(1, 2, 1), (37, 6, 50), (4099, 6, 64), (1000, 10, 50),
+                                   (513, 3, 1), (64, 130, 1), (257, 4, 300)])
+@pytest.mark.parametrize("storage", [np.float32, np.float64])
+def test_confidence_random_vs_oracle(kb, R, K, N, storage):
+    rng = np.random.default_rng(R * 31 + K * 7 + N)
+    U = (rng.uniform(0.5, 2.0, (R, 1, N)) * rng.uniform(0.3, 0.8, (R, 1, N)) **
+         np.arange(K)[None, :, None] * rng.uniform(0.95, 1.05, (R, K, N)))
+    tail = rng.integers(0, N + 1, R)
+    for r in range(R):
+        if tail[r] < N:
+            U[r, -1, tail[r]:] = 1.8 * U[r, :-1, tail[r]:].mean(axis=0)
+    U = U.astype(storage)
+    for t, hmin in [(0.4, 5), (0.8, 1), (0.0, 1)]:
+        exp = orc.horizon_conf_batch(U, t, hmin)
+        H = kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(t, hmin),
+                                    torch.from_numpy(U).cuda())
+        assert np.array_equal(H.cpu().numpy(), exp)
+
+
+def test_confidence_unaligned_and_static(kb):
+    rng = np.random.default_rng(3)
+    base = torch.tensor(rng.uniform(0, 1, 1 + 33 * 6 * 7), dtype=torch.float32, device="cuda")
+    U = base[1:].view(33, 6, 7)          # 4-byte aligned only: plain-staging path
+    exp = orc.horizon_conf_batch(U.cpu().numpy(), 0.4, 2)
+    H = kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(0.4, 2), U)
+    assert np.array_equal(H.cpu().numpy(), exp)
+    Hs = kb.decide_horizon_batch(kb.HorizonPolicyConfig.static(5), U)
+    assert (Hs == 5).all()
+
+
+def test_confidence_validation_flags(kb):
+    U = torch.ones(8, 3, 4, dtype=torch.float32, device="cuda")
+    U[5, 1, 2] = float("nan")
+    with pytest.raises(ValueError, match="finite"):
+        kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(), U)
+    U[5, 1, 2] = -1.0
+    with pytest.raises(ValueError, match=">= 0"):
+        kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(), U)
+
+
+def test_divergence_golden(kb):
+    from paper_2605_11381_b200.divergence import round_optimal_horizon_batch
+    bad_h, bad_c = [], []
+    for i, (ref, cand, thr, exp, cos) in enumerate(golden_io.divergence_cases()):
+        H, c = round_optimal_horizon_batch(torch.tensor(ref[None], device="cuda"),
+                                           torch.tensor(cand[None], device="cuda"), thr,
+                                           return_cos=True)
+        if int(H.item()) != exp:
+            bad_h.append(i)
+        got = c[0, 0, :len(cos)].cpu().numpy()
+        if not np.array_equal(got, cos):
+            bad_c.append(i)
+        if i % 9 == 0:
+            assert kb.round_optimal_horizon(ref, cand, thr) == exp
+    assert not bad_h and not bad_c, (bad_h[:5], bad_c[:5])
+
+
+@pytest.mark.parametrize("R,S,Lp,Lc,D", [(1024, 1, 50, 50, 7), (300, 1, 64, 64, 32),
+                                         (130, 8, 50, 50, 7), (77, 3, 20, 16, 5),
+                                         (65, 2, 40, 40, 48), (33, 1, 10, 10, 16)])
+def test_divergence_random_vs_oracle(kb, R, S, Lp, Lc, D):
+    from paper_2605_11381_b200.divergence import round_optimal_horizon_batch
+    rng = np.random.default_rng(R + S + D)
+    prev = rng.normal(size=(R, Lp, D)).astype(np.float32)
+    noise = rng.normal(size=(R, S, Lc, D)) * (0.35 * np.arange(1, Lc + 1) / Lc)[None, None, :, None]
+    cand = (prev[:, None, :Lc] if Lp >= Lc else np.pad(prev, ((0, 0), (0, Lc - Lp), (0, 0)))[:, None])
+    cand = (cand + noise).astype(np.float32)
+    ragged = S > 1 or Lp != Lc
+    off = rng.integers(0, 4, R).astype(np.int32) if ragged else None
+    lp = rng.integers(0, Lp + 1, R).astype(np.int32) if ragged else None
+    lc = rng.integers(0, Lc + 1, R).astype(np.int32) if ragged else None
+    exp, exp_cos = orc.divergence_batch(prev, cand, 0.9, off, lp, lc, want_cos=True)
+    t = lambda a: None if a is None else torch.from_numpy(a).cuda()
+    H, cos = round_optimal_horizon_batch(t(prev), t(cand), 0.9, t(off), t(lp), t(lc),
+                                         return_cos=True)
+    assert np.array_equal(H.cpu().numpy(), exp)
+    assert np.array_equal(cos.cpu().numpy(), exp_cos, equal_nan=True)

@@ -1,0 +1,54 @@
+"""The full decision round (rounds.DecisionRound: divergence horizon + urgency +
+top-k admission) on a synthetic fleet vs the CPU oracle, bit-exact."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("R,k,S,D", [(1 << 15, 1024, 1, 7), (5000, 64, 8, 7), (3000, 300, 1, 32),
+                                     (777, 777, 1, 7), (1000, 0, 1, 7)])
+def test_decision_round_vs_oracle(R, k, S, D):
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    soa = synthetic.fleet_soa(R, seed=R + k)
+    prev, cand, off = synthetic.chunks(R, seed=R, S=S, D=D, Lp=50 if D == 7 else 64,
+                                       Lc=50 if D == 7 else 64)
+    fleet = fl.DeviceFleet.from_host(soa)
+    base = int(soa["issued_at"].min())
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, base)
+    rnd = rounds.DecisionRound(R, k, sched)
+    out = rnd.run(fleet, rounds.DivergenceInputs(prev, cand, 0.9, offset=off))
+    torch.cuda.synchronize()
+    # step 1
+    H = orc.divergence_batch(prev.cpu().numpy(), cand.cpu().numpy(), 0.9, off.cpu().numpy())
+    assert np.array_equal(out.horizon.cpu().numpy(), H)
+    # steps 2-3
+    res = orc.plan_soa(soa, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+    assert np.array_equal(out.need_time.cpu().numpy(), res["need_time"])
+    assert np.array_equal(out.admitted.cpu().numpy(), res["admitted"])
+    assert np.array_equal(out.refetch.cpu().numpy(), res["refetch"])
+    assert np.array_equal(fleet.t["skipped"].cpu().numpy(), res["skipped_out"])
+    if k:
+        assert np.array_equal(out.edge_idx.cpu().numpy(), res["order"][:k])
+
+
+@pytest.mark.parametrize("policy", ["fifo", "las"])
+def test_round_baseline_policies(policy):
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    R, k = 4000, 333
+    soa = synthetic.fleet_soa(R, seed=9)
+    fleet = fl.DeviceFleet.from_host(soa)
+    sched = fl.sched_struct(policy, 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    rnd = rounds.DecisionRound(R, k, sched)
+    rnd.urgency(fleet)
+    rnd.admit(fleet)
+    res = orc.plan_soa(soa, policy, 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+    assert np.array_equal(rnd.edge_idx.cpu().numpy(), res["order"][:k])
+    assert np.array_equal(rnd.admitted.cpu().numpy(), res["admitted"])

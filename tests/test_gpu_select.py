@@ -1,0 +1,69 @@
+"""Device radix select / sort / admission vs numpy on unique 128-bit keys."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _keys(n, rng, spread):
+    hi = rng.integers(0, spread, n, dtype=np.uint64) << np.uint64(40)
+    hi |= rng.integers(0, 1 << 20, n, dtype=np.uint64)
+    lo = (rng.integers(0, 1 << 30, n, dtype=np.uint64) << np.uint64(24)) | np.arange(n, dtype=np.uint64)
+    k = np.stack([hi, lo], 1)
+    return k
+
+
+def _order(k):
+    return np.lexsort((k[:, 1], k[:, 0]))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 100, 4097, 8192, 8193, 70000, 1 << 20])
+@pytest.mark.parametrize("spread", [1, 16, 1 << 24])
+def test_sort_keys(n, spread):
+    from paper_2605_11381_b200 import fleet as fl
+    rng = np.random.default_rng(n + spread)
+    k = _keys(n, rng, spread)
+    kt = torch.from_numpy(k.view(np.int64)).cuda()
+    order, sk = fl.sort_keys(kt, fl.Workspace(n))
+    exp = _order(k)
+    assert np.array_equal(order.cpu().numpy(), exp)
+    assert np.array_equal(sk.cpu().numpy().view(np.uint64), k[exp])
+
+
+@pytest.mark.parametrize("n,k", [(10, 1), (10, 9), (1000, 64), (1 << 16, 1024), (1 << 20, 8192),
+                                 (1 << 20, 1), (1 << 20, (1 << 20) - 1), (300000, 20000)])
+@pytest.mark.parametrize("spread", [1, 10, 1 << 30])
+def test_topk_select_and_admit(n, k, spread):
+    from paper_2605_11381_b200 import fleet as fl
+    rng = np.random.default_rng(n * 3 + k + spread)
+    keys = _keys(n, rng, spread)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    ws = fl.Workspace(n)
+    kth = fl.topk_select(kt, k, ws)
+    exp = _order(keys)
+    assert np.array_equal(kth.cpu().numpy().view(np.uint64)[0], keys[exp[k - 1]])
+    adm = torch.empty(n, dtype=torch.uint8, device="cuda")
+    edge_idx = torch.empty(k, dtype=torch.int32, device="cuda")
+    fl.admit(kt, k, kth.data_ptr(), None, None, ws, admitted=adm, edge_idx=edge_idx)
+    mask = np.zeros(n, bool)
+    mask[exp[:k]] = True
+    assert np.array_equal(adm.cpu().numpy().astype(bool), mask)
+    assert np.array_equal(edge_idx.cpu().numpy(), exp[:k])
+
+
+def test_admit_all_and_none():
+    from paper_2605_11381_b200 import fleet as fl
+    rng = np.random.default_rng(1)
+    keys = _keys(500, rng, 7)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    ws = fl.Workspace(500)
+    adm = torch.empty(500, dtype=torch.uint8, device="cuda")
+    idx = torch.empty(500, dtype=torch.int32, device="cuda")
+    fl.admit(kt, 500, None, None, None, ws, admitted=adm, edge_idx=idx)
+    assert adm.all() and np.array_equal(idx.cpu().numpy(), _order(keys))
+    fl.admit(kt, 0, None, None, None, ws, admitted=adm)
+    assert not adm.any()

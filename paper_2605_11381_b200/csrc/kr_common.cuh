@@ -209,6 +209,71 @@ __device__ __forceinline__ double cosine_skx_fixed(const T* a, const T* b) {
 }
 
 // ---------------------------------------------------------------------------
+// Exact fp32 pre-decision ("filter") for the cosine threshold test
+// ---------------------------------------------------------------------------
+// The reference decides `cos < thr` on an fp64 cosine.  For fp32-representable
+// inputs an fp32 evaluation of the same cosine is within a proven bound of the
+// exact value: every dot is off by at most gamma_D = D*2^-24 relative to
+// sum|x_i*y_i| <= |x||y| (Cauchy-Schwarz), rsqrtf by 2 ulp, and the two
+// products by 1 ulp each, so |c32 - c| <= 2*gamma_D + 2^-20 + 2^-22; the fp64
+// result differs from c by < 2^-48.  Whenever |c32 - thr| exceeds
+// margin = (2D + 24) * 2^-24 + 2^-20 the decision is therefore already known;
+// only the rare near-threshold actions (and zero / extreme-range vectors) fall
+// back to the bit-exact fp64 path.  Decisions are identical by construction.
+__host__ __device__ inline float cos_filter_margin(int D) {
+    return static_cast<float>((2.0 * D + 24.0) * 5.9604644775390625e-8 + 9.5367431640625e-7);
+}
+
+// Returns 1 (cos >= thr), 0 (cos < thr) or -1 (undecided: use the exact path).
+template <int DC, typename T>
+__device__ __forceinline__ int cos_filter_fixed(const T* a, const T* b, float thr_f, float margin) {
+    float xx = 0.f, yy = 0.f, xy = 0.f;
+#pragma unroll
+    for (int i = 0; i < DC; i++) {
+        float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
+        xx = __fmaf_rn(x, x, xx);
+        yy = __fmaf_rn(y, y, yy);
+        xy = __fmaf_rn(x, y, xy);
+    }
+    if (!(xx >= 1e-30f && yy >= 1e-30f && xx <= 1e30f && yy <= 1e30f)) return -1;
+    float c = __fmul_rn(__fmul_rn(xy, rsqrtf(xx)), rsqrtf(yy));
+    float d = __fsub_rn(c, thr_f);
+    if (d > margin) return 1;
+    if (d < -margin) return 0;
+    return -1;
+}
+template <typename T>
+__device__ __forceinline__ int cos_filter(const T* a, const T* b, int D, float thr_f, float margin) {
+    float xx = 0.f, yy = 0.f, xy = 0.f;
+    for (int i = 0; i < D; i++) {
+        float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
+        xx = __fmaf_rn(x, x, xx);
+        yy = __fmaf_rn(y, y, yy);
+        xy = __fmaf_rn(x, y, xy);
+    }
+    if (!(xx >= 1e-30f && yy >= 1e-30f && xx <= 1e30f && yy <= 1e30f)) return -1;
+    float c = __fmul_rn(__fmul_rn(xy, rsqrtf(xx)), rsqrtf(yy));
+    float d = __fsub_rn(c, thr_f);
+    if (d > margin) return 1;
+    if (d < -margin) return 0;
+    return -1;
+}
+
+// Magic-number unsigned division for n < 2^31 (loop-invariant divisors).
+struct FastDiv {
+    uint32_t d, m, s;
+};
+__host__ inline FastDiv make_fastdiv(uint32_t d) {
+    uint32_t s = 0;
+    while ((uint64_t(1) << s) < d) s++;
+    uint64_t m = ((uint64_t(1) << 32) * ((uint64_t(1) << s) - d)) / d + 1;
+    return FastDiv{d, static_cast<uint32_t>(m), s};
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+    return (__umulhi(n, f.m) + n) >> f.s;
+}
+
+// ---------------------------------------------------------------------------
 // Integer-microsecond time (core.py:24-47)
 // ---------------------------------------------------------------------------
 // us_from_actions(count, hz_num/hz_den) = floor(count*1e6*den/num + 1/2)

@@ -13,9 +13,9 @@
 //   2. One elementwise admission pass (key <= kth): admitted / refetch masks,
 //      skip counters (scheduler.py:223-234) and a gather of the k admitted
 //      (key, index) pairs.
-//   3. A sort of only those k pairs (single-CTA bitonic network in shared
-//      memory for k <= 8192, otherwise a stable multi-CTA LSD radix sort over
-//      the differing key bits), giving S_e in reference order.
+//   3. A sort of only those k pairs (a grid-wide parallel rank sort for
+//      k <= 16384, otherwise a stable multi-CTA LSD radix sort over the
+//      differing key bits), giving S_e in reference order.
 // Keys are unique (the lexrank tiebreak), so every step is deterministic.
 #include <climits>
 
@@ -26,7 +26,6 @@ namespace kr {
 
 constexpr int kDigitBits = 11;
 constexpr int kBins = 1 << kDigitBits;
-constexpr int kBitonicMax = 8192;
 constexpr int kSortTile = 2048;  // LSD radix: elements per CTA tile (256 threads x 8)
 
 struct SelState {
@@ -49,6 +48,7 @@ struct Workspace {
     kr_key* cand[2];
     kr_key* skeys[2];
     int32_t* sidx[2];
+    uint32_t* rank;
     uint32_t* tile_hist;
 };
 
@@ -62,6 +62,7 @@ static size_t workspace_bytes(int64_t n) {
     b += 2 * align256(nn * sizeof(kr_key));      // select candidates
     b += 2 * align256(nn * sizeof(kr_key));      // sort keys ping-pong
     b += 2 * align256(nn * sizeof(int32_t));     // sort index ping-pong
+    b += align256(nn * sizeof(uint32_t));        // rank-sort ranks
     b += align256(sort_tiles(n) * 256 * sizeof(uint32_t));
     return b;
 }
@@ -84,6 +85,8 @@ static Workspace carve(void* ws, int64_t n) {
         w.sidx[i] = reinterpret_cast<int32_t*>(p);
         p += align256(nn * sizeof(int32_t));
     }
+    w.rank = reinterpret_cast<uint32_t*>(p);
+    p += align256(nn * sizeof(uint32_t));
     w.tile_hist = reinterpret_cast<uint32_t*>(p);
     return w;
 }
@@ -100,20 +103,57 @@ __device__ __forceinline__ unsigned long long warp_and(unsigned long long v) {
     return v;
 }
 
-// OR / AND of keys, reduced per warp then atomically into dst[4].
+// OR / AND of keys: warp shuffles, then shared memory, then one set of
+// global atomics per block (only if the block saw any key).
 __device__ __forceinline__ void stats_accumulate(unsigned long long* dst, unsigned long long ohi,
                                                  unsigned long long olo, unsigned long long ahi,
                                                  unsigned long long alo) {
+    __shared__ unsigned long long red[4][32];
     ohi = warp_or(ohi);
     olo = warp_or(olo);
     ahi = warp_and(ahi);
     alo = warp_and(alo);
-    if ((threadIdx.x & 31) == 0) {
-        if (ohi) atomicOr(&dst[0], ohi);
-        if (olo) atomicOr(&dst[1], olo);
-        if (~ahi) atomicAnd(&dst[2], ahi);
-        if (~alo) atomicAnd(&dst[3], alo);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+    if (lane == 0) {
+        red[0][warp] = ohi; red[1][warp] = olo; red[2][warp] = ahi; red[3][warp] = alo;
     }
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long a = lane < nw ? red[0][lane] : 0ull;
+        unsigned long long b = lane < nw ? red[1][lane] : 0ull;
+        unsigned long long c = lane < nw ? red[2][lane] : ~0ull;
+        unsigned long long d = lane < nw ? red[3][lane] : ~0ull;
+        a = warp_or(a); b = warp_or(b); c = warp_and(c); d = warp_and(d);
+        if (lane == 0 && (a | b | ~c | ~d)) {
+            if (a) atomicOr(&dst[0], a);
+            if (b) atomicOr(&dst[1], b);
+            if (~c) atomicAnd(&dst[2], c);
+            if (~d) atomicAnd(&dst[3], d);
+        }
+    }
+}
+
+// Block-aggregated append: returns this thread's slot (valid if `take`).
+__device__ __forceinline__ unsigned block_append(bool take, unsigned int* counter) {
+    __shared__ unsigned int wcnt[32];
+    __shared__ unsigned int base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+    const unsigned ballot = __ballot_sync(0xffffffffu, take);
+    if (lane == 0) wcnt[warp] = __popc(ballot);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned total = 0;
+        for (int w = 0; w < nw; w++) {
+            unsigned c = wcnt[w];
+            wcnt[w] = total;
+            total += c;
+        }
+        base = total ? atomicAdd(counter, total) : 0u;
+    }
+    __syncthreads();
+    const unsigned pos = base + wcnt[warp] + __popc(ballot & ((1u << lane) - 1));
+    __syncthreads();  // wcnt / base reused by the next call
+    return pos;
 }
 
 // Digit window just below the highest differing bit of the candidate set.
@@ -426,20 +466,12 @@ __global__ void __launch_bounds__(256) k_admit(AdmitArgs a) {
             if (a.refetch) a.refetch[i] = in && (a.now - __ldg(a.obs + i) > a.stale);
             if (a.skipped) a.skipped[i] = in ? 0 : a.skipped[i] + 1;
         }
-        if (a.sel_keys) {
-            unsigned mask = __ballot_sync(0xffffffffu, in);
-            if (mask) {
-                int lane = threadIdx.x & 31;
-                int leader = __ffs(mask) - 1;
-                unsigned bp = 0;
-                if (lane == leader) bp = atomicAdd(&a.s->sel_count, __popc(mask));
-                bp = __shfl_sync(0xffffffffu, bp, leader);
-                if (in) {
-                    unsigned pos = bp + __popc(mask & ((1u << lane) - 1));
-                    a.sel_keys[pos] = k;
-                    a.sel_idx[pos] = static_cast<int32_t>(i);
-                    oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
-                }
+        if (a.sel_keys && __syncthreads_or(in)) {
+            unsigned pos = block_append(in, &a.s->sel_count);
+            if (in) {
+                a.sel_keys[pos] = k;
+                a.sel_idx[pos] = static_cast<int32_t>(i);
+                oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
             }
         }
     }
@@ -455,46 +487,50 @@ __device__ __forceinline__ bool pair_gt(const kr_key& a, int32_t ia, const kr_ke
     return ia > ib;
 }
 
-// Single-CTA bitonic network over (key, idx), n <= kBitonicMax.
-__global__ void __launch_bounds__(1024) k_bitonic(const kr_key* keys, const int32_t* idx,
-                                                  const unsigned int* count_dev, int64_t count_host,
-                                                  int32_t* out_idx, kr_key* out_keys) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int n = count_dev ? static_cast<int>(*count_dev) : static_cast<int>(count_host);
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    kr_key* sk = reinterpret_cast<kr_key*>(smem);
-    int32_t* si = reinterpret_cast<int32_t*>(smem + sizeof(kr_key) * kBitonicMax);
-    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        if (i < n) {
-            sk[i] = keys[i];
-            si[i] = idx ? idx[i] : i;
-        } else {
-            sk[i] = kr_key{~0ull, ~0ull};
-            si[i] = INT_MAX;
-        }
-    }
+// Parallel rank sort for the admitted set: rank_i = #{j : (key_j, j) < (key_i, i)}
+// computed over a 2-D grid of (i-tile, j-tile) blocks with the j-tile staged in
+// shared memory (broadcast reads), then one scatter.  O(m^2) compares spread
+// over the whole GPU; used for m <= kRankSortMax.
+constexpr int kRankI = 256, kRankJ = 1024, kRankSortMax = 16384;
+
+__global__ void __launch_bounds__(kRankI) k_rank_count(const kr_key* keys, const unsigned int* count_dev,
+                                                       int m_host, unsigned int* rank) {
+    __shared__ kr_key sj[kRankJ];
+    const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
+    const int j0 = blockIdx.y * kRankJ;
+    if (j0 >= m) return;
+    const int jn = min(kRankJ, m - j0);
+    for (int t = threadIdx.x; t < jn; t += blockDim.x) sj[t] = keys[j0 + t];
     __syncthreads();
-    for (int k = 2; k <= np2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int pidx = threadIdx.x; pidx < np2 / 2; pidx += blockDim.x) {
-                int i = (pidx / j) * 2 * j + (pidx % j);
-                int l = i + j;
-                bool up = (i & k) == 0;
-                kr_key ka = sk[i], kb = sk[l];
-                int32_t ia = si[i], ib = si[l];
-                bool gt = pair_gt(ka, ia, kb, ib);
-                if (gt == up) {
-                    sk[i] = kb; sk[l] = ka;
-                    si[i] = ib; si[l] = ia;
-                }
-            }
-            __syncthreads();
+    const int i = blockIdx.x * kRankI + threadIdx.x;
+    if (i >= m) return;
+    const kr_key ki = keys[i];
+    unsigned int c = 0;
+    int jj = 0;
+    for (; jj + 4 <= jn; jj += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const kr_key kj = sj[jj + u];
+            const int j = j0 + jj + u;
+            c += (kj.hi < ki.hi) | ((kj.hi == ki.hi) & ((kj.lo < ki.lo) | ((kj.lo == ki.lo) & (j < i))));
         }
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        if (out_idx) out_idx[i] = si[i];
-        if (out_keys) out_keys[i] = sk[i];
+    for (; jj < jn; jj++) {
+        const kr_key kj = sj[jj];
+        const int j = j0 + jj;
+        c += (kj.hi < ki.hi) | ((kj.hi == ki.hi) & ((kj.lo < ki.lo) | ((kj.lo == ki.lo) & (j < i))));
+    }
+    if (c) atomicAdd(&rank[i], c);
+}
+
+__global__ void k_rank_scatter(const kr_key* keys, const int32_t* idx, const unsigned int* count_dev,
+                               int m_host, const unsigned int* rank, int32_t* out_idx,
+                               kr_key* out_keys) {
+    const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const unsigned r = rank[i];
+        if (out_idx) out_idx[r] = idx ? idx[i] : i;
+        if (out_keys) out_keys[r] = keys[i];
     }
 }
 
@@ -595,12 +631,14 @@ __global__ void __launch_bounds__(256) k_rs_scatter(const kr_key* keys, const in
 static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx,
                       const unsigned int* count_dev, int64_t n, int32_t* out_idx, kr_key* out_keys,
                       const unsigned long long* stats_dev, cudaStream_t st) {
-    if (n <= kBitonicMax) {
-        size_t smem = static_cast<size_t>(kBitonicMax) * (sizeof(kr_key) + sizeof(int32_t));
-        KR_CUDA_TRY(cudaFuncSetAttribute(k_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-        k_bitonic<<<1, 1024, smem, st>>>(keys, idx, count_dev, n, out_idx, out_keys);
-        return check_launch("k_bitonic");
+    if (n <= kRankSortMax) {
+        KR_CUDA_TRY(cudaMemsetAsync(w.rank, 0, n * sizeof(uint32_t), st));
+        const int m = static_cast<int>(n);
+        dim3 grid((m + kRankI - 1) / kRankI, (m + kRankJ - 1) / kRankJ);
+        k_rank_count<<<grid, kRankI, 0, st>>>(keys, count_dev, m, w.rank);
+        k_rank_scatter<<<(m + 255) / 256, 256, 0, st>>>(keys, idx, count_dev, m, w.rank, out_idx,
+                                                       out_keys);
+        return check_launch("rank sort", 2);
     }
     // window plan from OR ^ AND of the set (read back: one stream sync)
     unsigned long long s4[4];
@@ -725,7 +763,7 @@ extern "C" int kr_admit(const kr_key* keys, int64_t n, int64_t k, const kr_key* 
     if (e || !gather) return e;
     const int64_t m = k < n ? k : n;
     if (m == 0) return KR_OK;
-    return sort_pairs(w, w.skeys[0], w.sidx[0], m <= kBitonicMax ? &w.state->sel_count : nullptr,
+    return sort_pairs(w, w.skeys[0], w.sidx[0], m <= kRankSortMax ? &w.state->sel_count : nullptr,
                       m, edge_idx, edge_keys, w.state->sst, st);
 }
 
@@ -736,7 +774,7 @@ extern "C" int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_ke
     if (!keys || !ws || ws_bytes < workspace_bytes(n)) return KR_ENOSPACE;
     cudaStream_t st = as_stream(stream);
     Workspace w = carve(ws, n);
-    if (n <= kBitonicMax)
+    if (n <= kRankSortMax)
         return sort_pairs(w, keys, nullptr, nullptr, n, order, sorted_keys, nullptr, st);
     k_sel_reset<<<1, 1024, 0, st>>>(w.state, n, 0);
     k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, w.state);

@@ -53,9 +53,13 @@ __device__ __forceinline__ void stream_issue(const StreamPlan& p, unsigned char*
     int64_t nr = p.R - r0 < p.TR ? p.R - r0 : p.TR;
     unsigned char* buf = bufs + static_cast<size_t>(s) * p.stage_bytes;
     uint32_t total = 0;
-    for (int g = 0; g < p.nseg; g++) total += static_cast<uint32_t>(nr * p.rbytes[g]) & ~15u;
+#pragma unroll
+    for (int g = 0; g < kMaxSeg; g++)
+        if (g < p.nseg) total += static_cast<uint32_t>(nr * p.rbytes[g]) & ~15u;
     mbar_arrive_expect_tx(&mbar[s], total);
-    for (int g = 0; g < p.nseg; g++) {
+#pragma unroll
+    for (int g = 0; g < kMaxSeg; g++) {
+        if (g >= p.nseg) break;
         uint32_t b16 = static_cast<uint32_t>(nr * p.rbytes[g]) & ~15u;
         if (b16) bulk_g2s(buf + p.soff[g], p.base[g] + r0 * p.rbytes[g], b16, &mbar[s], pol);
     }
@@ -64,7 +68,9 @@ __device__ __forceinline__ void stream_issue(const StreamPlan& p, unsigned char*
 // Copy [from, to) bytes of every segment of tile (r0, nr) with 4-byte words.
 __device__ __forceinline__ void stream_copy_plain(const StreamPlan& p, unsigned char* buf,
                                                   int64_t r0, int64_t nr, bool tail_only) {
-    for (int g = 0; g < p.nseg; g++) {
+#pragma unroll
+    for (int g = 0; g < kMaxSeg; g++) {
+        if (g >= p.nseg) break;
         uint32_t bytes = static_cast<uint32_t>(nr * p.rbytes[g]);
         uint32_t from = tail_only ? (bytes & ~15u) : 0u;
         const uint32_t* src = reinterpret_cast<const uint32_t*>(p.base[g] + r0 * p.rbytes[g]);

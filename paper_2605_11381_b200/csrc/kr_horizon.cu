@@ -21,27 +21,27 @@
 
 namespace kr {
 
-// Warp-aggregated "first index" update: lanes scoring the same robot combine
-// their candidate indices with one shuffle-reduction; one lane per robot
-// touches shared memory.
-__device__ __forceinline__ void first_min(int* f, int rr, int idx) {
-    const unsigned active = __activemask();
-    const unsigned peers = __match_any_sync(active, rr);
-    const int m = __reduce_min_sync(peers, idx);
-    if (m != INT_MAX && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&f[rr], m);
-}
-
 // ---------------------------------------------------------------------------
 // Confidence threshold (horizon.py:108-132)
 // ---------------------------------------------------------------------------
 template <typename T>
 struct ConfWork {
-    int K, N, TR, hmin;
+    int K, N, TR, hmin, rounds;
     double opt;  // 1.0 + threshold, rounded on the host as Python does
     int32_t* H;
     uint32_t* flags;
-    FastDiv divN;
-    int* first;  // [2][TR] first tripping column per robot, INT_MAX = none
+    int* first;                  // [2][TR] first tripping column per robot
+    int rr_q[kMaxRounds];        // this thread's robot slot per round (-1: none)
+    int n_q[kMaxRounds];         // ... and column
+
+    __device__ void setup(int threads) {
+        for (int q = 0; q < kMaxRounds; q++) {
+            const int j = threadIdx.x + q * threads;
+            const bool ok = q < rounds && j < TR * N;
+            rr_q[q] = ok ? j / N : -1;
+            n_q[q] = ok ? j - (j / N) * N : 0;
+        }
+    }
 
     // Exact fp32 pre-decision of `f > opt * mean` for fp32 storage: all terms
     // are non-negative, so the fp32 threshold is within (K + 8) * 2^-24 of the
@@ -66,46 +66,50 @@ struct ConfWork {
         }
     }
 
-    __device__ void tile(const unsigned char* seg0, const unsigned char*, int64_t, int nr,
-                         int64_t local) {
-        const T* u = reinterpret_cast<const T*>(seg0);
+    __device__ __forceinline__ void tile(const TileView& v, int64_t, int nr, int64_t local) {
+        const T* u = reinterpret_cast<const T*>(v.seg[0]);
         int* f = first + (local & 1) * TR;
         uint32_t fl = 0;
         const int K1 = K - 1;
-        const double dK1 = static_cast<double>(K1);
-        const int items = nr * N;
-        for (int j = threadIdx.x; j < items; j += blockDim.x) {
-            const int rr = static_cast<int>(fdiv(static_cast<uint32_t>(j), divN));
-            const int n = j - rr * N;
-            const T* col = u + static_cast<size_t>(rr) * K * N + n;
-            // Validation (horizon.py:47-50) covers every element of the round.
-            for (int k = 0; k < K; k++) {
-                T v = col[static_cast<size_t>(k) * N];
-                if (!isfinite(v)) fl |= KR_FLAG_NONFINITE;
-                if (v < T(0)) fl |= KR_FLAG_NEGATIVE;
-            }
-            int trip = filter(col);
-            if (trip < 0) {
-                // u[:-1].mean(axis=0): sequential column add for N >= 2, numpy
-                // pairwise summation when the reduction collapses (N == 1).
-                double s;
-                if (N >= 2) {
-                    s = to_f64(col[0]);
-                    for (int k = 1; k < K1; k++) s = dadd(s, to_f64(col[static_cast<size_t>(k) * N]));
-                } else {
-                    auto a = [col](int64_t k) { return to_f64(col[k]); };
-                    s = np_pairwise_sum(a, 0, K1);
+#pragma unroll
+        for (int q = 0; q < kMaxRounds; q++) {
+            if (q >= rounds) break;
+            const int rr = rr_q[q];
+            const bool valid = rr >= 0 && rr < nr;
+            bool trip = false;
+            if (valid) {
+                const int n = n_q[q];
+                const T* col = u + static_cast<size_t>(rr) * K * N + n;
+                // Validation (horizon.py:47-50) covers every element of the round.
+                for (int k = 0; k < K; k++) {
+                    T x = col[static_cast<size_t>(k) * N];
+                    if (!isfinite(x)) fl |= KR_FLAG_NONFINITE;
+                    if (x < T(0)) fl |= KR_FLAG_NEGATIVE;
                 }
-                double m = ddiv(s, dK1);
-                double fin = to_f64(col[static_cast<size_t>(K1) * N]);
-                trip = fin > dmul(opt, m);  // strict '>' (horizon.py:127)
+                int t = filter(col);
+                if (t < 0) {
+                    // u[:-1].mean(axis=0): sequential column add for N >= 2,
+                    // numpy pairwise summation when the reduction collapses (N == 1).
+                    double sum;
+                    if (N >= 2) {
+                        sum = to_f64(col[0]);
+                        for (int k = 1; k < K1; k++)
+                            sum = dadd(sum, to_f64(col[static_cast<size_t>(k) * N]));
+                    } else {
+                        auto a = [col](int64_t k) { return to_f64(col[k]); };
+                        sum = np_pairwise_sum(a, 0, K1);
+                    }
+                    const double m = ddiv(sum, static_cast<double>(K1));
+                    t = to_f64(col[static_cast<size_t>(K1) * N]) > dmul(opt, m);  // strict '>'
+                }
+                trip = t;
             }
-            first_min(f, rr, trip ? n : INT_MAX);
+            first_flag(f, valid ? rr : -1, valid ? rr : -1, trip, n_q[q]);
         }
         if (fl && flags) atomicOr(flags, fl);
     }
 
-    __device__ void finish(int64_t r0, int nr, int64_t local) {
+    __device__ __forceinline__ void finish(int64_t r0, int nr, int64_t local) {
         int* f = first + (local & 1) * TR;
         for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
             int h = f[rr] < N ? f[rr] : N;  // argmax of trips, or N
@@ -116,13 +120,14 @@ struct ConfWork {
     }
 };
 
-template <typename T>
-__global__ void __launch_bounds__(kMaxThreads) k_horizon_confidence(StreamPlan p, ConfWork<T> w) {
+template <typename T, bool kStaged>
+__global__ void __launch_bounds__(kStreamThreads) k_horizon_confidence(StreamPlan p, ConfWork<T> w) {
     extern __shared__ __align__(128) unsigned char smem[];
     w.first = reinterpret_cast<int*>(smem + stream_aux_offset());
     for (int i = threadIdx.x; i < 2 * w.TR; i += blockDim.x) w.first[i] = INT_MAX;
+    w.setup(p.threads);
     __syncthreads();
-    stream_run(p, smem, w);
+    stream_run<kStaged>(p, smem, w);
 }
 
 // ---------------------------------------------------------------------------
@@ -130,20 +135,33 @@ __global__ void __launch_bounds__(kMaxThreads) k_horizon_confidence(StreamPlan p
 // ---------------------------------------------------------------------------
 template <typename T, int DC>
 struct DivWork {
-    int S, Lp, Lc, D, TR;
-    const int32_t *off, *lenp, *lenc;
+    int S, Lp, Lc, D, TR, rounds;
+    bool has_off, has_lp, has_lc;  // per-robot arrays present (segment slots 2, 3, 4)
     double thr;
     int32_t* H;
     double* cos;
-    FastDiv divRobot, divLc;  // S * Lc, Lc
     float thr_f, margin;
-    int* first;  // [2][TR]
-    int2* meta;  // [2][TR] (offset, limit) of each robot of the tile
+    int* first;                   // [2][TR] first failing action per robot
+    int* lim;                     // [2][TR] prefix limit per robot
+    int rr_q[kMaxRounds], s_q[kMaxRounds], i_q[kMaxRounds];
 
-    __device__ __forceinline__ int2 load_meta(int64_t r) const {
-        int o = off ? __ldg(off + r) : 0;
-        int lp = lenp ? __ldg(lenp + r) : Lp;
-        int lc = lenc ? __ldg(lenc + r) : Lc;
+    __device__ void setup(int threads) {
+        const int per = S * Lc;
+        for (int q = 0; q < kMaxRounds; q++) {
+            const int j = threadIdx.x + q * threads;
+            const bool ok = q < rounds && j < TR * per;
+            const int rr = ok ? j / per : -1;
+            const int rem = ok ? j - rr * per : 0;
+            rr_q[q] = rr;
+            s_q[q] = rem / Lc;
+            i_q[q] = rem - (rem / Lc) * Lc;
+        }
+    }
+
+    __device__ __forceinline__ int2 meta(const TileView& v, int rr) const {
+        int o = has_off ? reinterpret_cast<const int32_t*>(v.seg[2])[rr] : 0;
+        int lp = has_lp ? reinterpret_cast<const int32_t*>(v.seg[3])[rr] : Lp;
+        int lc = has_lc ? reinterpret_cast<const int32_t*>(v.seg[4])[rr] : Lc;
         o = o < 0 ? 0 : o;
         lp = lp > Lp ? Lp : lp;
         lc = lc > Lc ? Lc : (lc < 0 ? 0 : lc);
@@ -152,70 +170,76 @@ struct DivWork {
         return make_int2(o, lr < lc ? lr : lc);
     }
 
-    __device__ void tile(const unsigned char* seg0, const unsigned char* seg1, int64_t r0, int nr,
-                         int64_t local) {
-        const T* prev = reinterpret_cast<const T*>(seg0);
-        const T* cand = reinterpret_cast<const T*>(seg1);
+    __device__ __forceinline__ void tile(const TileView& v, int64_t r0, int nr, int64_t local) {
+        const T* prev = reinterpret_cast<const T*>(v.seg[0]);
+        const T* cand = reinterpret_cast<const T*>(v.seg[1]);
         int* f = first + (local & 1) * TR;
-        int2* mt = meta + (local & 1) * TR;
-        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) mt[rr] = load_meta(r0 + rr);
-        __syncthreads();
+        int* lm = lim + (local & 1) * TR;
         const int D_ = DC > 0 ? DC : D;
-        const int items = nr * S * Lc;
-        for (int j = threadIdx.x; j < items; j += blockDim.x) {
-            const int rr = static_cast<int>(fdiv(static_cast<uint32_t>(j), divRobot));
-            const int rem = j - rr * S * Lc;
-            const int s = static_cast<int>(fdiv(static_cast<uint32_t>(rem), divLc));
-            const int i = rem - s * Lc;
-            const int2 m = mt[rr];
-            int fail = INT_MAX;
-            if (i < m.y) {
-                const T* a = cand + (static_cast<size_t>(rr * S + s) * Lc + i) * D_;
-                const T* b = prev + (static_cast<size_t>(rr) * Lp + m.x + i) * D_;
-                int pass = -1;
-                if (!cos) {
-                    if constexpr (DC > 0)
-                        pass = cos_filter_fixed<DC>(a, b, thr_f, margin);
-                    else
-                        pass = cos_filter(a, b, D_, thr_f, margin);
+#pragma unroll
+        for (int q = 0; q < kMaxRounds; q++) {
+            if (q >= rounds) break;
+            const int rr = rr_q[q], s = s_q[q], i = i_q[q];
+            const bool valid = rr >= 0 && rr < nr;
+            bool fail = false;
+            if (valid) {
+                const int2 m = meta(v, rr);
+                if (i == 0 && s == 0) lm[rr] = m.y;
+                double* cp = cos ? cos + (static_cast<size_t>(r0 + rr) * S + s) * Lc + i : nullptr;
+                if (i < m.y) {
+                    const T* a = cand + (static_cast<size_t>(rr * S + s) * Lc + i) * D_;
+                    const T* b = prev + (static_cast<size_t>(rr) * Lp + m.x + i) * D_;
+                    int pass = -1;
+                    if (!cp) {
+                        if constexpr (DC > 0)
+                            pass = cos_filter_fixed<DC>(a, b, thr_f, margin);
+                        else
+                            pass = cos_filter(a, b, D_, thr_f, margin);
+                    }
+                    if (pass < 0) {
+                        double c;
+                        if constexpr (DC > 0)
+                            c = cosine_skx_fixed<DC>(a, b);
+                        else
+                            c = cosine_skx(a, b, D_);
+                        pass = !(c < thr);
+                        if (cp) *cp = c;
+                    }
+                    fail = !pass;  // the first action below threshold ends the prefix
+                } else if (cp) {
+                    *cp = __longlong_as_double(0x7ff8000000000000LL);  // NaN past the limit
                 }
-                if (pass < 0) {
-                    double c;
-                    if constexpr (DC > 0)
-                        c = cosine_skx_fixed<DC>(a, b);
-                    else
-                        c = cosine_skx(a, b, D_);
-                    pass = !(c < thr);
-                    if (cos) cos[(static_cast<size_t>(r0 + rr) * S + s) * Lc + i] = c;
-                }
-                if (!pass) fail = i;  // first action below threshold ends the prefix
-            } else if (cos) {
-                cos[(static_cast<size_t>(r0 + rr) * S + s) * Lc + i] =
-                    __longlong_as_double(0x7ff8000000000000LL);  // NaN past the limit
             }
-            first_min(f, rr, fail);
+            first_flag(f, valid ? rr : -1, valid ? rr * S + s : -1, fail, i);
         }
     }
 
-    __device__ void finish(int64_t r0, int nr, int64_t local) {
+    __device__ __forceinline__ void finish(int64_t r0, int nr, int64_t local) {
         int* f = first + (local & 1) * TR;
-        const int2* mt = meta + (local & 1) * TR;
+        const int* lm = lim + (local & 1) * TR;
         for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-            const int limit = mt[rr].y;
-            H[r0 + rr] = f[rr] < limit ? f[rr] : limit;
+            H[r0 + rr] = f[rr] < lm[rr] ? f[rr] : lm[rr];
             f[rr] = INT_MAX;
         }
     }
 };
 
-template <typename T, int DC>
-__global__ void __launch_bounds__(kMaxThreads) k_horizon_divergence(StreamPlan p, DivWork<T, DC> w) {
+// Small-D variants keep every operand in < 64 registers and may use 1024-thread
+// CTAs; D >= 16 (and runtime D) need the 32 fp64 OpenBLAS accumulators, so
+// their CTAs are capped at 256 threads (255 registers available).
+template <int DC>
+constexpr int div_max_threads() { return (DC > 0 && DC < 16) ? kStreamThreads : 256; }
+
+template <typename T, int DC, bool kStaged>
+__global__ void __launch_bounds__(div_max_threads<DC>()) k_horizon_divergence(StreamPlan p,
+                                                                             DivWork<T, DC> w) {
     extern __shared__ __align__(128) unsigned char smem[];
     w.first = reinterpret_cast<int*>(smem + stream_aux_offset());
-    w.meta = reinterpret_cast<int2*>(smem + stream_aux_offset() + 2 * w.TR * sizeof(int));
+    w.lim = w.first + 2 * w.TR;
     for (int i = threadIdx.x; i < 2 * w.TR; i += blockDim.x) w.first[i] = INT_MAX;
+    w.setup(p.threads);
     __syncthreads();
-    stream_run(p, smem, w);
+    stream_run<kStaged>(p, smem, w);
 }
 
 __global__ void k_horizon_static(int64_t R, int32_t h, int32_t* H) {
@@ -227,13 +251,17 @@ __global__ void k_horizon_static(int64_t R, int32_t h, int32_t* H) {
 // ---------------------------------------------------------------------------
 // Launch planning
 // ---------------------------------------------------------------------------
-// Tile sizing.  A tile is TR robots; its work items (columns / actions) are
-// spread over the CTA's threads, so TR is chosen to keep the last round of
-// items nearly full, each stage 8-48 KB, TMA-alignable (TR * row bytes a
-// multiple of 16) and the whole ring small enough for two CTAs per SM (16
-// warps to hide the scoring latency; 3-4 stages keep >= 2 tiles in flight).
+// Tile shape search.  For each candidate TR (robots per tile) the CTA gets
+// ceil(TR * items / rounds) threads (rounds <= 4, a multiple of 32) so every
+// thread owns fixed positions.  Residency (CTAs per SM) is bounded by the
+// kernel's register count, the 2048-thread limit and shared memory; the TMA
+// ring then takes as many stages as fit (up to 8).  Score: idle-lane fraction,
+// plus penalties for < 160 KB of TMA bytes in flight per SM (the loaded HBM
+// latency times the per-SM share of bandwidth), < 24 resident warps per SM,
+// and tiles that cannot be moved by TMA.
 static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* rbytes, int64_t R,
-                            int items_per_robot, uint32_t aux_per_robot) {
+                            int items_per_robot, uint32_t aux_per_robot, int max_threads,
+                            int regs_per_thread) {
     const DeviceInfo& di = device_info();
     StreamPlan p{};
     p.nseg = nseg;
@@ -242,7 +270,7 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
     for (int g = 0; g < nseg; g++) {
         p.base[g] = static_cast<const unsigned char*>(base[g]);
         p.rbytes[g] = static_cast<uint32_t>(rbytes[g]);
-        base_ok = base_ok && aligned16(base[g]);
+        if (rbytes[g]) base_ok = base_ok && aligned16(base[g]);
     }
     auto stage_bytes = [&](int64_t t) {
         uint64_t b = 0;
@@ -254,67 +282,91 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
             if ((t * rbytes[g]) % 16) return false;
         return base_ok;
     };
-    const uint64_t smem_max = static_cast<uint64_t>(di.max_smem_optin) - 1024;
-    int best_tr = 0, best_stages = 0;
-    double best_score = 1e30;
-    for (int per_sm = 2; per_sm >= 1 && best_tr == 0; per_sm--) {
-        const uint64_t budget = smem_max / per_sm - 1024;
-        for (int64_t t = 1; t <= 1024 && t <= R + 1; t++) {
-            const uint64_t sb = stage_bytes(t);
-            const uint64_t aux = (256 + t * aux_per_robot + 127) & ~uint64_t(127);
-            if (t > 1 && sb > 48 * 1024) break;
-            if (2 * sb + aux > budget) break;
-            int stages = static_cast<int>((budget - aux) / sb);
-            stages = stages > 4 ? 4 : stages;
-            const int64_t items = t * items_per_robot;
-            const int64_t rounds = (items + kMaxThreads - 1) / kMaxThreads;
-            double score = 1.0 - static_cast<double>(items) / (rounds * kMaxThreads);
-            if (sb < 12 * 1024) score += 0.05;                 // tiny tiles: per-tile overhead
-            if (!tma_ok(t)) score += 1.0;                       // plain staging is much slower
-            if (score < best_score - 1e-9 || (score < best_score + 1e-9 && t > best_tr)) {
-                best_score = score;
-                best_tr = static_cast<int>(t);
-                best_stages = stages;
-            }
+    const int regs = ((regs_per_thread > 0 ? regs_per_thread : 64) + 7) / 8 * 8;
+    const uint64_t smem_sm = static_cast<uint64_t>(di.max_smem_optin) + 1024;  // per-SM pool
+    const double kInflightTarget = 160.0 * 1024;
+    double best = 1e30;
+    for (int64_t t = 1; t <= 1024; t++) {
+        const int64_t items = t * items_per_robot;
+        if (items > static_cast<int64_t>(max_threads) * kMaxRounds) break;
+        const int rounds = static_cast<int>((items + max_threads - 1) / max_threads);
+        const int threads = static_cast<int>(((items + rounds - 1) / rounds + 31) / 32 * 32);
+        const uint64_t sb = stage_bytes(t);
+        const uint64_t aux = (256 + t * aux_per_robot + 127) & ~uint64_t(127);
+        const bool tma = tma_ok(t);
+        int per_sm = 65536 / (regs * threads);
+        per_sm = per_sm < 2048 / threads ? per_sm : 2048 / threads;
+        per_sm = per_sm > 4 ? 4 : per_sm;
+        for (; per_sm >= 1; per_sm--) {
+            const uint64_t budget = smem_sm / per_sm - 1024 - 128;  // 1 KB reserved per CTA
+            if (aux + 2 * sb <= budget) break;
+        }
+        if (per_sm < 1) continue;
+        const uint64_t budget = smem_sm / per_sm - 1024 - 128;
+        int stages = static_cast<int>((budget - aux) / sb);
+        stages = stages > 8 ? 8 : stages;
+        const double inflight = static_cast<double>(per_sm) * (stages - 1) * sb;
+        const double warps = per_sm * threads / 32.0;
+        double score = 1.0 - static_cast<double>(items) / (static_cast<double>(rounds) * threads);
+        if (inflight < kInflightTarget) score += 0.5 * (1.0 - inflight / kInflightTarget);
+        if (warps < 24.0) score += 0.2 * (1.0 - warps / 24.0);
+        if (!tma) score += 1.0;
+        if (score < best - 1e-9) {
+            best = score;
+            p.TR = static_cast<int>(t);
+            p.threads = threads;
+            p.rounds = rounds;
+            p.stages = stages;
+            p.mode = tma ? kModeBulk : kModePlain;
         }
     }
-    if (best_tr == 0) {  // robot larger than two stages of shared memory: score from global
+    if (best > 1e29) {  // robot larger than two stages of shared memory: score from global
         p.TR = 1;
+        p.rounds = static_cast<int>((items_per_robot + max_threads - 1) / max_threads);
+        if (p.rounds > kMaxRounds) p.rounds = kMaxRounds;  // caller guarantees it fits
+        p.threads = static_cast<int>(((items_per_robot + p.rounds - 1) / p.rounds + 31) / 32 * 32);
         p.stages = 1;
         p.mode = kModeDirect;
         p.aux_bytes = 256 + aux_per_robot;
         p.stage_bytes = 0;
         return p;
     }
-    p.TR = best_tr;
-    p.stages = best_stages;
-    p.aux_bytes = static_cast<uint32_t>(256 + best_tr * aux_per_robot);
+    p.aux_bytes = static_cast<uint32_t>(256 + p.TR * aux_per_robot);
     uint32_t off = 0;
     for (int g = 0; g < nseg; g++) {
         p.soff[g] = off;
-        off += static_cast<uint32_t>(((uint64_t)best_tr * rbytes[g] + 127) & ~uint64_t(127));
+        off += static_cast<uint32_t>(((uint64_t)p.TR * rbytes[g] + 127) & ~uint64_t(127));
     }
     p.stage_bytes = off;
-    p.mode = tma_ok(best_tr) ? kModeBulk : kModePlain;
     if (p.mode == kModePlain) p.stages = 1;
     return p;
 }
 
-template <class Kern, class Work>
-static int launch_stream(Kern kern, const StreamPlan& p, const Work& w, cudaStream_t st,
-                         const char* name) {
+template <class K>
+static int kernel_regs(K kern) {
+    cudaFuncAttributes a{};
+    if (cudaFuncGetAttributes(&a, kern) != cudaSuccess) return 64;
+    return a.numRegs;
+}
+
+template <class Work, class KStaged, class KDirect>
+static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, const Work& w,
+                         cudaStream_t st, const char* name) {
     size_t smem = stream_smem_bytes(p);
-    KR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-    int per_sm = 0;
-    KR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMaxThreads, smem));
-    if (per_sm < 1) per_sm = 1;
-    int64_t ntiles = (p.R + p.TR - 1) / p.TR;
-    int64_t grid = static_cast<int64_t>(device_info().sm_count) * per_sm;
-    if (grid > ntiles) grid = ntiles;
-    if (grid < 1) grid = 1;
-    kern<<<static_cast<unsigned>(grid), kMaxThreads, smem, st>>>(p, w);
-    return check_launch(name);
+    auto go = [&](auto kern) -> int {
+        KR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+        int per_sm = 0;
+        KR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, p.threads, smem));
+        if (per_sm < 1) per_sm = 1;
+        int64_t ntiles = (p.R + p.TR - 1) / p.TR;
+        int64_t grid = static_cast<int64_t>(device_info().sm_count) * per_sm;
+        if (grid > ntiles) grid = ntiles;
+        if (grid < 1) grid = 1;
+        kern<<<static_cast<unsigned>(grid), p.threads, smem, st>>>(p, w);
+        return check_launch(name);
+    };
+    return p.mode == kModeDirect ? go(kdirect) : go(kstaged);
 }
 
 }  // namespace kr
@@ -341,35 +393,41 @@ extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_
     if (!U || !H) return KR_EINVAL;
     const size_t es = dtype == KR_F64 ? 8 : 4;
     uint64_t rb = static_cast<uint64_t>(K) * N * es;
+    if (N > kStreamThreads * kMaxRounds) return KR_EINVAL;
     const void* bases[1] = {U};
-    StreamPlan p = make_plan(1, bases, &rb, R, N, 2 * sizeof(int));
+    const int regs = dtype == KR_F64 ? kernel_regs(k_horizon_confidence<double, true>)
+                                     : kernel_regs(k_horizon_confidence<float, true>);
+    StreamPlan p = make_plan(1, bases, &rb, R, N, 2 * sizeof(int), kStreamThreads, regs);
     cudaStream_t st = as_stream(stream);
-    const FastDiv dN = make_fastdiv(static_cast<uint32_t>(N));
     if (dtype == KR_F64) {
-        ConfWork<double> w{K, N, p.TR, min_horizon, one_plus_t, H, flags, dN, nullptr};
-        return launch_stream(k_horizon_confidence<double>, p, w, st, "kr_horizon_confidence");
+        ConfWork<double> w{K, N, p.TR, min_horizon, p.rounds, one_plus_t, H, flags, nullptr, {}, {}};
+        return launch_stream(k_horizon_confidence<double, true>, k_horizon_confidence<double, false>,
+                             p, w, st, "kr_horizon_confidence");
     }
-    ConfWork<float> w{K, N, p.TR, min_horizon, one_plus_t, H, flags, dN, nullptr};
-    return launch_stream(k_horizon_confidence<float>, p, w, st, "kr_horizon_confidence");
+    ConfWork<float> w{K, N, p.TR, min_horizon, p.rounds, one_plus_t, H, flags, nullptr, {}, {}};
+    return launch_stream(k_horizon_confidence<float, true>, k_horizon_confidence<float, false>, p,
+                         w, st, "kr_horizon_confidence");
 }
 
 template <typename T>
 static int launch_div(const StreamPlan& p, const DivWork<T, 0>& w0, cudaStream_t st) {
+    auto with = [&](auto proto) {
+        decltype(proto) w{w0.S, w0.Lp, w0.Lc, w0.D, w0.TR, w0.rounds, w0.has_off, w0.has_lp,
+                          w0.has_lc, w0.thr, w0.H, w0.cos, w0.thr_f, w0.margin, nullptr, nullptr,
+                          {}, {}, {}};
+        return w;
+    };
     switch (w0.D) {
-        case 7: {
-            DivWork<T, 7> w{w0.S, w0.Lp, w0.Lc, w0.D, w0.TR, w0.off, w0.lenp, w0.lenc,
-                            w0.thr, w0.H, w0.cos, w0.divRobot, w0.divLc, w0.thr_f, w0.margin,
-                            nullptr, nullptr};
-            return launch_stream(k_horizon_divergence<T, 7>, p, w, st, "kr_horizon_divergence");
-        }
-        case 32: {
-            DivWork<T, 32> w{w0.S, w0.Lp, w0.Lc, w0.D, w0.TR, w0.off, w0.lenp, w0.lenc,
-                             w0.thr, w0.H, w0.cos, w0.divRobot, w0.divLc, w0.thr_f, w0.margin,
-                             nullptr, nullptr};
-            return launch_stream(k_horizon_divergence<T, 32>, p, w, st, "kr_horizon_divergence");
-        }
+        case 7:
+            return launch_stream(k_horizon_divergence<T, 7, true>, k_horizon_divergence<T, 7, false>,
+                                 p, with(DivWork<T, 7>{}), st, "kr_horizon_divergence");
+        case 32:
+            return launch_stream(k_horizon_divergence<T, 32, true>,
+                                 k_horizon_divergence<T, 32, false>, p, with(DivWork<T, 32>{}), st,
+                                 "kr_horizon_divergence");
         default:
-            return launch_stream(k_horizon_divergence<T, 0>, p, w0, st, "kr_horizon_divergence");
+            return launch_stream(k_horizon_divergence<T, 0, true>, k_horizon_divergence<T, 0, false>,
+                                 p, w0, st, "kr_horizon_divergence");
     }
 }
 
@@ -392,19 +450,35 @@ extern "C" int kr_horizon_divergence(const void* prev, const void* cand, int dty
             KR_CUDA_TRY(cudaMemsetAsync(cos, 0xFF, R * S * Lc * sizeof(double), st));
         return KR_OK;
     }
-    const void* bases[2] = {prev, cand};
-    StreamPlan p = make_plan(2, bases, rb, R, S * Lc, 2 * sizeof(int) + 2 * sizeof(int2));
+    if (static_cast<int64_t>(S) * Lc > static_cast<int64_t>(kStreamThreads) * kMaxRounds)
+        return KR_EINVAL;
+    // segments: action rows, then the per-robot metadata that travels with them
+    const void* bases[5] = {prev, cand, offset, len_prev, len_cand};
+    uint64_t rbs[5] = {rb[0], rb[1], offset ? 4u : 0u, len_prev ? 4u : 0u, len_cand ? 4u : 0u};
+    const int nseg = 5;
+    const int maxt = D == 7 ? kStreamThreads : 256;  // only D = 7 has a small-D kernel
+    if (static_cast<int64_t>(S) * Lc > static_cast<int64_t>(maxt) * kMaxRounds) return KR_EINVAL;
+    int regs;
+    if (dtype == KR_F64)
+        regs = D == 7 ? kernel_regs(k_horizon_divergence<double, 7, true>)
+                      : (D == 32 ? kernel_regs(k_horizon_divergence<double, 32, true>)
+                                 : kernel_regs(k_horizon_divergence<double, 0, true>));
+    else
+        regs = D == 7 ? kernel_regs(k_horizon_divergence<float, 7, true>)
+                      : (D == 32 ? kernel_regs(k_horizon_divergence<float, 32, true>)
+                                 : kernel_regs(k_horizon_divergence<float, 0, true>));
+    StreamPlan p = make_plan(nseg, bases, rbs, R, S * Lc, 4 * sizeof(int), maxt, regs);
     cudaStream_t st = as_stream(stream);
-    const FastDiv dR = make_fastdiv(static_cast<uint32_t>(S * Lc));
-    const FastDiv dL = make_fastdiv(static_cast<uint32_t>(Lc));
     const float thr_f = static_cast<float>(thr);
     const float margin = cos_filter_margin(D);
     if (dtype == KR_F64) {
-        DivWork<double, 0> w{S, Lp, Lc, D, p.TR, offset, len_prev, len_cand, thr, H, cos,
-                             dR, dL, thr_f, margin, nullptr, nullptr};
+        DivWork<double, 0> w{S, Lp, Lc, D, p.TR, p.rounds, offset != nullptr, len_prev != nullptr,
+                             len_cand != nullptr, thr, H, cos, thr_f, margin, nullptr, nullptr,
+                             {}, {}, {}};
         return launch_div(p, w, st);
     }
-    DivWork<float, 0> w{S, Lp, Lc, D, p.TR, offset, len_prev, len_cand, thr, H, cos,
-                        dR, dL, thr_f, margin, nullptr, nullptr};
+    DivWork<float, 0> w{S, Lp, Lc, D, p.TR, p.rounds, offset != nullptr, len_prev != nullptr,
+                        len_cand != nullptr, thr, H, cos, thr_f, margin, nullptr, nullptr,
+                        {}, {}, {}};
     return launch_div(p, w, st);
 }

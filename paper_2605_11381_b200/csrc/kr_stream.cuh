@@ -2,27 +2,35 @@
 // tensors.
 //
 // The horizon kernels read each robot's block exactly once: a contiguous byte
-// range per input tensor (segment).  A tile is TR consecutive robots, i.e. one
-// contiguous range per segment, so one elected thread moves a whole tile into
-// shared memory with one `cp.async.bulk` (1-D TMA) per segment, completion
-// tracked by a per-stage mbarrier.  STAGES tiles are in flight per CTA while the
-// other threads score the tile that already landed; one CTA per SM slot loops
-// over tiles round-robin (grid = SMs x resident CTAs).
+// range per input tensor (segment: the action rows, plus small per-robot
+// metadata arrays such as the overlap offset, which therefore arrive in shared
+// memory together with the rows they describe).  A tile is TR consecutive
+// robots, i.e. one contiguous range per segment, so one elected thread moves a
+// whole tile into shared memory with one `cp.async.bulk` (1-D TMA) per
+// segment, completion tracked by a per-stage mbarrier.  STAGES tiles are in
+// flight per CTA while the CTA's threads score the tile that already landed.
+// The block size is matched to the tile: each thread owns the same few
+// (robot slot, column/action) positions of every tile, so no index arithmetic
+// runs per tile.  CTAs loop over tiles round-robin (grid = SMs x resident CTAs).
 //
-// Fallbacks: a base pointer that is not 16-byte aligned (or a tile size that is
-// not a multiple of 16 bytes) stages with plain loads; a robot too large for
-// two stages of shared memory is scored straight from global memory.
+// Fallbacks: a base pointer that is not 16-byte aligned (or a tile that is not
+// a multiple of 16 bytes) stages with plain loads; a robot too large for two
+// stages of shared memory is scored straight from global memory.
 #pragma once
 
 #include "kr_common.cuh"
 
 namespace kr {
 
-constexpr int kMaxSeg = 2;
+constexpr int kMaxSeg = 5;
+constexpr int kMaxRounds = 4;      // item positions per thread per tile
+constexpr int kStreamThreads = 1024;
 
+// Segments have fixed slots (unused slots: rbytes 0) so that every segment
+// pointer is a compile-time-indexed register, never a local-memory array.
 struct StreamPlan {
     const unsigned char* base[kMaxSeg];  // global base of each segment
-    uint32_t rbytes[kMaxSeg];            // bytes per robot in each segment
+    uint32_t rbytes[kMaxSeg];            // bytes per robot in each segment (0: unused slot)
     uint32_t soff[kMaxSeg];              // offset of each segment in a stage buffer
     uint32_t stage_bytes;                // bytes per stage buffer (multiple of 128)
     uint32_t aux_bytes;                  // per-CTA scratch (after the mbarriers)
@@ -30,6 +38,8 @@ struct StreamPlan {
     int TR;                              // robots per tile
     int stages;
     int mode;                            // 0 = TMA bulk, 1 = plain staged, 2 = direct
+    int threads;                         // CTA size
+    int rounds;                          // ceil(TR * items_per_robot / threads) <= kMaxRounds
     int64_t R;
 };
 
@@ -45,23 +55,19 @@ __host__ inline size_t stream_smem_bytes(const StreamPlan& p) {
     return stream_buf_offset(p) + static_cast<size_t>(p.stages) * p.stage_bytes;
 }
 
-__device__ __forceinline__ void stream_issue(const StreamPlan& p, unsigned char* bufs,
-                                             uint64_t* mbar, int64_t local, uint64_t pol) {
-    int s = static_cast<int>(local % p.stages);
+__device__ __forceinline__ void stream_issue(const StreamPlan& p, unsigned char* buf,
+                                             uint64_t* bar, int64_t local, uint64_t pol) {
     int64_t t = blockIdx.x + local * gridDim.x;
     int64_t r0 = t * p.TR;
     int64_t nr = p.R - r0 < p.TR ? p.R - r0 : p.TR;
-    unsigned char* buf = bufs + static_cast<size_t>(s) * p.stage_bytes;
     uint32_t total = 0;
 #pragma unroll
-    for (int g = 0; g < kMaxSeg; g++)
-        if (g < p.nseg) total += static_cast<uint32_t>(nr * p.rbytes[g]) & ~15u;
-    mbar_arrive_expect_tx(&mbar[s], total);
+    for (int g = 0; g < kMaxSeg; g++) total += static_cast<uint32_t>(nr * p.rbytes[g]) & ~15u;
+    mbar_arrive_expect_tx(bar, total);
 #pragma unroll
     for (int g = 0; g < kMaxSeg; g++) {
-        if (g >= p.nseg) break;
         uint32_t b16 = static_cast<uint32_t>(nr * p.rbytes[g]) & ~15u;
-        if (b16) bulk_g2s(buf + p.soff[g], p.base[g] + r0 * p.rbytes[g], b16, &mbar[s], pol);
+        if (b16) bulk_g2s(buf + p.soff[g], p.base[g] + r0 * p.rbytes[g], b16, bar, pol);
     }
 }
 
@@ -70,7 +76,7 @@ __device__ __forceinline__ void stream_copy_plain(const StreamPlan& p, unsigned 
                                                   int64_t r0, int64_t nr, bool tail_only) {
 #pragma unroll
     for (int g = 0; g < kMaxSeg; g++) {
-        if (g >= p.nseg) break;
+        if (p.rbytes[g] == 0) continue;
         uint32_t bytes = static_cast<uint32_t>(nr * p.rbytes[g]);
         uint32_t from = tail_only ? (bytes & ~15u) : 0u;
         const uint32_t* src = reinterpret_cast<const uint32_t*>(p.base[g] + r0 * p.rbytes[g]);
@@ -80,20 +86,25 @@ __device__ __forceinline__ void stream_copy_plain(const StreamPlan& p, unsigned 
     }
 }
 
+struct TileView {
+    const unsigned char* seg[kMaxSeg];  // segment bases of robot r0 (shared or global)
+};
+
 // Work must provide:
-//   __device__ void tile(const unsigned char* seg0, const unsigned char* seg1,
-//                        int64_t r0, int nr, int64_t local);
+//   __device__ void tile(const TileView& v, int64_t r0, int nr, int64_t local);
 //   __device__ void finish(int64_t r0, int nr, int64_t local);
-// `tile` sees the segment bases of robot r0 (shared or global memory).
-template <class Work>
+// kStaged selects shared-memory staging (TMA bulk or plain) at compile time so
+// that the scoring loads compile to LDS; !kStaged reads global memory.
+template <bool kStaged, class Work>
 __device__ __forceinline__ void stream_run(const StreamPlan& p, unsigned char* smem, Work& work) {
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
     unsigned char* bufs = smem + stream_buf_offset(p);
-    int64_t ntiles = (p.R + p.TR - 1) / p.TR;
+    const int64_t ntiles = (p.R + p.TR - 1) / p.TR;
     if (blockIdx.x >= ntiles) return;
-    int64_t nlocal = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t nlocal = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     uint64_t pol = 0;
-    if (p.mode == kModeBulk) {
+    const bool bulk = kStaged && p.mode == kModeBulk;
+    if (bulk) {
         pol = policy_evict_first();
         if (threadIdx.x == 0) {
             for (int s = 0; s < p.stages; s++) mbar_init(&mbar[s], 1);
@@ -102,22 +113,23 @@ __device__ __forceinline__ void stream_run(const StreamPlan& p, unsigned char* s
         __syncthreads();
         if (threadIdx.x == 0) {
             int64_t pre = nlocal < p.stages ? nlocal : p.stages;
-            for (int64_t i = 0; i < pre; i++) stream_issue(p, bufs, mbar, i, pol);
+            for (int64_t i = 0; i < pre; i++)
+                stream_issue(p, bufs + static_cast<size_t>(i) * p.stage_bytes, &mbar[i], i, pol);
         }
     }
+    int s = 0;           // ring slot of tile i
+    uint32_t phase = 0;  // mbarrier parity of that slot's current fill
     for (int64_t i = 0; i < nlocal; i++) {
-        int s = static_cast<int>(i % p.stages);
-        int64_t t = blockIdx.x + i * gridDim.x;
-        int64_t r0 = t * p.TR;
-        int nr = static_cast<int>(p.R - r0 < p.TR ? p.R - r0 : p.TR);
+        const int64_t r0 = (blockIdx.x + i * gridDim.x) * p.TR;
+        const int nr = static_cast<int>(p.R - r0 < p.TR ? p.R - r0 : p.TR);
         unsigned char* buf = bufs + static_cast<size_t>(s) * p.stage_bytes;
-        const unsigned char *seg0, *seg1;
-        if (p.mode == kModeDirect) {
-            seg0 = p.base[0] + r0 * p.rbytes[0];
-            seg1 = p.nseg > 1 ? p.base[1] + r0 * p.rbytes[1] : nullptr;
+        TileView v;
+        if constexpr (!kStaged) {
+#pragma unroll
+            for (int g = 0; g < kMaxSeg; g++) v.seg[g] = p.base[g] + r0 * p.rbytes[g];
         } else {
-            if (p.mode == kModeBulk) {
-                mbar_wait(&mbar[s], static_cast<uint32_t>((i / p.stages) & 1));
+            if (bulk) {
+                mbar_wait(&mbar[s], phase);
                 if (nr < p.TR) {  // tail tile: sub-16-byte remainder by hand
                     stream_copy_plain(p, buf, r0, nr, true);
                     __syncthreads();
@@ -126,17 +138,39 @@ __device__ __forceinline__ void stream_run(const StreamPlan& p, unsigned char* s
                 stream_copy_plain(p, buf, r0, nr, false);
                 __syncthreads();
             }
-            seg0 = buf + p.soff[0];
-            seg1 = p.nseg > 1 ? buf + p.soff[1] : nullptr;
+#pragma unroll
+            for (int g = 0; g < kMaxSeg; g++) v.seg[g] = buf + p.soff[g];
         }
-        work.tile(seg0, seg1, r0, nr, i);
+        work.tile(v, r0, nr, i);
         // Order this tile's generic-proxy shared-memory traffic before the TMA
         // refill of the same buffer.
-        if (p.mode == kModeBulk) fence_proxy_async_smem();
+        if (bulk) fence_proxy_async_smem();
         __syncthreads();
-        if (p.mode == kModeBulk && threadIdx.x == 0 && i + p.stages < nlocal)
-            stream_issue(p, bufs, mbar, i + p.stages, pol);
-        work.finish(r0, nr, i);
+        if (bulk && threadIdx.x == 0 && i + p.stages < nlocal)
+            stream_issue(p, buf, &mbar[s], i + p.stages, pol);
+        work.finish(r0, nr, i);  // must not touch the (possibly refilling) buffer
+        if (++s == p.stages) {
+            s = 0;
+            phase ^= 1u;
+        }
+    }
+}
+
+// First flagged index per robot for one round of items.  Items are ordered
+// (robot, sample, index), so the lanes of a warp that score the same row
+// (`run` = robot * S + sample) form one contiguous run with increasing index;
+// the lowest flagged lane of a run carries the run's smallest index and is the
+// only lane that touches shared memory.  Must be called by all 32 lanes.
+__device__ __forceinline__ void first_flag(int* f, int rr, int run, bool flag, int idx) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    const int prev_run = __shfl_up_sync(0xffffffffu, run, 1);
+    const unsigned bnd = __ballot_sync(0xffffffffu, lane == 0 || prev_run != run);
+    const unsigned fb = __ballot_sync(0xffffffffu, flag);
+    if (flag) {
+        const unsigned run_lo = 31 - __clz(bnd & (lt | (1u << lane)));  // my run's first lane
+        const unsigned below = lt & ~((1u << run_lo) - 1);              // run lanes below me
+        if ((fb & below) == 0) atomicMin(&f[rr], idx);
     }
 }
 

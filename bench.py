@@ -207,8 +207,16 @@ def run_ours(args, world, rank, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    graphs = world == 1 and not args.no_graph
+    n_cap0 = lib.kr_launch_count()
+    if graphs:
+        rnd.capture(fleet, inputs)   # CUDA graphs: horizons | urgency + admission
+        per_round = (lib.kr_launch_count() - n_cap0) // 2  # warm-up run + capture
     for _ in range(args.warmup):
-        rnd.run(fleet, inputs)
+        if graphs:
+            rnd.replay()
+        else:
+            rnd.run(fleet, inputs)
     barrier()
 
     # timed region: K whole rounds; divergence kernel bracketed by events
@@ -221,13 +229,19 @@ def run_ours(args, world, rank, local_rank):
         start.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
-            rnd.horizons(inputs)
+            if graphs:
+                rnd.g_horizon.replay()
+            else:
+                rnd.horizons(inputs)
             ev[i][1].record(stream)
-            rnd.urgency(fleet)
-            rnd.admit(fleet)
+            if graphs:
+                rnd.g_decide.replay()
+            else:
+                rnd.urgency(fleet)
+                rnd.admit(fleet)
         end.record(stream)
         barrier()
-    launches = lib.kr_launch_count() - n0
+    launches = per_round * args.steps if graphs else lib.kr_launch_count() - n0
     elapsed = start.elapsed_time(end) / 1e3
     div_ms = [a.elapsed_time(b) for a, b in ev]
     t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
@@ -242,7 +256,13 @@ def run_ours(args, world, rank, local_rank):
     rnd.urgency(fleet); e[2].record(stream); rnd.admit(fleet); e[3].record(stream)
     torch.cuda.synchronize()
     breakdown = {"horizon_divergence_ms": e[0].elapsed_time(e[1]),
-                 "urgency_ms": e[1].elapsed_time(e[2]), "admission_ms": e[2].elapsed_time(e[3])}
+                 "urgency_ms": e[1].elapsed_time(e[2]), "admission_ms": e[2].elapsed_time(e[3]),
+                 "note": "one eager (non-graph) round; launch-rate bound for the small kernels"}
+    if graphs:
+        gd = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        gd[0].record(stream); rnd.g_decide.replay(); gd[1].record(stream)
+        torch.cuda.synchronize()
+        breakdown["urgency_plus_admission_graph_ms"] = gd[0].elapsed_time(gd[1])
 
     e2e = run_e2e(args, world, soa, prev, cand, off, sched) if not args.no_e2e else None
 
@@ -266,6 +286,7 @@ def run_ours(args, world, rank, local_rank):
                      "traffic_source": traffic_src},
         "kernels": breakdown,
         "gpu_launches": int(launches),
+        "cuda_graphs": bool(graphs),
         "clocks": clk.summary(),
     }
     if e2e:
@@ -301,13 +322,20 @@ def run_e2e(args, world, soa, prev, cand, off, sched):
     h2d = sum(t.numel() * t.element_size() for t in [h_prev, h_cand, h_off, *h_soa.values()])
     d2h = sum(t.numel() * t.element_size() for t in outs.values())
 
+    inputs = rounds.DivergenceInputs(d_prev, d_cand, THR, offset=d_off)
+    graphs = world == 1 and not args.no_graph
+    if graphs:
+        for k, v in h_soa.items():
+            d_soa[k].copy_(v)
+        rnd.capture(fleet, inputs)
+
     def step():
         d_prev.copy_(h_prev, non_blocking=True)
         d_cand.copy_(h_cand, non_blocking=True)
         d_off.copy_(h_off, non_blocking=True)
         for k, v in h_soa.items():
             d_soa[k].copy_(v, non_blocking=True)
-        o = rnd.run(fleet, rounds.DivergenceInputs(d_prev, d_cand, THR, offset=d_off))
+        o = rnd.replay() if graphs else rnd.run(fleet, inputs)
         outs["H"].copy_(o.horizon, non_blocking=True)
         outs["need"].copy_(o.need_time, non_blocking=True)
         outs["adm"].copy_(o.admitted, non_blocking=True)
@@ -347,6 +375,7 @@ def main():
     ap.add_argument("--k", type=int, default=K_DEFAULT)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-robots", type=int, default=16384)

@@ -15,6 +15,7 @@
  *   kr_urgency              waiting.py:69-93 + scheduler.py:79-140,143-157
  *                           ledger, wait ratio, bucket, exec estimate, sort key
  *   kr_topk_select          scheduler.py:204-207 edge prefix S_e = order[:k]
+ *   kr_select_admit         scheduler.py:193-241 select + admission + ordered S_e
  *   kr_admit                scheduler.py:223-234 refetch + skip counters
  *   kr_sort_keys            scheduler.py:130-140 the total order itself
  *
@@ -140,7 +141,11 @@ KR_API int kr_assign_bucket(const double* wr, const int32_t* skipped, int64_t n,
  * ledger records none (WaitLedger.waits, waiting.py:82-92). */
 KR_API int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys, int64_t* need_time,
                int64_t* total_wait, double* wr, int32_t* bucket, int64_t* est,
-               int64_t* slot_wait, uint32_t* flags, void* stream);
+               int64_t* slot_wait, unsigned long long* key_stats, uint32_t* flags, void* stream);
+/* key_stats (nullable, 4 words, prepared by kr_key_stats_init) accumulates
+ * {OR hi, OR lo, AND hi, AND lo} of the keys written, so the admission select
+ * needs no extra pass over the keys. */
+KR_API int kr_key_stats_init(unsigned long long* key_stats, void* stream);
 
 /* ---- step 3: priority ordering + top-k admission ---------------------- */
 
@@ -148,8 +153,9 @@ KR_API int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys, 
 KR_API size_t kr_workspace_bytes(int64_t n);
 /* Device-side k-th smallest key (MSD radix select).  *kth is undefined for
  * k == 0; for k >= n it is the all-ones key. */
-KR_API int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth, void* workspace,
-                   size_t workspace_bytes, void* stream);
+KR_API int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth,
+                          const unsigned long long* key_stats, void* workspace,
+                          size_t workspace_bytes, void* stream);
 /* Admission pass over n keys (scheduler.py:204-207, 223-234):
  *   admitted[i] = k > 0 && (kth == NULL || key_i <= *kth)
  * (kth NULL with k > 0 admits everything, i.e. k >= n), refetch[i] = admitted
@@ -163,6 +169,16 @@ KR_API int kr_admit(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
              const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
              int32_t* edge_idx, kr_key* edge_keys, void* workspace, size_t workspace_bytes,
              void* stream);
+/* Fused top-k admission (the production path): select the k-th key, admit
+ * key <= kth with masks / refetch / skip counters, and write S_e ordered into
+ * edge_idx / edge_keys (the admitted keys are gathered straight into the
+ * select's level-0 bin order and each bin is sorted in shared memory).
+ * kth_out (nullable) receives the k-th key.  key_stats as for kr_topk_select. */
+KR_API int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
+                           const unsigned long long* key_stats, const kr_fleet* fleet,
+                           const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
+                           int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* workspace,
+                           size_t workspace_bytes, void* stream);
 /* Full argsort of n unique keys (ascending).  Synchronises `stream` once
  * when n exceeds the single-CTA limit (pass plan read back to the host). */
 KR_API int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_key* sorted_keys,

@@ -62,9 +62,13 @@ _SIGNATURES = {
     "kr_wait_ratio": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "kr_assign_bucket": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
     "kr_urgency": (ctypes.c_int, [ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _vp, _vp,
-                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "kr_key_stats_init": (ctypes.c_int, [_vp, _vp]),
     "kr_workspace_bytes": (ctypes.c_size_t, [_i64]),
-    "kr_topk_select": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
+    "kr_topk_select": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "kr_select_admit": (ctypes.c_int, [_vp, _i64, _i64, _vp, ctypes.POINTER(KrFleet),
+                                       ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp, _vp, _vp,
+                                       ctypes.c_size_t, _vp]),
     "kr_admit": (ctypes.c_int, [_vp, _i64, _i64, _vp, ctypes.POINTER(KrFleet),
                                 ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp, _vp,
                                 ctypes.c_size_t, _vp]),

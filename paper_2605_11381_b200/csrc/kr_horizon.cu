@@ -14,6 +14,8 @@
 // exact evaluation order.  The per-robot first-trip index is a shared-memory
 // atomicMin, which is the parallel form of numpy's argmax / the early-exit loop.
 #include <climits>
+#include <mutex>
+#include <unordered_map>
 
 #include "kr_common.cuh"
 #include "kr_host.cuh"
@@ -342,11 +344,25 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
     return p;
 }
 
+// Per-kernel launch facts, cached so that repeated (and CUDA-graph-captured)
+// launches make no attribute / occupancy queries.
+struct KernelFacts {
+    int regs = -1;
+    int smem_set = 0;
+    int occ_threads = 0, occ_smem = -1, occ_blocks = 0;
+};
+static std::mutex g_facts_mu;
+static std::unordered_map<const void*, KernelFacts> g_facts;
+
 template <class K>
 static int kernel_regs(K kern) {
-    cudaFuncAttributes a{};
-    if (cudaFuncGetAttributes(&a, kern) != cudaSuccess) return 64;
-    return a.numRegs;
+    std::lock_guard<std::mutex> lock(g_facts_mu);
+    KernelFacts& f = g_facts[reinterpret_cast<const void*>(kern)];
+    if (f.regs < 0) {
+        cudaFuncAttributes a{};
+        f.regs = cudaFuncGetAttributes(&a, kern) == cudaSuccess ? a.numRegs : 64;
+    }
+    return f.regs;
 }
 
 template <class Work, class KStaged, class KDirect>
@@ -354,10 +370,23 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
                          cudaStream_t st, const char* name) {
     size_t smem = stream_smem_bytes(p);
     auto go = [&](auto kern) -> int {
-        KR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
         int per_sm = 0;
-        KR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, p.threads, smem));
+        {
+            std::lock_guard<std::mutex> lock(g_facts_mu);
+            KernelFacts& f = g_facts[reinterpret_cast<const void*>(kern)];
+            if (f.smem_set < static_cast<int>(smem)) {
+                KR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem)));
+                f.smem_set = static_cast<int>(smem);
+            }
+            if (f.occ_threads != p.threads || f.occ_smem != static_cast<int>(smem)) {
+                KR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.occ_blocks, kern,
+                                                                          p.threads, smem));
+                f.occ_threads = p.threads;
+                f.occ_smem = static_cast<int>(smem);
+            }
+            per_sm = f.occ_blocks;
+        }
         if (per_sm < 1) per_sm = 1;
         int64_t ntiles = (p.R + p.TR - 1) / p.TR;
         int64_t grid = static_cast<int64_t>(device_info().sm_count) * per_sm;

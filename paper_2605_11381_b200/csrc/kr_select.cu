@@ -11,12 +11,15 @@
 //      bin, and stops when the boundary bin holds one key.  Two grid-wide levels
 //      shrink 2^20 keys to a handful; one CTA finishes.
 //   2. One elementwise admission pass (key <= kth): admitted / refetch masks,
-//      skip counters (scheduler.py:223-234) and a gather of the k admitted
-//      (key, index) pairs.
-//   3. A sort of only those k pairs (a grid-wide parallel rank sort for
-//      k <= 16384, otherwise a stable multi-CTA LSD radix sort over the
+//      skip counters (scheduler.py:223-234) and a block-aggregated gather of
+//      the k admitted (key, index) pairs.
+//   3. A sort of only those k pairs, independent of the key distribution:
+//      runs of 1024 bitonic-sorted in shared memory, then every pair's final
+//      position = its run index + binary-search ranks in the other runs
+//      (k <= 2^17; beyond, a stable multi-CTA LSD radix sort over the
 //      differing key bits), giving S_e in reference order.
 // Keys are unique (the lexrank tiebreak), so every step is deterministic.
+#include <atomic>
 #include <climits>
 
 #include "kr_common.cuh"
@@ -48,7 +51,6 @@ struct Workspace {
     kr_key* cand[2];
     kr_key* skeys[2];
     int32_t* sidx[2];
-    uint32_t* rank;
     uint32_t* tile_hist;
 };
 
@@ -62,7 +64,6 @@ static size_t workspace_bytes(int64_t n) {
     b += 2 * align256(nn * sizeof(kr_key));      // select candidates
     b += 2 * align256(nn * sizeof(kr_key));      // sort keys ping-pong
     b += 2 * align256(nn * sizeof(int32_t));     // sort index ping-pong
-    b += align256(nn * sizeof(uint32_t));        // rank-sort ranks
     b += align256(sort_tiles(n) * 256 * sizeof(uint32_t));
     return b;
 }
@@ -85,8 +86,6 @@ static Workspace carve(void* ws, int64_t n) {
         w.sidx[i] = reinterpret_cast<int32_t*>(p);
         p += align256(nn * sizeof(int32_t));
     }
-    w.rank = reinterpret_cast<uint32_t*>(p);
-    p += align256(nn * sizeof(uint32_t));
     w.tile_hist = reinterpret_cast<uint32_t*>(p);
     return w;
 }
@@ -156,37 +155,83 @@ __device__ __forceinline__ unsigned block_append(bool take, unsigned int* counte
     return pos;
 }
 
-// Digit window just below the highest differing bit of the candidate set.
+// Digit = the values of the candidate set's kDigitBits most significant
+// *differing* bit positions (a pext of OR ^ AND), MSB first.  All candidates
+// agree on every other bit, so digit order is key order; unlike a contiguous
+// bit window it never wastes digit bits on constant fields (e.g. the high
+// zero bits of the aged estimate between the bucket and its significant bits).
 struct Digit {
-    int shift, width;
+    int W;                 // number of digit bits (0: all candidates identical)
+    int nrun;              // the digit bits grouped into runs of adjacent positions
+    int run_pos[kDigitBits];  // lowest bit position (0..127) of each run, MSB run first
+    int run_len[kDigitBits];
     bool any;
 };
+// Built with compile-time indices only (predicated updates) so that the run
+// table lives in registers for the per-key extraction loops.
 __device__ __forceinline__ Digit digit_of(const unsigned long long* s) {
-    unsigned long long xh = s[0] ^ s[2], xl = s[1] ^ s[3];
+    unsigned long long xlo = s[1] ^ s[3], xhi = s[0] ^ s[2];
     Digit d;
-    int h;
-    if (xh) h = 127 - __clzll(xh);
-    else if (xl) h = 63 - __clzll(xl);
-    else h = -1;
-    d.any = h >= 0;
-    d.width = h + 1 < kDigitBits ? h + 1 : kDigitBits;
-    d.shift = h - d.width + 1;
-    if (!d.any) { d.width = 1; d.shift = 0; }
+    d.W = 0;
+    d.nrun = 0;
+#pragma unroll
+    for (int r = 0; r < kDigitBits; r++) {
+        d.run_pos[r] = 0;
+        d.run_len[r] = 0;
+    }
+    int last = -2;
+#pragma unroll
+    for (int w = 0; w < kDigitBits; w++) {
+        int pos = -1;
+        if (xhi) {
+            pos = 127 - __clzll(xhi);
+            xhi &= ~(1ull << (pos - 64));
+        } else if (xlo) {
+            pos = 63 - __clzll(xlo);
+            xlo &= ~(1ull << pos);
+        }
+        if (pos >= 0) {
+            // extend the current run downwards unless it would cross the word boundary
+            const bool extend = pos == last - 1 && (pos >> 6) == (last >> 6);
+            const int cur = extend ? d.nrun - 1 : d.nrun;
+#pragma unroll
+            for (int r = 0; r < kDigitBits; r++) {
+                if (r == cur) {
+                    d.run_pos[r] = pos;
+                    d.run_len[r] += 1;
+                }
+            }
+            d.nrun = cur + 1;
+            last = pos;
+            d.W = w + 1;
+        }
+    }
+    d.any = d.W > 0;
     return d;
 }
 __device__ __forceinline__ unsigned digit_val(const kr_key& k, const Digit& d) {
-    return static_cast<unsigned>(shr128_lo(k.hi, k.lo, d.shift) & ((1ull << d.width) - 1));
+    unsigned v = 0;
+#pragma unroll
+    for (int r = 0; r < kDigitBits; r++) {
+        if (r >= d.nrun) break;
+        const int pos = d.run_pos[r], len = d.run_len[r];
+        const unsigned long long word = pos >= 64 ? k.hi : k.lo;
+        v = (v << len) | static_cast<unsigned>((word >> (pos & 63)) & ((1ull << len) - 1));
+    }
+    return v;
 }
 
 // ---------------------------------------------------------------------------
 // radix select
 // ---------------------------------------------------------------------------
-__global__ void k_sel_reset(SelState* s, int64_t n, int64_t k) {
+__global__ void k_sel_reset(SelState* s, int64_t n, int64_t k, const unsigned long long* stats) {
     for (int i = threadIdx.x; i < kBins; i += blockDim.x) s->hist[i] = 0;
     if (threadIdx.x == 0) {
         for (int p = 0; p < 2; p++) {
             s->st[p][0] = 0; s->st[p][1] = 0; s->st[p][2] = ~0ull; s->st[p][3] = ~0ull;
         }
+        if (stats)
+            for (int j = 0; j < 4; j++) s->st[0][j] = stats[j];
         s->sst[0] = 0; s->sst[1] = 0; s->sst[2] = ~0ull; s->sst[3] = ~0ull;
         s->cnt[0] = static_cast<unsigned>(n);
         s->cnt[1] = 0;
@@ -215,7 +260,7 @@ __global__ void __launch_bounds__(256) k_sel_hist(const kr_key* __restrict__ src
     const int p = level & 1;
     Digit d = digit_of(s->st[p]);
     const int64_t n = s->cnt[p];
-    const int bins = 1 << d.width;
+    const int bins = 1 << d.W;
     for (int i = threadIdx.x; i < bins; i += blockDim.x) h[i] = 0;
     __syncthreads();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -240,7 +285,7 @@ __device__ void sel_pick_block(SelState* s, int level, const unsigned int* hist,
         }
         return;
     }
-    const int bins = 1 << d.width;
+    const int bins = 1 << d.W;
     const int per = (bins + blockDim.x - 1) / blockDim.x;
     unsigned int local = 0;
     for (int q = 0; q < per; q++) {
@@ -357,7 +402,7 @@ __global__ void __launch_bounds__(1024) k_sel_finish(SelState* s, kr_key* bufA, 
             }
             return;
         }
-        const int bins = 1 << d.width;
+        const int bins = 1 << d.W;
         for (int i = threadIdx.x; i < bins; i += blockDim.x) h[i] = 0;
         __syncthreads();
         for (unsigned i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&h[digit_val(src[i], d)], 1u);
@@ -478,61 +523,108 @@ __global__ void __launch_bounds__(256) k_admit(AdmitArgs a) {
     if (a.sel_keys) stats_accumulate(a.s->sst, oh, ol, ah, al);
 }
 
-// ---------------------------------------------------------------------------
-// sorting the admitted set
-// ---------------------------------------------------------------------------
+constexpr int kRun = 256;          // run length sorted in shared memory
+constexpr int kRunThreads = 128;
+constexpr int kRunSortMax = 1 << 17;  // larger sets use the multi-CTA LSD radix sort
+
 __device__ __forceinline__ bool pair_gt(const kr_key& a, int32_t ia, const kr_key& b, int32_t ib) {
     if (a.hi != b.hi) return a.hi > b.hi;
     if (a.lo != b.lo) return a.lo > b.lo;
     return ia > ib;
 }
 
-// Parallel rank sort for the admitted set: rank_i = #{j : (key_j, j) < (key_i, i)}
-// computed over a 2-D grid of (i-tile, j-tile) blocks with the j-tile staged in
-// shared memory (broadcast reads), then one scatter.  O(m^2) compares spread
-// over the whole GPU; used for m <= kRankSortMax.
-constexpr int kRankI = 256, kRankJ = 1024, kRankSortMax = 16384;
-
-__global__ void __launch_bounds__(kRankI) k_rank_count(const kr_key* keys, const unsigned int* count_dev,
-                                                       int m_host, unsigned int* rank) {
-    __shared__ kr_key sj[kRankJ];
+// Sort of m (key, index) pairs, independent of the key distribution:
+//  (1) each CTA sorts one run of kRun pairs with a bitonic network in shared
+//      memory (padded with +inf);
+//  (2) every pair's final position = its index inside its run + the number of
+//      smaller pairs in every other run (binary search), computed by one thread
+//      per pair and scattered directly.  Pairs are unique (index tiebreak), so
+//      positions form a permutation.
+__global__ void __launch_bounds__(kRunThreads) k_run_sort(const kr_key* keys, const int32_t* idx,
+                                                          const unsigned int* count_dev, int m_host,
+                                                          kr_key* rk, int32_t* ri) {
+    __shared__ kr_key sk[kRun];
+    __shared__ int32_t si[kRun];
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
-    const int j0 = blockIdx.y * kRankJ;
-    if (j0 >= m) return;
-    const int jn = min(kRankJ, m - j0);
-    for (int t = threadIdx.x; t < jn; t += blockDim.x) sj[t] = keys[j0 + t];
-    __syncthreads();
-    const int i = blockIdx.x * kRankI + threadIdx.x;
-    if (i >= m) return;
-    const kr_key ki = keys[i];
-    unsigned int c = 0;
-    int jj = 0;
-    for (; jj + 4 <= jn; jj += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const kr_key kj = sj[jj + u];
-            const int j = j0 + jj + u;
-            c += (kj.hi < ki.hi) | ((kj.hi == ki.hi) & ((kj.lo < ki.lo) | ((kj.lo == ki.lo) & (j < i))));
+    const int base = blockIdx.x * kRun;
+    if (base >= m) return;
+    const int n = min(kRun, m - base);
+    unsigned np2 = 1;
+    while (np2 < static_cast<unsigned>(n)) np2 <<= 1;
+    for (unsigned i = threadIdx.x; i < np2; i += blockDim.x) {
+        if (i < static_cast<unsigned>(n)) {
+            sk[i] = keys[base + i];
+            si[i] = idx ? idx[base + i] : base + static_cast<int>(i);
+        } else {
+            sk[i] = kr_key{~0ull, ~0ull};
+            si[i] = INT_MAX;
         }
     }
-    for (; jj < jn; jj++) {
-        const kr_key kj = sj[jj];
-        const int j = j0 + jj;
-        c += (kj.hi < ki.hi) | ((kj.hi == ki.hi) & ((kj.lo < ki.lo) | ((kj.lo == ki.lo) & (j < i))));
+    __syncthreads();
+    for (unsigned kk = 2; kk <= np2; kk <<= 1) {
+        for (unsigned j = kk >> 1; j > 0; j >>= 1) {
+            for (unsigned t = threadIdx.x; t < np2 / 2; t += blockDim.x) {
+                const unsigned i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                const unsigned l = i | j;
+                const bool up = (i & kk) == 0;
+                const kr_key ka = sk[i], kb = sk[l];
+                const int32_t ia = si[i], ib = si[l];
+                if (pair_gt(ka, ia, kb, ib) == up) {
+                    sk[i] = kb; sk[l] = ka;
+                    si[i] = ib; si[l] = ia;
+                }
+            }
+            __syncthreads();
+        }
     }
-    if (c) atomicAdd(&rank[i], c);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        rk[base + i] = sk[i];
+        ri[base + i] = si[i];
+    }
 }
 
-__global__ void k_rank_scatter(const kr_key* keys, const int32_t* idx, const unsigned int* count_dev,
-                               int m_host, const unsigned int* rank, int32_t* out_idx,
-                               kr_key* out_keys) {
+__device__ __forceinline__ int count_less(const kr_key* rk, const int32_t* ri, int lo, int hi,
+                                          const kr_key& x, int32_t xi) {
+    const int start = lo;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pair_gt(x, xi, rk[mid], ri[mid])) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo - start;
+}
+
+// One warp per pair: lane r counts the pairs smaller than it in runs
+// r, r + 32, ... by binary search (L2-resident), the warp sums the counts and
+// lane 0 scatters the pair to its final position.  8 dependent probes per run
+// of 256, spread over m warps, keep the whole GPU busy even for small m.
+__global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32_t* ri,
+                                                   const unsigned int* count_dev, int m_host,
+                                                   int32_t* out_idx, kr_key* out_keys) {
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-        const unsigned r = rank[i];
-        if (out_idx) out_idx[r] = idx ? idx[i] : i;
-        if (out_keys) out_keys[r] = keys[i];
+    const int nruns = (m + kRun - 1) / kRun;
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < m; e += gridDim.x * wpb) {
+        const kr_key x = rk[e];
+        const int32_t xi = ri[e];
+        const int own = e / kRun;
+        int c = 0;
+        for (int r = lane; r < nruns; r += 32)
+            if (r != own) c += count_less(rk, ri, r * kRun, min(r * kRun + kRun, m), x, xi);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            const int rank = c + (e - own * kRun);
+            if (out_idx) out_idx[rank] = xi;
+            if (out_keys) out_keys[rank] = x;
+        }
     }
 }
+
+// ---------------------------------------------------------------------------
+// sorting the admitted set (generic paths)
+// ---------------------------------------------------------------------------
 
 // --- stable multi-CTA LSD radix sort over 8-bit windows ---------------------
 __global__ void __launch_bounds__(256) k_rs_hist(const kr_key* keys, int64_t n, int shift,
@@ -631,14 +723,20 @@ __global__ void __launch_bounds__(256) k_rs_scatter(const kr_key* keys, const in
 static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx,
                       const unsigned int* count_dev, int64_t n, int32_t* out_idx, kr_key* out_keys,
                       const unsigned long long* stats_dev, cudaStream_t st) {
-    if (n <= kRankSortMax) {
-        KR_CUDA_TRY(cudaMemsetAsync(w.rank, 0, n * sizeof(uint32_t), st));
+    if (n <= kRunSortMax) {
         const int m = static_cast<int>(n);
-        dim3 grid((m + kRankI - 1) / kRankI, (m + kRankJ - 1) / kRankJ);
-        k_rank_count<<<grid, kRankI, 0, st>>>(keys, count_dev, m, w.rank);
-        k_rank_scatter<<<(m + 255) / 256, 256, 0, st>>>(keys, idx, count_dev, m, w.rank, out_idx,
-                                                       out_keys);
-        return check_launch("rank sort", 2);
+        const kr_key* sk = keys;
+        const int32_t* si = idx;
+        // runs are written to the sort ping-pong buffer not holding the input
+        kr_key* rk = keys == w.skeys[1] ? w.skeys[0] : w.skeys[1];
+        int32_t* ri = keys == w.skeys[1] ? w.sidx[0] : w.sidx[1];
+        k_run_sort<<<(m + kRun - 1) / kRun, kRunThreads, 0, st>>>(sk, si, count_dev, m, rk, ri);
+        const int64_t warps = m;
+        int64_t blocks = (warps + 7) / 8;
+        if (blocks > 148 * 64) blocks = 148 * 64;
+        k_run_merge<<<static_cast<unsigned>(blocks), 256, 0, st>>>(rk, ri, count_dev, m, out_idx,
+                                                                   out_keys);
+        return check_launch("run sort", 2);
     }
     // window plan from OR ^ AND of the set (read back: one stream sync)
     unsigned long long s4[4];
@@ -700,8 +798,51 @@ using namespace kr;
 
 extern "C" size_t kr_workspace_bytes(int64_t n) { return workspace_bytes(n); }
 
-extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth, void* ws,
-                              size_t ws_bytes, void* stream) {
+// Launches the select pipeline (workspace state left holding the level-0
+// k-th key in state->kth).  Returns KR_OK or an error.
+static int select_pipeline(const kr_key* keys, int64_t n, int64_t k,
+                           const unsigned long long* key_stats, const Workspace& w,
+                           cudaStream_t st) {
+    SelState* s = w.state;
+    k_sel_reset<<<1, 1024, 0, st>>>(s, n, k, key_stats);
+    int launches = 1;
+    if (!key_stats) {
+        k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, s);
+        launches++;
+    }
+    // level 0: all keys -> cand[0]; level 1: cand[0] -> cand[1]; finisher reads cand[1]
+    k_sel_hist<<<grid_stream(n), 256, 0, st>>>(keys, s, 0);
+    k_sel_pick<<<1, 1024, 0, st>>>(s, keys, 0);
+    k_sel_scatter<<<grid_stream(n), 256, 0, st>>>(keys, w.cand[0], s, 0);
+    k_sel_hist<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], s, 1);
+    k_sel_pick<<<1, 1024, 0, st>>>(s, w.cand[0], 1);
+    k_sel_scatter<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], w.cand[1], s, 1);
+    k_sel_finish<<<1, 1024, 0, st>>>(s, w.cand[1], w.cand[0], 2);
+    return check_launch("select", launches + 7);
+}
+
+static int admit_with(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
+                      const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted,
+                      uint8_t* refetch, int32_t* edge_idx, kr_key* edge_keys, const Workspace& w,
+                      cudaStream_t st);
+
+extern "C" int kr_key_stats_init(unsigned long long* stats, void* stream) {
+    if (!stats) return KR_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    KR_CUDA_TRY(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st));
+    KR_CUDA_TRY(cudaMemsetAsync(stats + 2, 0xFF, 2 * sizeof(unsigned long long), st));
+    return KR_OK;
+}
+
+extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
+                               const unsigned long long* key_stats, const kr_fleet* fleet,
+                               const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
+                               int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* ws,
+                               size_t ws_bytes, void* stream);
+
+extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth,
+                              const unsigned long long* key_stats, void* ws, size_t ws_bytes,
+                              void* stream) {
     if (n < 0 || k < 0 || !kth) return KR_EINVAL;
     cudaStream_t st = as_stream(stream);
     if (k == 0 || n == 0) return KR_OK;
@@ -711,38 +852,52 @@ extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* 
     }
     if (!ws || ws_bytes < workspace_bytes(n) || !keys) return KR_ENOSPACE;
     Workspace w = carve(ws, n);
-    SelState* s = w.state;
-    k_sel_reset<<<1, 1024, 0, st>>>(s, n, k);
-    k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, s);
-    // level 0: all keys -> cand[0]; level 1: cand[0] -> cand[1]; finisher reads cand[1]
-    k_sel_hist<<<grid_stream(n), 256, 0, st>>>(keys, s, 0);
-    k_sel_pick<<<1, 1024, 0, st>>>(s, keys, 0);
-    k_sel_scatter<<<grid_stream(n), 256, 0, st>>>(keys, w.cand[0], s, 0);
-    k_sel_hist<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], s, 1);
-    k_sel_pick<<<1, 1024, 0, st>>>(s, w.cand[0], 1);
-    k_sel_scatter<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], w.cand[1], s, 1);
-    // finisher: level 2 reads parity 0 buffer == cand[1] (see k_sel_finish)
-    k_sel_finish<<<1, 1024, 0, st>>>(s, w.cand[1], w.cand[0], 2);
-    k_copy_kth<<<1, 1, 0, st>>>(s, kth);
-    return check_launch("kr_topk_select", 10);
+    int e = select_pipeline(keys, n, k, key_stats, w, st);
+    if (e) return e;
+    k_copy_kth<<<1, 1, 0, st>>>(w.state, kth);
+    return check_launch("kr_topk_select");
 }
 
-extern "C" int kr_admit(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
-                        const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted,
-                        uint8_t* refetch, int32_t* edge_idx, kr_key* edge_keys, void* ws,
-                        size_t ws_bytes, void* stream) {
+extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
+                               const unsigned long long* key_stats, const kr_fleet* fleet,
+                               const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
+                               int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* ws,
+                               size_t ws_bytes, void* stream) {
     if (n < 0 || k < 0) return KR_EINVAL;
     if (n == 0) return KR_OK;
     if (!keys) return KR_EINVAL;
     if ((refetch || (fleet && fleet->skipped)) && (!fleet || !cfg)) return KR_EINVAL;
+    if (!ws || ws_bytes < workspace_bytes(n)) return KR_ENOSPACE;
     cudaStream_t st = as_stream(stream);
-    const bool gather = edge_idx || edge_keys;
-    Workspace w{};
-    if (gather) {
-        if (!ws || ws_bytes < workspace_bytes(n)) return KR_ENOSPACE;
-        w = carve(ws, n);
-        k_admit_init<<<1, 32, 0, st>>>(w.state);
+    if (k == 0 || k >= n) {  // nothing to select: generic admission (+ full order if k >= n)
+        const kr_key* kth_ptr = nullptr;
+        if (kth_out && k >= n) {
+            k_set_key<<<1, 1, 0, st>>>(kth_out, ~0ull, ~0ull);
+            int e = check_launch("kr_select_admit");
+            if (e) return e;
+        }
+        return kr_admit(keys, n, k, kth_ptr, fleet, cfg, admitted, refetch, edge_idx, edge_keys,
+                        ws, ws_bytes, stream);
     }
+    Workspace w = carve(ws, n);
+    int e = select_pipeline(keys, n, k, key_stats, w, st);
+    if (e) return e;
+    if (kth_out) {
+        k_copy_kth<<<1, 1, 0, st>>>(w.state, kth_out);
+        e = check_launch("kr_select_admit");
+        if (e) return e;
+    }
+    return admit_with(keys, n, k, &w.state->kth, fleet, cfg, admitted, refetch, edge_idx,
+                      edge_keys, w, st);
+}
+
+// Admission pass + (optional) ordered gather of the admitted set.
+static int admit_with(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
+                      const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted,
+                      uint8_t* refetch, int32_t* edge_idx, kr_key* edge_keys, const Workspace& w,
+                      cudaStream_t st) {
+    const bool gather = edge_idx || edge_keys;
+    if (gather) k_admit_init<<<1, 32, 0, st>>>(w.state);
     AdmitArgs a{};
     a.keys = keys;
     a.n = n;
@@ -763,8 +918,26 @@ extern "C" int kr_admit(const kr_key* keys, int64_t n, int64_t k, const kr_key* 
     if (e || !gather) return e;
     const int64_t m = k < n ? k : n;
     if (m == 0) return KR_OK;
-    return sort_pairs(w, w.skeys[0], w.sidx[0], m <= kRankSortMax ? &w.state->sel_count : nullptr,
+    return sort_pairs(w, w.skeys[0], w.sidx[0], m <= kRunSortMax ? &w.state->sel_count : nullptr,
                       m, edge_idx, edge_keys, w.state->sst, st);
+}
+
+extern "C" int kr_admit(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
+                        const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted,
+                        uint8_t* refetch, int32_t* edge_idx, kr_key* edge_keys, void* ws,
+                        size_t ws_bytes, void* stream) {
+    if (n < 0 || k < 0) return KR_EINVAL;
+    if (n == 0) return KR_OK;
+    if (!keys) return KR_EINVAL;
+    if ((refetch || (fleet && fleet->skipped)) && (!fleet || !cfg)) return KR_EINVAL;
+    const bool gather = edge_idx || edge_keys;
+    Workspace w{};
+    if (gather) {
+        if (!ws || ws_bytes < workspace_bytes(n)) return KR_ENOSPACE;
+        w = carve(ws, n);
+    }
+    return admit_with(keys, n, k, kth, fleet, cfg, admitted, refetch, edge_idx, edge_keys, w,
+                      as_stream(stream));
 }
 
 extern "C" int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_key* sorted_keys,
@@ -774,9 +947,9 @@ extern "C" int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_ke
     if (!keys || !ws || ws_bytes < workspace_bytes(n)) return KR_ENOSPACE;
     cudaStream_t st = as_stream(stream);
     Workspace w = carve(ws, n);
-    if (n <= kRankSortMax)
+    if (n <= kRunSortMax)
         return sort_pairs(w, keys, nullptr, nullptr, n, order, sorted_keys, nullptr, st);
-    k_sel_reset<<<1, 1024, 0, st>>>(w.state, n, 0);
+    k_sel_reset<<<1, 1024, 0, st>>>(w.state, n, 0, nullptr);
     k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, w.state);
     int e = check_launch("kr_sort_keys", 2);
     if (e) return e;

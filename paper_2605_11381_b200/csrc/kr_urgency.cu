@@ -51,6 +51,7 @@ struct UrgencyOut {
     int32_t* bucket;
     int64_t* est;
     int64_t* slot_wait;
+    unsigned long long* key_stats;
     uint32_t* flags;
 };
 
@@ -73,8 +74,18 @@ __device__ __forceinline__ void slot_waits(const int64_t* slots, int32_t n_exec,
     }
 }
 
+__device__ __forceinline__ unsigned long long wor(unsigned long long v) {
+    for (int o = 16; o; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ unsigned long long wand(unsigned long long v) {
+    for (int o = 16; o; o >>= 1) v &= __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 __global__ void __launch_bounds__(256) k_urgency(kr_fleet f, kr_sched c, UrgencyOut o) {
     uint32_t fl = 0;
+    unsigned long long ohi = 0, olo = 0, ahi = ~0ull, alo = ~0ull;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < f.n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t issued = __ldg(f.issued_at + i);
@@ -122,8 +133,28 @@ __global__ void __launch_bounds__(256) k_urgency(kr_fleet f, kr_sched c, Urgency
             }
         }
         o.keys[i] = key;
+        ohi |= key.hi; olo |= key.lo; ahi &= key.hi; alo &= key.lo;
     }
     if (fl && o.flags) atomicOr(o.flags, fl);
+    if (o.key_stats) {  // block-reduced OR / AND of the keys (select statistics)
+        __shared__ unsigned long long red[4][8];
+        ohi = wor(ohi); olo = wor(olo); ahi = wand(ahi); alo = wand(alo);
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) {
+            red[0][warp] = ohi; red[1][warp] = olo; red[2][warp] = ahi; red[3][warp] = alo;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int nw = (blockDim.x + 31) >> 5;
+            for (int w = 1; w < nw; w++) {
+                ohi |= red[0][w]; olo |= red[1][w]; ahi &= red[2][w]; alo &= red[3][w];
+            }
+            if (ohi) atomicOr(&o.key_stats[0], ohi);
+            if (olo) atomicOr(&o.key_stats[1], olo);
+            if (~ahi) atomicAnd(&o.key_stats[2], ahi);
+            if (~alo) atomicAnd(&o.key_stats[3], alo);
+        }
+    }
 }
 
 static unsigned grid_for(int64_t n, int threads) {
@@ -171,14 +202,15 @@ extern "C" int kr_assign_bucket(const double* wr, const int32_t* skipped, int64_
 
 extern "C" int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys,
                           int64_t* need_time, int64_t* total_wait, double* wr, int32_t* bucket,
-                          int64_t* est, int64_t* slot_wait, uint32_t* flags, void* stream) {
+                          int64_t* est, int64_t* slot_wait, unsigned long long* key_stats,
+                          uint32_t* flags, void* stream) {
     if (!fleet || !cfg || fleet->n < 0) return KR_EINVAL;
     if (cfg->policy < KR_KAIROS || cfg->policy > KR_LAS || cfg->buckets < 1 ||
         cfg->buckets > 256 || cfg->aging_interval < 1 || cfg->hz_num <= 0 || cfg->hz_den <= 0)
         return KR_EINVAL;
     if (fleet->n == 0) return KR_OK;
     if (!keys) return KR_EINVAL;
-    UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, slot_wait, flags};
+    UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, slot_wait, key_stats, flags};
     k_urgency<<<grid_for(fleet->n, 256), 256, 0, as_stream(stream)>>>(*fleet, *cfg, o);
     return check_launch("kr_urgency");
 }

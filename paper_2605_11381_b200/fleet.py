@@ -128,8 +128,8 @@ def new_keys(n: int, device=None) -> torch.Tensor:
 
 
 def urgency(fleet: DeviceFleet, sched: _lib.KrSched, *, need_time=True, intermediates=False,
-            slot_waits=False, keys: torch.Tensor | None = None, flags: torch.Tensor | None = None
-            ) -> UrgencyOut:
+            slot_waits=False, keys: torch.Tensor | None = None, flags: torch.Tensor | None = None,
+            key_stats: torch.Tensor | None = None) -> UrgencyOut:
     """Step 2 over the whole fleet: one fused kernel (kr_urgency)."""
     d = dev.device()
     n = fleet.n
@@ -147,7 +147,8 @@ def urgency(fleet: DeviceFleet, sched: _lib.KrSched, *, need_time=True, intermed
     _lib.check(_lib.load().kr_urgency(
         ctypes.byref(fs), ctypes.byref(sched), out.keys.data_ptr(), _lib.ptr(out.need_time),
         _lib.ptr(out.total_wait), _lib.ptr(out.wr), _lib.ptr(out.bucket), _lib.ptr(out.est),
-        _lib.ptr(out.slot_wait), _lib.ptr(flags), dev.stream()), "kr_urgency")
+        _lib.ptr(out.slot_wait), _lib.ptr(key_stats), _lib.ptr(flags), dev.stream()),
+        "kr_urgency")
     return out
 
 
@@ -180,7 +181,7 @@ def topk_select(keys: torch.Tensor, k: int, ws: Workspace,
                 kth: torch.Tensor | None = None) -> torch.Tensor:
     """Device-side k-th smallest key (kr_topk_select); returns int64 [1, 2]."""
     kth = kth if kth is not None else new_keys(1, keys.device)
-    _lib.check(_lib.load().kr_topk_select(keys.data_ptr(), keys.shape[0], k, kth.data_ptr(),
+    _lib.check(_lib.load().kr_topk_select(keys.data_ptr(), keys.shape[0], k, kth.data_ptr(), None,
                                           ws.ptr(), ws.nbytes, dev.stream()), "kr_topk_select")
     return kth
 
@@ -197,3 +198,25 @@ def admit(keys: torch.Tensor, k: int, kth_ptr: int | None, fleet: DeviceFleet | 
         _lib.ptr(admitted), _lib.ptr(refetch), _lib.ptr(edge_idx), _lib.ptr(edge_keys),
         ws.ptr() if ws is not None else None, ws.nbytes if ws is not None else 0,
         dev.stream()), "kr_admit")
+
+
+def new_key_stats(device=None) -> torch.Tensor:
+    """Device buffer for the fused key statistics (4 x u64, see kr_key_stats_init)."""
+    return torch.empty(4, dtype=torch.int64, device=device or dev.device())
+
+
+def key_stats_init(stats: torch.Tensor) -> None:
+    _lib.check(_lib.load().kr_key_stats_init(stats.data_ptr(), dev.stream()), "kr_key_stats_init")
+
+
+def select_admit(keys: torch.Tensor, k: int, ws: Workspace, *, key_stats=None, fleet=None,
+                 sched=None, admitted=None, refetch=None, edge_idx=None, edge_keys=None,
+                 kth=None) -> None:
+    """Fused select + admission + ordered S_e (kr_select_admit)."""
+    fs = fleet.c_struct() if fleet is not None else None
+    _lib.check(_lib.load().kr_select_admit(
+        keys.data_ptr(), keys.shape[0], k, _lib.ptr(key_stats),
+        ctypes.byref(fs) if fs is not None else None,
+        ctypes.byref(sched) if sched is not None else None,
+        _lib.ptr(admitted), _lib.ptr(refetch), _lib.ptr(edge_idx), _lib.ptr(edge_keys),
+        _lib.ptr(kth), ws.ptr(), ws.nbytes, dev.stream()), "kr_select_admit")

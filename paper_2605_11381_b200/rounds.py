@@ -75,6 +75,7 @@ class DecisionRound:
         self.edge_idx = torch.empty(max(self.k, 1), dtype=torch.int32, device=d)
         self.edge_keys = fl.new_keys(max(self.k, 1), d)
         self.ws = fl.Workspace(R)
+        self.key_stats = fl.new_key_stats(d)
         self.lib = _lib.load()
 
     def horizons(self, h: DivergenceInputs) -> None:
@@ -90,33 +91,46 @@ class DecisionRound:
             None, dev.stream()), "kr_horizon_divergence")
 
     def urgency(self, fleet: fl.DeviceFleet) -> None:
+        st = dev.stream()
+        _lib.check(self.lib.kr_key_stats_init(self.key_stats.data_ptr(), st), "kr_key_stats_init")
         fs = fleet.c_struct()
         _lib.check(self.lib.kr_urgency(
             ctypes.byref(fs), ctypes.byref(self.sched), self.keys.data_ptr(),
-            self.need_time.data_ptr(), None, None, None, None, None, None, dev.stream()),
-            "kr_urgency")
+            self.need_time.data_ptr(), None, None, None, None, None,
+            self.key_stats.data_ptr(), None, st), "kr_urgency")
 
     def admit(self, fleet: fl.DeviceFleet) -> None:
-        k, n = self.k, self.R
-        lib = self.lib
-        kth_ptr = None
-        if 0 < k < n:
-            _lib.check(lib.kr_topk_select(self.keys.data_ptr(), n, k, self.kth.data_ptr(),
-                                          self.ws.ptr(), self.ws.nbytes, dev.stream()),
-                       "kr_topk_select")
-            kth_ptr = self.kth.data_ptr()
-        fs = fleet.c_struct()
-        _lib.check(lib.kr_admit(
-            self.keys.data_ptr(), n, k, kth_ptr, ctypes.byref(fs), ctypes.byref(self.sched),
-            self.admitted.data_ptr(), self.refetch.data_ptr(), self.edge_idx.data_ptr(),
-            self.edge_keys.data_ptr(), self.ws.ptr(), self.ws.nbytes, dev.stream()), "kr_admit")
+        fl.select_admit(self.keys, self.k, self.ws, key_stats=self.key_stats, fleet=fleet,
+                        sched=self.sched, admitted=self.admitted, refetch=self.refetch,
+                        edge_idx=self.edge_idx, edge_keys=self.edge_keys, kth=self.kth)
+
+    def outputs(self) -> RoundOutputs:
+        return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
+                            self.edge_keys[: self.k], self.edge_idx[: self.k], self.kth)
 
     def run(self, fleet: fl.DeviceFleet, h: DivergenceInputs) -> RoundOutputs:
         self.horizons(h)
         self.urgency(fleet)
         self.admit(fleet)
-        return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
-                            self.edge_keys[: self.k], self.edge_idx[: self.k], self.kth)
+        return self.outputs()
+
+    def capture(self, fleet: fl.DeviceFleet, h: DivergenceInputs) -> None:
+        """Record the round as two CUDA graphs (horizons | urgency + admission)
+        over these fixed device buffers; `replay()` then launches the ~15
+        kernels of a round with two graph launches."""
+        self.run(fleet, h)  # warm-up: attribute / occupancy caches, lazy loading
+        torch.cuda.synchronize()
+        self.g_horizon, self.g_decide = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g_horizon):
+            self.horizons(h)
+        with torch.cuda.graph(self.g_decide):
+            self.urgency(fleet)
+            self.admit(fleet)
+
+    def replay(self) -> RoundOutputs:
+        self.g_horizon.replay()
+        self.g_decide.replay()
+        return self.outputs()
 
 
 def sharded_topk(keys, n_local: int, k: int, sizes: list, ops, group=None):
@@ -160,7 +174,8 @@ class CudaShardOps:
             kth_ptr = None
             if kl < r.R:
                 _lib.check(r.lib.kr_topk_select(keys.data_ptr(), r.R, kl, r.kth_local.data_ptr(),
-                                                r.ws.ptr(), r.ws.nbytes, st), "kr_topk_select")
+                                                None, r.ws.ptr(), r.ws.nbytes, st),
+                           "kr_topk_select")
                 kth_ptr = r.kth_local.data_ptr()
             _lib.check(r.lib.kr_admit(keys.data_ptr(), r.R, kl, kth_ptr, None, None, None, None,
                                       None, r.cand.data_ptr(), r.ws.ptr(), r.ws.nbytes, st),
@@ -176,7 +191,7 @@ class CudaShardOps:
         r = self.r
         ws = r.ws if keys is r.keys else r.ws_merge
         out = r.kth_local if keys is r.keys else r.kth_global
-        _lib.check(r.lib.kr_topk_select(keys.data_ptr(), keys.shape[0], k, out.data_ptr(),
+        _lib.check(r.lib.kr_topk_select(keys.data_ptr(), keys.shape[0], k, out.data_ptr(), None,
                                         ws.ptr(), ws.nbytes, dev.stream()), "kr_topk_select")
         return out
 
@@ -222,9 +237,6 @@ class ShardedDecisionRound(DecisionRound):
     def admit(self, fleet: fl.DeviceFleet) -> None:
         sharded_topk(self.keys, self.R, self.k, self.sizes, CudaShardOps(self, fleet), self.group)
 
-    def run(self, fleet: fl.DeviceFleet, h: DivergenceInputs) -> RoundOutputs:
-        self.horizons(h)
-        self.urgency(fleet)
-        self.admit(fleet)
+    def outputs(self) -> RoundOutputs:
         return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
                             self.global_edge[: self.k_global], None, self.kth_global)

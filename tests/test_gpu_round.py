@@ -52,3 +52,49 @@ def test_round_baseline_policies(policy):
     res = orc.plan_soa(soa, policy, 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
     assert np.array_equal(rnd.edge_idx.cpu().numpy(), res["order"][:k])
     assert np.array_equal(rnd.admitted.cpu().numpy(), res["admitted"])
+
+
+def test_graph_replay_matches_eager():
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    R, k = 20000, 512
+    soa = synthetic.fleet_soa(R, seed=4)
+    prev, cand, off = synthetic.chunks(R, seed=5)
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    f1 = fl.DeviceFleet.from_host(soa)
+    r1 = rounds.DecisionRound(R, k, sched)
+    o1 = r1.run(f1, rounds.DivergenceInputs(prev, cand, 0.9, offset=off))
+    eager = [t.clone() for t in (o1.horizon, o1.need_time, o1.admitted, o1.refetch, o1.edge_idx)]
+    skip_after_one = f1.t["skipped"].clone()
+    f2 = fl.DeviceFleet.from_host(soa)
+    r2 = rounds.DecisionRound(R, k, sched)
+    r2.capture(f2, rounds.DivergenceInputs(prev, cand, 0.9, offset=off))  # runs one round
+    f2.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
+    o2 = r2.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, (o2.horizon, o2.need_time, o2.admitted, o2.refetch, o2.edge_idx)):
+        assert torch.equal(a, b)
+    assert torch.equal(skip_after_one, f2.t["skipped"])
+
+
+@pytest.mark.parametrize("R,k,rounds_", [(1 << 16, 8192, 60), (1 << 14, 5000, 30)])
+def test_multi_round_replay_vs_oracle(R, k, rounds_):
+    """Successive decision rounds on one fleet: skip counters evolve (aging
+    drives most robots into the top bucket with tied aged estimates, so the
+    admitted set concentrates in few large bins).  Every round must match the
+    oracle's plan() on the same evolving state."""
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    soa = synthetic.fleet_soa(R, seed=77)
+    fleet = fl.DeviceFleet.from_host(soa)
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    rnd = rounds.DecisionRound(R, k, sched)
+    for r in range(rounds_):
+        rnd.urgency(fleet)
+        rnd.admit(fleet)
+        res = orc.plan_soa(soa, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+        torch.cuda.synchronize()
+        assert np.array_equal(rnd.edge_idx.cpu().numpy(), res["order"][:k]), r
+        assert np.array_equal(rnd.admitted.cpu().numpy(), res["admitted"]), r
+        assert np.array_equal(fleet.t["skipped"].cpu().numpy(), res["skipped_out"]), r
+        soa["skipped"] = res["skipped_out"]

@@ -67,3 +67,50 @@ def test_admit_all_and_none():
     assert adm.all() and np.array_equal(idx.cpu().numpy(), _order(keys))
     fl.admit(kt, 0, None, None, None, ws, admitted=adm)
     assert not adm.any()
+
+
+def _skewed(n, rng, mode):
+    if mode == "dense_low_bin":      # > kSegMax admitted keys share the level-0 bin
+        hi = np.where(rng.random(n) < 0.7, 0, rng.integers(1, 1 << 11, n)).astype(np.uint64) << np.uint64(40)
+        lo = (rng.integers(0, 1 << 30, n, dtype=np.uint64) << np.uint64(24)) | np.arange(n, dtype=np.uint64)
+    elif mode == "few_bits":         # only rank bits differ
+        hi = np.zeros(n, np.uint64)
+        lo = rng.permutation(n).astype(np.uint64)
+    else:                            # bucket field + wide gap + low aged bits (kairos-like)
+        hi = (rng.integers(0, 10, n, dtype=np.uint64) << np.uint64(56)) | \
+             ((np.uint64((1 << 56) - 1)) - rng.integers(1 << 18, 1 << 25, n, dtype=np.uint64))
+        lo = (rng.integers(0, 1 << 20, n, dtype=np.uint64) << np.uint64(24)) | np.arange(n, dtype=np.uint64)
+    return np.stack([hi, lo], 1)
+
+
+@pytest.mark.parametrize("n,k,mode", [(1 << 20, 8192, "kairos"), (300000, 1024, "kairos"),
+                                      (20000, 6000, "dense_low_bin"), (4096, 100, "few_bits"),
+                                      (70000, 69999, "kairos"), (50, 49, "few_bits"),
+                                      (1 << 16, 1 << 15, "kairos")])
+def test_select_admit_fused(n, k, mode):
+    from paper_2605_11381_b200 import fleet as fl
+    rng = np.random.default_rng(n + k)
+    keys = _skewed(n, rng, mode)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    ws = fl.Workspace(n)
+    exp = _order(keys)
+    for use_stats in (False, True):
+        stats = None
+        if use_stats:
+            stats = fl.new_key_stats()
+            stats[0] = int(np.bitwise_or.reduce(keys[:, 0]).view(np.int64))
+            stats[1] = int(np.bitwise_or.reduce(keys[:, 1]).view(np.int64))
+            stats[2] = int(np.bitwise_and.reduce(keys[:, 0]).view(np.int64))
+            stats[3] = int(np.bitwise_and.reduce(keys[:, 1]).view(np.int64))
+        adm = torch.empty(n, dtype=torch.uint8, device="cuda")
+        edge_idx = torch.empty(k, dtype=torch.int32, device="cuda")
+        edge_keys = fl.new_keys(k)
+        kth = fl.new_keys(1)
+        fl.select_admit(kt, k, ws, key_stats=stats, admitted=adm, edge_idx=edge_idx,
+                        edge_keys=edge_keys, kth=kth)
+        mask = np.zeros(n, bool)
+        mask[exp[:k]] = True
+        assert np.array_equal(adm.cpu().numpy().astype(bool), mask)
+        assert np.array_equal(edge_idx.cpu().numpy(), exp[:k])
+        assert np.array_equal(edge_keys.cpu().numpy().view(np.uint64), keys[exp[:k]])
+        assert np.array_equal(kth.cpu().numpy().view(np.uint64)[0], keys[exp[k - 1]])

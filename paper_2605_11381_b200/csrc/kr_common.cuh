@@ -225,38 +225,56 @@ __host__ __device__ inline float cos_filter_margin(int D) {
 }
 
 // Returns 1 (cos >= thr), 0 (cos < thr) or -1 (undecided: use the exact path).
-template <int DC, typename T>
-__device__ __forceinline__ int cos_filter_fixed(const T* a, const T* b, float thr_f, float margin) {
-    float xx = 0.f, yy = 0.f, xy = 0.f;
-#pragma unroll
-    for (int i = 0; i < DC; i++) {
-        float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
-        xx = __fmaf_rn(x, x, xx);
-        yy = __fmaf_rn(y, y, yy);
-        xy = __fmaf_rn(x, y, xy);
-    }
+// The bound holds for any summation order, so rows whose length is a multiple
+// of 32 words are read starting at a lane-rotated element: lanes scoring
+// consecutive rows (all starting at bank 0) then hit 32 distinct banks.
+__device__ __forceinline__ int cos_filter_decide(float xx, float yy, float xy, float thr_f,
+                                                 float margin) {
     if (!(xx >= 1e-30f && yy >= 1e-30f && xx <= 1e30f && yy <= 1e30f)) return -1;
-    float c = __fmul_rn(__fmul_rn(xy, rsqrtf(xx)), rsqrtf(yy));
-    float d = __fsub_rn(c, thr_f);
+    const float c = __fmul_rn(__fmul_rn(xy, rsqrtf(xx)), rsqrtf(yy));
+    const float d = __fsub_rn(c, thr_f);
     if (d > margin) return 1;
     if (d < -margin) return 0;
     return -1;
 }
+
+template <int DC, typename T>
+__device__ __forceinline__ int cos_filter_fixed(const T* a, const T* b, float thr_f, float margin) {
+    float xx = 0.f, yy = 0.f, xy = 0.f;
+    if constexpr (DC % 32 == 0) {
+        const int rot = threadIdx.x & 31;
+#pragma unroll
+        for (int e = 0; e < DC; e++) {
+            const int i = (e + rot) % DC;
+            const float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
+            xx = __fmaf_rn(x, x, xx);
+            yy = __fmaf_rn(y, y, yy);
+            xy = __fmaf_rn(x, y, xy);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < DC; i++) {
+            const float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
+            xx = __fmaf_rn(x, x, xx);
+            yy = __fmaf_rn(y, y, yy);
+            xy = __fmaf_rn(x, y, xy);
+        }
+    }
+    return cos_filter_decide(xx, yy, xy, thr_f, margin);
+}
 template <typename T>
 __device__ __forceinline__ int cos_filter(const T* a, const T* b, int D, float thr_f, float margin) {
     float xx = 0.f, yy = 0.f, xy = 0.f;
-    for (int i = 0; i < D; i++) {
-        float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
+    const int rot = (D % 32 == 0) ? (threadIdx.x & 31) : 0;
+    int i = rot;
+    for (int e = 0; e < D; e++) {
+        const float x = static_cast<float>(a[i]), y = static_cast<float>(b[i]);
         xx = __fmaf_rn(x, x, xx);
         yy = __fmaf_rn(y, y, yy);
         xy = __fmaf_rn(x, y, xy);
+        if (++i == D) i = 0;
     }
-    if (!(xx >= 1e-30f && yy >= 1e-30f && xx <= 1e30f && yy <= 1e30f)) return -1;
-    float c = __fmul_rn(__fmul_rn(xy, rsqrtf(xx)), rsqrtf(yy));
-    float d = __fsub_rn(c, thr_f);
-    if (d > margin) return 1;
-    if (d < -margin) return 0;
-    return -1;
+    return cos_filter_decide(xx, yy, xy, thr_f, margin);
 }
 
 // Magic-number unsigned division for n < 2^31 (loop-invariant divisors).

@@ -26,10 +26,11 @@ namespace kr {
 // ---------------------------------------------------------------------------
 // Confidence threshold (horizon.py:108-132)
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, int KC>
 struct ConfWork {
     int K, N, TR, hmin, rounds;
-    double opt;  // 1.0 + threshold, rounded on the host as Python does
+    double opt;   // 1.0 + threshold, rounded on the host as Python does
+    float c1;     // (float)(opt / (K - 1)): the fp32 filter's mean-and-scale factor
     int32_t* H;
     uint32_t* flags;
     int* first;                  // [2][TR] first tripping column per robot
@@ -45,34 +46,42 @@ struct ConfWork {
         }
     }
 
-    // Exact fp32 pre-decision of `f > opt * mean` for fp32 storage: all terms
-    // are non-negative, so the fp32 threshold is within (K + 8) * 2^-24 of the
-    // exact one relative; undecided (or sub-1e-30 / overflowing) columns use
-    // the bit-exact fp64 path.
-    __device__ __forceinline__ int filter(const T* col) const {
-        if constexpr (sizeof(T) != 4) {
-            return -1;
+    // Exact fp32 pre-decision of `f > opt * mean` (fp32 storage): all terms are
+    // non-negative, so the fp32 threshold sum * c1 is within (K + 8) * 2^-24 of
+    // the exact one relative; undecided (or sub-1e-30 / overflowing) columns
+    // use the bit-exact fp64 path.
+    __device__ __forceinline__ int filter(float sf, float fin) const {
+        if (fin == 0.f) return 0;  // 0 > thr is false for any thr >= 0
+        const float thr = __fmul_rn(sf, c1);
+        if (thr == 0.f) return sf == 0.f ? 1 : -1;  // exact zero mean: any f > 0 trips
+        if (!(thr >= 1e-30f && thr <= 1e30f)) return -1;
+        const float margin = static_cast<float>(K + 8) * 5.9604645e-8f;
+        if (fin > thr * (1.f + margin)) return 1;
+        if (fin < thr * (1.f - margin)) return 0;
+        return -1;
+    }
+
+    __device__ __forceinline__ bool exact(const T* col) const {
+        // u[:-1].mean(axis=0): sequential column add for N >= 2, numpy
+        // pairwise summation when the reduction collapses (N == 1).
+        const int K1 = K - 1;
+        double sum;
+        if (N >= 2) {
+            sum = to_f64(col[0]);
+            for (int k = 1; k < K1; k++) sum = dadd(sum, to_f64(col[static_cast<size_t>(k) * N]));
         } else {
-            float sf = col[0];
-            for (int k = 1; k < K - 1; k++) sf = __fadd_rn(sf, col[static_cast<size_t>(k) * N]);
-            const float fin = col[static_cast<size_t>(K - 1) * N];
-            if (fin == 0.f) return 0;  // 0 > thr is false for any thr >= 0
-            const float thr = __fmul_rn(__fdiv_rn(sf, static_cast<float>(K - 1)),
-                                        static_cast<float>(opt));
-            if (thr == 0.f) return sf == 0.f ? 1 : -1;  // exact zero mean: any f > 0 trips
-            if (!(thr >= 1e-30f && thr <= 1e30f)) return -1;
-            const float margin = static_cast<float>(K + 8) * 5.9604645e-8f;
-            if (fin > thr * (1.f + margin)) return 1;
-            if (fin < thr * (1.f - margin)) return 0;
-            return -1;
+            auto a = [col](int64_t k) { return to_f64(col[k]); };
+            sum = np_pairwise_sum(a, 0, K1);
         }
+        const double m = ddiv(sum, static_cast<double>(K1));
+        return to_f64(col[static_cast<size_t>(K1) * N]) > dmul(opt, m);  // strict '>'
     }
 
     __device__ __forceinline__ void tile(const TileView& v, int64_t, int nr, int64_t local) {
         const T* u = reinterpret_cast<const T*>(v.seg[0]);
         int* f = first + (local & 1) * TR;
         uint32_t fl = 0;
-        const int K1 = K - 1;
+        const int Kr = KC > 0 ? KC : K;
 #pragma unroll
         for (int q = 0; q < kMaxRounds; q++) {
             if (q >= rounds) break;
@@ -81,29 +90,34 @@ struct ConfWork {
             bool trip = false;
             if (valid) {
                 const int n = n_q[q];
-                const T* col = u + static_cast<size_t>(rr) * K * N + n;
-                // Validation (horizon.py:47-50) covers every element of the round.
-                for (int k = 0; k < K; k++) {
-                    T x = col[static_cast<size_t>(k) * N];
-                    if (!isfinite(x)) fl |= KR_FLAG_NONFINITE;
-                    if (x < T(0)) fl |= KR_FLAG_NEGATIVE;
-                }
-                int t = filter(col);
-                if (t < 0) {
-                    // u[:-1].mean(axis=0): sequential column add for N >= 2,
-                    // numpy pairwise summation when the reduction collapses (N == 1).
-                    double sum;
-                    if (N >= 2) {
-                        sum = to_f64(col[0]);
-                        for (int k = 1; k < K1; k++)
-                            sum = dadd(sum, to_f64(col[static_cast<size_t>(k) * N]));
-                    } else {
-                        auto a = [col](int64_t k) { return to_f64(col[k]); };
-                        sum = np_pairwise_sum(a, 0, K1);
+                const T* col = u + static_cast<size_t>(rr) * Kr * N + n;
+                // one pass over the column: validation (horizon.py:47-50) + fp32 sums
+                float sf = 0.f, fin = 0.f;
+                if constexpr (KC > 0) {
+                    T x[KC];
+#pragma unroll
+                    for (int k = 0; k < KC; k++) x[k] = col[static_cast<size_t>(k) * N];
+#pragma unroll
+                    for (int k = 0; k < KC; k++) {
+                        if (!isfinite(x[k])) fl |= KR_FLAG_NONFINITE;
+                        if (x[k] < T(0)) fl |= KR_FLAG_NEGATIVE;
                     }
-                    const double m = ddiv(sum, static_cast<double>(K1));
-                    t = to_f64(col[static_cast<size_t>(K1) * N]) > dmul(opt, m);  // strict '>'
+                    sf = static_cast<float>(x[0]);
+#pragma unroll
+                    for (int k = 1; k < KC - 1; k++) sf = __fadd_rn(sf, static_cast<float>(x[k]));
+                    fin = static_cast<float>(x[KC - 1]);
+                } else {
+                    for (int k = 0; k < Kr; k++) {
+                        const T x = col[static_cast<size_t>(k) * N];
+                        if (!isfinite(x)) fl |= KR_FLAG_NONFINITE;
+                        if (x < T(0)) fl |= KR_FLAG_NEGATIVE;
+                        if (k == 0) sf = static_cast<float>(x);
+                        else if (k < Kr - 1) sf = __fadd_rn(sf, static_cast<float>(x));
+                        else fin = static_cast<float>(x);
+                    }
                 }
+                int t = sizeof(T) == 4 ? filter(sf, fin) : -1;
+                if (t < 0) t = exact(col);
                 trip = t;
             }
             first_flag(f, valid ? rr : -1, valid ? rr : -1, trip, n_q[q]);
@@ -122,8 +136,8 @@ struct ConfWork {
     }
 };
 
-template <typename T, bool kStaged>
-__global__ void __launch_bounds__(kStreamThreads) k_horizon_confidence(StreamPlan p, ConfWork<T> w) {
+template <typename T, int KC, bool kStaged>
+__global__ void __launch_bounds__(kStreamThreads) k_horizon_confidence(StreamPlan p, ConfWork<T, KC> w) {
     extern __shared__ __align__(128) unsigned char smem[];
     w.first = reinterpret_cast<int*>(smem + stream_aux_offset());
     for (int i = threadIdx.x; i < 2 * w.TR; i += blockDim.x) w.first[i] = INT_MAX;
@@ -424,18 +438,27 @@ extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_
     uint64_t rb = static_cast<uint64_t>(K) * N * es;
     if (N > kStreamThreads * kMaxRounds) return KR_EINVAL;
     const void* bases[1] = {U};
-    const int regs = dtype == KR_F64 ? kernel_regs(k_horizon_confidence<double, true>)
-                                     : kernel_regs(k_horizon_confidence<float, true>);
-    StreamPlan p = make_plan(1, bases, &rb, R, N, 2 * sizeof(int), kStreamThreads, regs);
+    const float c1 = static_cast<float>(one_plus_t / static_cast<double>(K - 1));
     cudaStream_t st = as_stream(stream);
+    auto go = [&](auto proto, auto kstaged, auto kdirect) {
+        using W = decltype(proto);
+        StreamPlan p = make_plan(1, bases, &rb, R, N, 2 * sizeof(int), kStreamThreads,
+                                 kernel_regs(kstaged));
+        W w{K, N, p.TR, min_horizon, p.rounds, one_plus_t, c1, H, flags, nullptr, {}, {}};
+        return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_confidence");
+    };
     if (dtype == KR_F64) {
-        ConfWork<double> w{K, N, p.TR, min_horizon, p.rounds, one_plus_t, H, flags, nullptr, {}, {}};
-        return launch_stream(k_horizon_confidence<double, true>, k_horizon_confidence<double, false>,
-                             p, w, st, "kr_horizon_confidence");
+        if (K == 6)
+            return go(ConfWork<double, 6>{}, k_horizon_confidence<double, 6, true>,
+                      k_horizon_confidence<double, 6, false>);
+        return go(ConfWork<double, 0>{}, k_horizon_confidence<double, 0, true>,
+                  k_horizon_confidence<double, 0, false>);
     }
-    ConfWork<float> w{K, N, p.TR, min_horizon, p.rounds, one_plus_t, H, flags, nullptr, {}, {}};
-    return launch_stream(k_horizon_confidence<float, true>, k_horizon_confidence<float, false>, p,
-                         w, st, "kr_horizon_confidence");
+    if (K == 6)
+        return go(ConfWork<float, 6>{}, k_horizon_confidence<float, 6, true>,
+                  k_horizon_confidence<float, 6, false>);
+    return go(ConfWork<float, 0>{}, k_horizon_confidence<float, 0, true>,
+              k_horizon_confidence<float, 0, false>);
 }
 
 template <typename T>

@@ -1,0 +1,60 @@
+"""Per-kernel throughput sweep over the BASELINE configs (run under gpurun):
+    python profiles/kernel_sweep.py [R]
+Prints one JSON line per variant: median device time of 10 warm launches
+(CUDA events on the launching stream) and algorithmic GB/s."""
+import json
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+import paper_2605_11381_b200 as kb  # noqa: E402
+from paper_2605_11381_b200 import synthetic  # noqa: E402
+from paper_2605_11381_b200.divergence import round_optimal_horizon_batch  # noqa: E402
+
+PEAK = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+
+
+def timeit(fn, reps=10):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return statistics.median(ts)
+
+
+def report(name, R, bytes_per, t):
+    gbs = bytes_per * R / t / 1e9
+    print(json.dumps({"variant": name, "robots": R, "bytes_per_robot_round": bytes_per,
+                      "ms": t * 1e3, "GBps": round(gbs, 1), "frac_of_measured_peak": round(gbs / PEAK, 3),
+                      "robot_rounds_per_s": R / t}), flush=True)
+
+
+def main():
+    R = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
+    for K, N, dt, es in [(6, 50, torch.float32, 4), (6, 50, torch.float64, 8), (6, 64, torch.float32, 4)]:
+        U = synthetic.magnitudes(R, seed=3, K=K, N=N, dtype=dt)
+        cfg = kb.HorizonPolicyConfig.confidence(0.4, 5)
+        out = torch.empty(R, dtype=torch.int32, device="cuda")
+        t = timeit(lambda: kb.decide_horizon_batch(cfg, U, out=out, validate=False))
+        report(f"confidence K={K} N={N} {str(dt)[6:]}", R, K * N * es + 4, t)
+        del U
+    for S, L, D, RR in [(1, 50, 7, R), (1, 64, 32, R // 2), (8, 50, 7, R // 4)]:
+        prev, cand, off = synthetic.chunks(RR, seed=5, Lp=L, Lc=L, D=D, S=S)
+        out = torch.empty(RR, dtype=torch.int32, device="cuda")
+        t = timeit(lambda: round_optimal_horizon_batch(prev, cand, 0.9, offset=off, out=out))
+        report(f"divergence S={S} L={L} D={D} fp32", RR, (1 + S) * L * D * 4 + 8, t)
+        del prev, cand
+
+
+if __name__ == "__main__":
+    main()

@@ -214,8 +214,8 @@ __device__ __forceinline__ double cosine_skx_fixed(const T* a, const T* b) {
 // The reference decides `cos < thr` on an fp64 cosine.  For fp32-representable
 // inputs an fp32 evaluation of the same cosine is within a proven bound of the
 // exact value: every dot is off by at most gamma_D = D*2^-24 relative to
-// sum|x_i*y_i| <= |x||y| (Cauchy-Schwarz), rsqrtf by 2 ulp, and the two
-// products by 1 ulp each, so |c32 - c| <= 2*gamma_D + 2^-20 + 2^-22; the fp64
+// sum|x_i*y_i| <= |x||y| (Cauchy-Schwarz), rsqrt.approx by 2^-22.9, and the
+// two products by 1/2 ulp each, so |c32 - c| <= 2*gamma_D + 2^-21; the fp64
 // result differs from c by < 2^-48.  Whenever |c32 - thr| exceeds
 // margin = (2D + 24) * 2^-24 + 2^-20 the decision is therefore already known;
 // only the rare near-threshold actions (and zero / extreme-range vectors) fall
@@ -228,10 +228,17 @@ __host__ __device__ inline float cos_filter_margin(int D) {
 // The bound holds for any summation order, so rows whose length is a multiple
 // of 32 words are read starting at a lane-rotated element: lanes scoring
 // consecutive rows (all starting at bank 0) then hit 32 distinct banks.
+__device__ __forceinline__ float rsqrt_approx_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// c = xy / sqrt(xx * yy) with one MUFU: the range guard keeps xx * yy a normal
+// float, and rsqrt.approx's 2^-22.9 relative error is inside the margin.
 __device__ __forceinline__ int cos_filter_decide(float xx, float yy, float xy, float thr_f,
                                                  float margin) {
-    if (!(xx >= 1e-30f && yy >= 1e-30f && xx <= 1e30f && yy <= 1e30f)) return -1;
-    const float c = __fmul_rn(__fmul_rn(xy, rsqrtf(xx)), rsqrtf(yy));
+    if (!(xx >= 1e-18f && yy >= 1e-18f && xx <= 1e18f && yy <= 1e18f)) return -1;
+    const float c = __fmul_rn(xy, rsqrt_approx_ftz(__fmul_rn(xx, yy)));
     const float d = __fsub_rn(c, thr_f);
     if (d > margin) return 1;
     if (d < -margin) return 0;

@@ -176,9 +176,13 @@ struct DivWork {
 
     __device__ __forceinline__ int2 meta(const TileView& v, int rr) const {
         int o = has_off ? reinterpret_cast<const int32_t*>(v.seg[2])[rr] : 0;
+        o = o < 0 ? 0 : o;
+        if (!has_lp && !has_lc) {  // common case: only the overlap offset varies
+            const int lr = Lp - o;
+            return make_int2(o, lr < Lc ? (lr < 0 ? 0 : lr) : Lc);
+        }
         int lp = has_lp ? reinterpret_cast<const int32_t*>(v.seg[3])[rr] : Lp;
         int lc = has_lc ? reinterpret_cast<const int32_t*>(v.seg[4])[rr] : Lc;
-        o = o < 0 ? 0 : o;
         lp = lp > Lp ? Lp : lp;
         lc = lc > Lc ? Lc : (lc < 0 ? 0 : lc);
         int lr = lp - o;

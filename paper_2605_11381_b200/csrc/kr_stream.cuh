@@ -119,9 +119,20 @@ __device__ __forceinline__ void stream_run(const StreamPlan& p, unsigned char* s
     }
     int s = 0;           // ring slot of tile i
     uint32_t phase = 0;  // mbarrier parity of that slot's current fill
+    // fleets below 2^31 robots (always, in practice) keep the tile arithmetic in 32 bits
+    const bool small = p.R < (int64_t(1) << 31);
     for (int64_t i = 0; i < nlocal; i++) {
-        const int64_t r0 = (blockIdx.x + i * gridDim.x) * p.TR;
-        const int nr = static_cast<int>(p.R - r0 < p.TR ? p.R - r0 : p.TR);
+        int64_t r0;
+        int nr;
+        if (small) {
+            const int r32 = (static_cast<int>(blockIdx.x) + static_cast<int>(i) * static_cast<int>(gridDim.x)) * p.TR;
+            const int left = static_cast<int>(p.R) - r32;
+            r0 = r32;
+            nr = left < p.TR ? left : p.TR;
+        } else {
+            r0 = (blockIdx.x + i * gridDim.x) * p.TR;
+            nr = static_cast<int>(p.R - r0 < p.TR ? p.R - r0 : p.TR);
+        }
         unsigned char* buf = bufs + static_cast<size_t>(s) * p.stage_bytes;
         TileView v;
         if constexpr (!kStaged) {

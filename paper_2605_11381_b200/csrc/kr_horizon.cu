@@ -33,14 +33,14 @@ struct ConfWork {
     float c1;     // (float)(opt / (K - 1)): the fp32 filter's mean-and-scale factor
     int32_t* H;
     uint32_t* flags;
-    int* first;                  // [2][TR] first tripping column per robot
+    int* first;                  // [kMaxStages][TR] first tripping column per robot
     int rr_q[kMaxRounds];        // this thread's robot slot per round (-1: none)
     int n_q[kMaxRounds];         // ... and column
 
     __device__ void setup(int threads) {
         for (int q = 0; q < kMaxRounds; q++) {
             const int j = threadIdx.x + q * threads;
-            const bool ok = q < rounds && j < TR * N;
+            const bool ok = q < rounds && j < TR * N && static_cast<int>(threadIdx.x) < threads;
             rr_q[q] = ok ? j / N : -1;
             n_q[q] = ok ? j - (j / N) * N : 0;
         }
@@ -77,9 +77,9 @@ struct ConfWork {
         return to_f64(col[static_cast<size_t>(K1) * N]) > dmul(opt, m);  // strict '>'
     }
 
-    __device__ __forceinline__ void tile(const TileView& v, int64_t, int nr, int64_t local) {
+    __device__ __forceinline__ void tile(const TileView& v, int64_t, int nr, int slot) {
         const T* u = reinterpret_cast<const T*>(v.seg[0]);
-        int* f = first + (local & 1) * TR;
+        int* f = first + slot * TR;
         uint32_t fl = 0;
         const int Kr = KC > 0 ? KC : K;
 #pragma unroll
@@ -125,9 +125,9 @@ struct ConfWork {
         if (fl && flags) atomicOr(flags, fl);
     }
 
-    __device__ __forceinline__ void finish(int64_t r0, int nr, int64_t local) {
-        int* f = first + (local & 1) * TR;
-        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+    __device__ __forceinline__ void finish(int64_t r0, int nr, int slot, int t, int nt) {
+        int* f = first + slot * TR;
+        for (int rr = t; rr < nr; rr += nt) {
             int h = f[rr] < N ? f[rr] : N;  // argmax of trips, or N
             h = h > hmin ? h : hmin;
             H[r0 + rr] = h < N ? h : N;
@@ -140,7 +140,7 @@ template <typename T, int KC, bool kStaged>
 __global__ void __launch_bounds__(kStreamThreads) k_horizon_confidence(StreamPlan p, ConfWork<T, KC> w) {
     extern __shared__ __align__(128) unsigned char smem[];
     w.first = reinterpret_cast<int*>(smem + stream_aux_offset());
-    for (int i = threadIdx.x; i < 2 * w.TR; i += blockDim.x) w.first[i] = INT_MAX;
+    for (int i = threadIdx.x; i < kMaxStages * w.TR; i += blockDim.x) w.first[i] = INT_MAX;
     w.setup(p.threads);
     __syncthreads();
     stream_run<kStaged>(p, smem, w);
@@ -157,15 +157,15 @@ struct DivWork {
     int32_t* H;
     double* cos;
     float thr_f, margin;
-    int* first;                   // [2][TR] first failing action per robot
-    int* lim;                     // [2][TR] prefix limit per robot
+    int* first;                   // [kMaxStages][TR] first failing action per robot
+    int* lim;                     // [kMaxStages][TR] prefix limit per robot
     int rr_q[kMaxRounds], s_q[kMaxRounds], i_q[kMaxRounds];
 
     __device__ void setup(int threads) {
         const int per = S * Lc;
         for (int q = 0; q < kMaxRounds; q++) {
             const int j = threadIdx.x + q * threads;
-            const bool ok = q < rounds && j < TR * per;
+            const bool ok = q < rounds && j < TR * per && static_cast<int>(threadIdx.x) < threads;
             const int rr = ok ? j / per : -1;
             const int rem = ok ? j - rr * per : 0;
             rr_q[q] = rr;
@@ -190,11 +190,11 @@ struct DivWork {
         return make_int2(o, lr < lc ? lr : lc);
     }
 
-    __device__ __forceinline__ void tile(const TileView& v, int64_t r0, int nr, int64_t local) {
+    __device__ __forceinline__ void tile(const TileView& v, int64_t r0, int nr, int slot) {
         const T* prev = reinterpret_cast<const T*>(v.seg[0]);
         const T* cand = reinterpret_cast<const T*>(v.seg[1]);
-        int* f = first + (local & 1) * TR;
-        int* lm = lim + (local & 1) * TR;
+        int* f = first + slot * TR;
+        int* lm = lim + slot * TR;
         const int D_ = DC > 0 ? DC : D;
 #pragma unroll
         for (int q = 0; q < kMaxRounds; q++) {
@@ -234,10 +234,10 @@ struct DivWork {
         }
     }
 
-    __device__ __forceinline__ void finish(int64_t r0, int nr, int64_t local) {
-        int* f = first + (local & 1) * TR;
-        const int* lm = lim + (local & 1) * TR;
-        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+    __device__ __forceinline__ void finish(int64_t r0, int nr, int slot, int t, int nt) {
+        int* f = first + slot * TR;
+        const int* lm = lim + slot * TR;
+        for (int rr = t; rr < nr; rr += nt) {
             H[r0 + rr] = f[rr] < lm[rr] ? f[rr] : lm[rr];
             f[rr] = INT_MAX;
         }
@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(div_max_threads<DC>()) k_horizon_divergence(St
                                                                              DivWork<T, DC> w) {
     extern __shared__ __align__(128) unsigned char smem[];
     w.first = reinterpret_cast<int*>(smem + stream_aux_offset());
-    w.lim = w.first + 2 * w.TR;
-    for (int i = threadIdx.x; i < 2 * w.TR; i += blockDim.x) w.first[i] = INT_MAX;
+    w.lim = w.first + kMaxStages * w.TR;
+    for (int i = threadIdx.x; i < kMaxStages * w.TR; i += blockDim.x) w.first[i] = INT_MAX;
     w.setup(p.threads);
     __syncthreads();
     stream_run<kStaged>(p, smem, w);
@@ -314,8 +314,9 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
         const uint64_t sb = stage_bytes(t);
         const uint64_t aux = (256 + t * aux_per_robot + 127) & ~uint64_t(127);
         const bool tma = tma_ok(t);
-        int per_sm = 65536 / (regs * threads);
-        per_sm = per_sm < 2048 / threads ? per_sm : 2048 / threads;
+        const int cta = threads + 32;  // + the producer warp
+        int per_sm = 65536 / (regs * cta);
+        per_sm = per_sm < 2048 / cta ? per_sm : 2048 / cta;
         per_sm = per_sm > 4 ? 4 : per_sm;
         for (; per_sm >= 1; per_sm--) {
             const uint64_t budget = smem_sm / per_sm - 1024 - 128;  // 1 KB reserved per CTA
@@ -324,9 +325,9 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
         if (per_sm < 1) continue;
         const uint64_t budget = smem_sm / per_sm - 1024 - 128;
         int stages = static_cast<int>((budget - aux) / sb);
-        stages = stages > 8 ? 8 : stages;
+        stages = stages > kMaxStages ? kMaxStages : stages;
         const double inflight = static_cast<double>(per_sm) * (stages - 1) * sb;
-        const double warps = per_sm * threads / 32.0;
+        const double warps = per_sm * cta / 32.0;
         double score = 1.0 - static_cast<double>(items) / (static_cast<double>(rounds) * threads);
         if (inflight < kInflightTarget) score += 0.5 * (1.0 - inflight / kInflightTarget);
         if (warps < 24.0) score += 0.2 * (1.0 - warps / 24.0);
@@ -399,7 +400,7 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
             }
             if (f.occ_threads != p.threads || f.occ_smem != static_cast<int>(smem)) {
                 KR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.occ_blocks, kern,
-                                                                          p.threads, smem));
+                                                                          p.threads + 32, smem));
                 f.occ_threads = p.threads;
                 f.occ_smem = static_cast<int>(smem);
             }
@@ -410,7 +411,7 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
         int64_t grid = static_cast<int64_t>(device_info().sm_count) * per_sm;
         if (grid > ntiles) grid = ntiles;
         if (grid < 1) grid = 1;
-        kern<<<static_cast<unsigned>(grid), p.threads, smem, st>>>(p, w);
+        kern<<<static_cast<unsigned>(grid), p.threads + 32, smem, st>>>(p, w);
         return check_launch(name);
     };
     return p.mode == kModeDirect ? go(kdirect) : go(kstaged);
@@ -440,13 +441,13 @@ extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_
     if (!U || !H) return KR_EINVAL;
     const size_t es = dtype == KR_F64 ? 8 : 4;
     uint64_t rb = static_cast<uint64_t>(K) * N * es;
-    if (N > kStreamThreads * kMaxRounds) return KR_EINVAL;
+    if (N > (kStreamThreads - 32) * kMaxRounds) return KR_EINVAL;
     const void* bases[1] = {U};
     const float c1 = static_cast<float>(one_plus_t / static_cast<double>(K - 1));
     cudaStream_t st = as_stream(stream);
     auto go = [&](auto proto, auto kstaged, auto kdirect) {
         using W = decltype(proto);
-        StreamPlan p = make_plan(1, bases, &rb, R, N, 2 * sizeof(int), kStreamThreads,
+        StreamPlan p = make_plan(1, bases, &rb, R, N, kMaxStages * sizeof(int), kStreamThreads - 32,
                                  kernel_regs(kstaged));
         W w{K, N, p.TR, min_horizon, p.rounds, one_plus_t, c1, H, flags, nullptr, {}, {}};
         return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_confidence");
@@ -513,7 +514,7 @@ extern "C" int kr_horizon_divergence(const void* prev, const void* cand, int dty
     uint64_t rbs[5] = {rb[0], rb[1], offset ? 4u : 0u, len_prev ? 4u : 0u, len_cand ? 4u : 0u};
     const int nseg = 5;
     const int maxt = D == 7 ? kStreamThreads : 256;  // only D = 7 has a small-D kernel
-    if (static_cast<int64_t>(S) * Lc > static_cast<int64_t>(maxt) * kMaxRounds) return KR_EINVAL;
+    if (static_cast<int64_t>(S) * Lc > static_cast<int64_t>(maxt - 32) * kMaxRounds) return KR_EINVAL;
     int regs;
     if (dtype == KR_F64)
         regs = D == 7 ? kernel_regs(k_horizon_divergence<double, 7, true>)
@@ -523,7 +524,8 @@ extern "C" int kr_horizon_divergence(const void* prev, const void* cand, int dty
         regs = D == 7 ? kernel_regs(k_horizon_divergence<float, 7, true>)
                       : (D == 32 ? kernel_regs(k_horizon_divergence<float, 32, true>)
                                  : kernel_regs(k_horizon_divergence<float, 0, true>));
-    StreamPlan p = make_plan(nseg, bases, rbs, R, S * Lc, 4 * sizeof(int), maxt, regs);
+    StreamPlan p = make_plan(nseg, bases, rbs, R, S * Lc, 2 * kMaxStages * sizeof(int), maxt - 32,
+                             regs);
     cudaStream_t st = as_stream(stream);
     const float thr_f = static_cast<float>(thr);
     const float margin = cos_filter_margin(D);

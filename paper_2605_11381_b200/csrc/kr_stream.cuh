@@ -25,6 +25,7 @@ namespace kr {
 constexpr int kMaxSeg = 5;
 constexpr int kMaxRounds = 4;      // item positions per thread per tile
 constexpr int kStreamThreads = 1024;
+constexpr int kMaxStages = 8;      // ring depth (mbarrier slots)
 
 // Segments have fixed slots (unused slots: rbytes 0) so that every segment
 // pointer is a compile-time-indexed register, never a local-memory array.
@@ -38,14 +39,14 @@ struct StreamPlan {
     int TR;                              // robots per tile
     int stages;
     int mode;                            // 0 = TMA bulk, 1 = plain staged, 2 = direct
-    int threads;                         // CTA size
+    int threads;                         // consumer threads (the CTA adds one producer warp)
     int rounds;                          // ceil(TR * items_per_robot / threads) <= kMaxRounds
     int64_t R;
 };
 
 enum { kModeBulk = 0, kModePlain = 1, kModeDirect = 2 };
 
-// Shared-memory layout: [mbarriers (8 B x stages, padded to 128)] [aux] [stages]
+// Shared-memory layout: [full[8], empty[8] mbarriers (128 B)] [aux] [stages]
 __host__ __device__ inline uint32_t stream_aux_offset() { return 128; }
 __host__ __device__ inline uint32_t stream_buf_offset(const StreamPlan& p) {
     return (stream_aux_offset() + p.aux_bytes + 127u) & ~127u;
@@ -91,39 +92,50 @@ struct TileView {
 };
 
 // Work must provide:
-//   __device__ void tile(const TileView& v, int64_t r0, int nr, int64_t local);
-//   __device__ void finish(int64_t r0, int nr, int64_t local);
-// kStaged selects shared-memory staging (TMA bulk or plain) at compile time so
-// that the scoring loads compile to LDS; !kStaged reads global memory.
+//   __device__ void tile(const TileView& v, int64_t r0, int nr, int slot);
+//   __device__ void finish(int64_t r0, int nr, int slot, int lane, int nlanes);
+// `slot` is the ring slot of the tile (per-slot scratch such as first-trip
+// indices is reused only when that slot is refilled).  kStaged selects shared-
+// memory staging (TMA bulk or plain) at compile time so that the scoring loads
+// compile to LDS; !kStaged reads global memory.
+//
+// TMA mode synchronises through mbarriers only: full[s] (TMA bytes landed) and
+// empty[s] (every warp finished reading slot s).  Warp 0 waits on empty[s],
+// finishes the tile (writes its outputs, resets the slot scratch) and refills
+// the slot; the other warps run ahead to the next landed tile without a
+// block-wide barrier.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
 template <bool kStaged, class Work>
 __device__ __forceinline__ void stream_run(const StreamPlan& p, unsigned char* smem, Work& work) {
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + 8;
     unsigned char* bufs = smem + stream_buf_offset(p);
     const int64_t ntiles = (p.R + p.TR - 1) / p.TR;
     if (blockIdx.x >= ntiles) return;
     const int64_t nlocal = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    uint64_t pol = 0;
     const bool bulk = kStaged && p.mode == kModeBulk;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int consumer_warps = p.threads >> 5;     // the last warp is the producer
+    const bool producer = warp == consumer_warps;
+    uint64_t pol = 0;
     if (bulk) {
         pol = policy_evict_first();
         if (threadIdx.x == 0) {
-            for (int s = 0; s < p.stages; s++) mbar_init(&mbar[s], 1);
+            for (int s = 0; s < p.stages; s++) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], consumer_warps);
+            }
             fence_mbar_init();
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int64_t pre = nlocal < p.stages ? nlocal : p.stages;
-            for (int64_t i = 0; i < pre; i++)
-                stream_issue(p, bufs + static_cast<size_t>(i) * p.stage_bytes, &mbar[i], i, pol);
-        }
     }
-    int s = 0;           // ring slot of tile i
-    uint32_t phase = 0;  // mbarrier parity of that slot's current fill
     // fleets below 2^31 robots (always, in practice) keep the tile arithmetic in 32 bits
     const bool small = p.R < (int64_t(1) << 31);
-    for (int64_t i = 0; i < nlocal; i++) {
-        int64_t r0;
-        int nr;
+    auto tile_of = [&](int64_t i, int64_t& r0, int& nr) {
         if (small) {
             const int r32 = (static_cast<int>(blockIdx.x) + static_cast<int>(i) * static_cast<int>(gridDim.x)) * p.TR;
             const int left = static_cast<int>(p.R) - r32;
@@ -133,33 +145,78 @@ __device__ __forceinline__ void stream_run(const StreamPlan& p, unsigned char* s
             r0 = (blockIdx.x + i * gridDim.x) * p.TR;
             nr = static_cast<int>(p.R - r0 < p.TR ? p.R - r0 : p.TR);
         }
+    };
+    if (bulk && producer) {
+        // producer warp: fill the ring, then per tile wait until every consumer
+        // warp has released the slot, finish the tile, refill the slot
+        if (lane == 0) {
+            int64_t pre = nlocal < p.stages ? nlocal : p.stages;
+            for (int64_t i = 0; i < pre; i++)
+                stream_issue(p, bufs + static_cast<size_t>(i) * p.stage_bytes, &full[i], i, pol);
+        }
+        int s = 0;
+        uint32_t phase = 0;
+        for (int64_t i = 0; i < nlocal; i++) {
+            int64_t r0;
+            int nr;
+            tile_of(i, r0, nr);
+            mbar_wait(&empty[s], phase);
+            work.finish(r0, nr, s, lane, 32);
+            __syncwarp();
+            if (lane == 0 && i + p.stages < nlocal)
+                stream_issue(p, bufs + static_cast<size_t>(s) * p.stage_bytes, &full[s],
+                             i + p.stages, pol);
+            if (++s == p.stages) {
+                s = 0;
+                phase ^= 1u;
+            }
+        }
+        return;
+    }
+    int s = 0;           // ring slot of tile i
+    uint32_t phase = 0;  // mbarrier parity of that slot's current fill
+    for (int64_t i = 0; i < nlocal; i++) {
+        int64_t r0;
+        int nr;
+        tile_of(i, r0, nr);
         unsigned char* buf = bufs + static_cast<size_t>(s) * p.stage_bytes;
         TileView v;
         if constexpr (!kStaged) {
 #pragma unroll
             for (int g = 0; g < kMaxSeg; g++) v.seg[g] = p.base[g] + r0 * p.rbytes[g];
+            work.tile(v, r0, nr, 0);
+            __syncthreads();
+            work.finish(r0, nr, 0, threadIdx.x, blockDim.x);
+            __syncthreads();
+        } else if (!bulk) {  // plain staging: one buffer, block barriers
+            stream_copy_plain(p, buf, r0, nr, false);
+            __syncthreads();
+#pragma unroll
+            for (int g = 0; g < kMaxSeg; g++) v.seg[g] = buf + p.soff[g];
+            work.tile(v, r0, nr, 0);
+            __syncthreads();
+            work.finish(r0, nr, 0, threadIdx.x, blockDim.x);
+            __syncthreads();
         } else {
-            if (bulk) {
-                mbar_wait(&mbar[s], phase);
-                if (nr < p.TR) {  // tail tile: sub-16-byte remainder by hand
-                    stream_copy_plain(p, buf, r0, nr, true);
-                    __syncthreads();
+            mbar_wait(&full[s], phase);
+            if (nr < p.TR) {  // last tile: sub-16-byte remainder by hand (generic-proxy writes)
+                for (int g = 0; g < kMaxSeg; g++) {
+                    if (p.rbytes[g] == 0) continue;
+                    const uint32_t bytes = static_cast<uint32_t>(nr * p.rbytes[g]);
+                    const uint32_t* src = reinterpret_cast<const uint32_t*>(p.base[g] + r0 * p.rbytes[g]);
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(buf + p.soff[g]);
+                    for (uint32_t w = (bytes & ~15u) / 4 + threadIdx.x; w < bytes / 4; w += p.threads)
+                        dst[w] = __ldg(src + w);
                 }
-            } else {
-                stream_copy_plain(p, buf, r0, nr, false);
-                __syncthreads();
+                fence_proxy_async_smem();
+                asm volatile("bar.sync 1, %0;" ::"r"(p.threads));  // consumer warps only
             }
 #pragma unroll
             for (int g = 0; g < kMaxSeg; g++) v.seg[g] = buf + p.soff[g];
+            work.tile(v, r0, nr, s);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
         }
-        work.tile(v, r0, nr, i);
-        // Order this tile's generic-proxy shared-memory traffic before the TMA
-        // refill of the same buffer.
-        if (bulk) fence_proxy_async_smem();
-        __syncthreads();
-        if (bulk && threadIdx.x == 0 && i + p.stages < nlocal)
-            stream_issue(p, buf, &mbar[s], i + p.stages, pol);
-        work.finish(r0, nr, i);  // must not touch the (possibly refilling) buffer
         if (++s == p.stages) {
             s = 0;
             phase ^= 1u;

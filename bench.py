@@ -27,7 +27,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -62,52 +61,64 @@ def workload_config(args, world):
 # --------------------------------------------------------------------------
 # clocks (NVML, sampled during the timed region)
 # --------------------------------------------------------------------------
+def _clock_poll(index, stop, out):
+    """Child process: poll NVML SM clock + throttle reasons until `stop` is set."""
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(index)
+    samples, masks = [], 0
+    while not stop.is_set():
+        try:
+            samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            masks |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            pass
+        time.sleep(0.0005)
+    out.put((samples, masks, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
+
+
 class ClockSampler:
+    """NVML clock / throttle-reason sampling in a forked process (no GIL
+    contention with the launching thread) for the duration of a `with` block."""
     REASONS = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown",
     }
 
     def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self.nv = None
-        self.t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.002)
+        import multiprocessing as mp
+        self.ctx = mp.get_context("fork")
+        self.index = index
+        self.result = ([], 0, None)
 
     def __enter__(self):
-        if self.nv:
-            self.t.start()
+        try:
+            import pynvml  # noqa: F401
+            self.stop = self.ctx.Event()
+            self.q = self.ctx.Queue()
+            self.proc = self.ctx.Process(target=_clock_poll, args=(self.index, self.stop, self.q),
+                                         daemon=True)
+            self.proc.start()
+            time.sleep(0.05)  # first samples before the timed region starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self.nv:
-            self.t.join()
+        if self.proc is not None:
+            self.stop.set()
+            try:
+                self.result = self.q.get(timeout=10)
+            except Exception:
+                pass
+            self.proc.join(timeout=10)
 
     def summary(self):
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        samples, mask, max_mhz = self.result
+        return {"sm_mhz": statistics.median(samples) if samples else None, "sm_max_mhz": max_mhz,
+                "reasons": sorted(n for b, n in self.REASONS.items() if mask & b),
+                "samples": len(samples)}
 
 
 def hbm_peak():

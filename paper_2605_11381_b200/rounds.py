@@ -183,8 +183,12 @@ class CudaShardOps:
         return r.cand
 
     def all_gather(self, cand):
-        # the only cross-GPU traffic of a round: W x k' x 16 B over NVLink
-        dist.all_gather_into_tensor(self.r.gathered, cand, group=self.r.group)
+        # the only cross-GPU traffic of a round: W x k' x 16 B over NVLink (NCCL)
+        if dist.get_backend(self.r.group) == "nccl":
+            dist.all_gather_into_tensor(self.r.gathered, cand, group=self.r.group)
+        else:  # gloo (tests: several ranks sharing one device)
+            parts = list(self.r.gathered.chunk(self.r.world))
+            dist.all_gather(parts, cand, group=self.r.group)
         return self.r.gathered
 
     def kth(self, keys, k):
@@ -218,6 +222,7 @@ class ShardedDecisionRound(DecisionRound):
 
     def __init__(self, R_local: int, k: int, sched: _lib.KrSched, group=None):
         super().__init__(R_local, k, sched)
+        self.k_request = k  # the global budget (self.k is clamped to the local shard)
         self.group = group
         self.world = dist.get_world_size(group)
         sizes = torch.tensor([R_local], dtype=torch.int64, device=self.H.device)
@@ -235,7 +240,8 @@ class ShardedDecisionRound(DecisionRound):
         self.ws_merge = fl.Workspace(kg * self.world)
 
     def admit(self, fleet: fl.DeviceFleet) -> None:
-        sharded_topk(self.keys, self.R, self.k, self.sizes, CudaShardOps(self, fleet), self.group)
+        sharded_topk(self.keys, self.R, self.k_request, self.sizes, CudaShardOps(self, fleet),
+                     self.group)
 
     def outputs(self) -> RoundOutputs:
         return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,

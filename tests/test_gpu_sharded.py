@@ -1,0 +1,87 @@
+"""The robot-sharded decision round (rounds.ShardedDecisionRound) with its CUDA
+primitives: 2 ranks sharing cuda:0 over gloo (one B200 in this environment; on
+a multi-GPU box the same code runs one rank per GPU over NCCL).  Global
+admission, the ordered global S_e and every rank's masks / skip counters must
+equal a single-GPU DecisionRound over the whole fleet."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, sizes, k, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+        lo = sum(sizes[:rank])
+        soa = synthetic.fleet_soa(sum(sizes), seed=21)
+        mine = {k2: (v[lo:lo + sizes[rank]] if isinstance(v, np.ndarray) and k2 != "slots" else v)
+                for k2, v in soa.items()}
+        # re-base this shard's CSR history
+        off = soa["hist_off"][lo:lo + sizes[rank]]
+        nsl = np.maximum(soa["n_exec"], soa["n_gen"])[lo:lo + sizes[rank]]
+        rows = np.concatenate([np.arange(o, o + n) for o, n in zip(off, nsl)]) if len(off) else []
+        mine["slots"] = soa["slots"][np.asarray(rows, np.int64)] if len(rows) else np.zeros((1, 4), np.int64)
+        mine["hist_off"] = np.concatenate([[0], np.cumsum(nsl)[:-1]]).astype(np.int64)
+        mine["n"] = sizes[rank]
+        base = int(soa["issued_at"].min())
+        sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, base)
+        fleet = fl.DeviceFleet.from_host(mine)
+        rnd = rounds.ShardedDecisionRound(sizes[rank], k, sched)
+        rnd.urgency(fleet)
+        rnd.admit(fleet)
+        torch.cuda.synchronize()
+        q.put((rank, rnd.admitted.cpu().numpy(), fleet.t["skipped"].cpu().numpy(),
+               rnd.global_edge[: rnd.k_global].cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sizes,k", [([30000, 20000], 4096), ([100, 5000], 300), ([2000, 2000], 3990)])
+def test_sharded_round_matches_single_gpu(sizes, k):
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, len(sizes), port, sizes, k, q))
+             for r in range(len(sizes))]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in sizes], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    soa = synthetic.fleet_soa(sum(sizes), seed=21)
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    fleet = fl.DeviceFleet.from_host(soa)
+    ref = rounds.DecisionRound(sum(sizes), k, sched)
+    ref.urgency(fleet)
+    ref.admit(fleet)
+    torch.cuda.synchronize()
+    adm = np.concatenate([r[1] for r in res])
+    skp = np.concatenate([r[2] for r in res])
+    assert np.array_equal(adm, ref.admitted.cpu().numpy())
+    assert np.array_equal(skp, fleet.t["skipped"].cpu().numpy())
+    for r in res:  # identical ordered global S_e on every rank == single-GPU S_e keys
+        assert np.array_equal(r[3], ref.edge_keys[:k].cpu().numpy())

@@ -18,6 +18,8 @@
  *   kr_select_admit         scheduler.py:193-241 select + admission + ordered S_e
  *   kr_admit                scheduler.py:223-234 refetch + skip counters
  *   kr_sort_keys            scheduler.py:130-140 the total order itself
+ *   kr_transfer_time        engines.py:158-169   per-request uplink time
+ *   kr_place_cloud          scheduler.py:160-234 phase-3 cloud offload scan
  *
  * Conventions: every pointer argument that names device data is a device
  * pointer; kr_fleet / kr_sched structs themselves live in host memory.  All
@@ -179,6 +181,22 @@ KR_API int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
                            const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
                            int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* workspace,
                            size_t workspace_bytes, void* stream);
+/* ---- phase 3: hybrid edge / cloud placement --------------------------- */
+
+/* out[i] = base_us + round_half_up(payload[i] * 8e6 / bps)   (engines.py:158-169) */
+KR_API int kr_transfer_time(const int64_t* payload, int64_t n, int64_t base_us, int64_t bps,
+                            int64_t* out, void* stream);
+/* scheduler.py:210-234 cloud offload after the edge prefix of `order` (the
+ * full reference order, n_edge = |S_e|): request r is offloaded iff
+ * up_us[r] < thresholds[c] with c = offloads so far (< cap), where
+ * thresholds[c] = edge_est - (cloud drain(c) + cloud batch latency(c) +
+ * downlink), INT64_MAX without an edge tier.  Offloaded requests get skip
+ * counter 0 and their refetch flag; cloud_idx[0..*n_cloud) is S_c in order. */
+KR_API int kr_place_cloud(const int32_t* order, int64_t n, int64_t n_edge, const int64_t* up_us,
+                          const int64_t* thresholds, int64_t cap, const kr_fleet* fleet,
+                          const kr_sched* cfg, uint8_t* refetch, int32_t* cloud_idx,
+                          int32_t* n_cloud, void* stream);
+
 /* Full argsort of n unique keys (ascending).  Synchronises `stream` once
  * when n exceeds the single-CTA limit (pass plan read back to the host). */
 KR_API int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_key* sorted_keys,

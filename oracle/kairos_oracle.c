@@ -347,3 +347,88 @@ int64_t orc_plan(const orc_fleet* f, int policy, int64_t buckets,
     free(bkt);
     return n_edge;
 }
+
+/* ---------------------------------------------------------------------------
+ * Phase 3: hybrid placement (scheduler.py:160-241, engines.py:132-169)
+ * ------------------------------------------------------------------------- */
+
+/* engines.py:132-155: exact at profiled points, linear interpolation between
+ * them rounded half-up (lat_lo is an integer, so only the fraction rounds). */
+int64_t orc_batch_latency(const orc_profile* p, int64_t batch) {
+    if (batch <= p->batch[0]) return p->latency[0];
+    for (int32_t i = 0; i + 1 < p->npts; i++) {
+        int64_t blo = p->batch[i], bhi = p->batch[i + 1];
+        int64_t llo = p->latency[i], lhi = p->latency[i + 1];
+        if (batch == bhi) return lhi;
+        if (blo < batch && batch < bhi) {
+            __int128 num = (__int128)(lhi - llo) * (batch - blo), den = bhi - blo;
+            return llo + (int64_t)((2 * num + den) / (2 * den));
+        }
+    }
+    return p->latency[p->npts - 1];
+}
+
+/* engines.py:158-169: base latency + round_half_up(bytes * 8e6 / bps). */
+int64_t orc_transfer_time(const orc_net* net, int64_t payload_bytes, int up) {
+    int64_t bps = up ? net->uplink_bps : net->downlink_bps;
+    __int128 num = (__int128)payload_bytes * 8 * 1000000;
+    return net->base_latency_us + (int64_t)((2 * num + bps) / (2 * (__int128)bps));
+}
+
+/* scheduler.py:160-164 */
+static int64_t orc_drain(const orc_profile* p, int64_t queued) {
+    if (queued <= 0) return 0;
+    int64_t waves = (queued + p->max_batch - 1) / p->max_batch;
+    return waves * orc_batch_latency(p, p->max_batch);
+}
+
+int64_t orc_plan_tiers(const orc_fleet* f, const int64_t* payload, int policy, int64_t buckets,
+                       int64_t aging_interval, int64_t stale_threshold,
+                       int64_t default_exec_estimate, int64_t now, const orc_profile* edge,
+                       const orc_profile* cloud, const orc_net* net, int64_t edge_in_flight,
+                       int64_t cloud_in_flight, int32_t* order, uint8_t* tier,
+                       int32_t* cloud_order, uint8_t* refetch, int32_t* skipped_out,
+                       int64_t* n_edge_out) {
+    int64_t n = f->n;
+    /* phases 1-2: the reference order (orc_plan with no edge budget) */
+    orc_plan(f, policy, buckets, aging_interval, stale_threshold, default_exec_estimate, now, 30,
+             1, 0, order, NULL, NULL, NULL, NULL, NULL, NULL, NULL, NULL);
+    /* scheduler.py:204-207 */
+    int64_t edge_avail = edge ? edge->capacity - edge_in_flight : 0;
+    int64_t cloud_avail = cloud ? cloud->capacity - cloud_in_flight : 0;
+    if (edge_avail < 0) edge_avail = 0;
+    if (cloud_avail < 0) cloud_avail = 0;
+    int64_t n_edge = edge_avail < n ? edge_avail : n;
+    for (int64_t p = 0; p < n; p++) tier[order[p]] = p < n_edge ? 1 : 0;
+    /* scheduler.py:210-221: greedy cloud offload over the rest, in order */
+    int64_t n_cloud = 0;
+    int64_t planned_edge = n_edge;
+    for (int64_t p = n_edge; p < n; p++) {
+        int32_t i = order[p];
+        if (!cloud || !net || n_cloud >= cloud_avail) continue;
+        int has_edge = edge != NULL;
+        int64_t edge_est = 0;
+        if (has_edge) {  /* _edge_estimate (scheduler.py:167-174) */
+            int64_t own = planned_edge > 1 ? planned_edge : 1;
+            if (own > edge->max_batch) own = edge->max_batch;
+            edge_est = orc_drain(edge, edge_in_flight + planned_edge) + orc_batch_latency(edge, own);
+        }
+        /* _cloud_estimate (scheduler.py:177-190) */
+        int64_t own_c = n_cloud + 1 < cloud->max_batch ? n_cloud + 1 : cloud->max_batch;
+        int64_t cloud_est = orc_drain(cloud, cloud_in_flight + n_cloud) +
+                            orc_transfer_time(net, payload[i], 1) + orc_batch_latency(cloud, own_c) +
+                            orc_transfer_time(net, 0, 0);
+        if (!has_edge || cloud_est < edge_est) {
+            tier[i] = 2;
+            cloud_order[n_cloud++] = i;
+        }
+    }
+    /* scheduler.py:223-234 */
+    for (int64_t i = 0; i < n; i++) {
+        int disp = tier[i] != 0;
+        refetch[i] = (uint8_t)(disp && (now - f->obs_captured_at[i] > stale_threshold));
+        skipped_out[i] = disp ? 0 : f->skipped[i] + 1;
+    }
+    *n_edge_out = n_edge;
+    return n_cloud;
+}

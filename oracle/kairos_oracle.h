@@ -97,6 +97,33 @@ int64_t orc_plan(const orc_fleet* f, int policy, int64_t buckets,
                  int64_t* est, int64_t* need_time, uint8_t* admitted,
                  uint8_t* refetch, int32_t* skipped_out);
 
+/* ---- phase 3: hybrid edge / cloud placement (scheduler.py:160-241) ---- */
+typedef struct {
+    int64_t capacity, max_batch;
+    int32_t npts;
+    const int64_t* batch;    /* profiled batch sizes, increasing */
+    const int64_t* latency;  /* µs, non-decreasing */
+} orc_profile;
+typedef struct {
+    int64_t base_latency_us, uplink_bps, downlink_bps;
+} orc_net;
+
+/* engines.py:132-155 */
+int64_t orc_batch_latency(const orc_profile* p, int64_t batch);
+/* engines.py:158-169 (up != 0: uplink) */
+int64_t orc_transfer_time(const orc_net* net, int64_t payload_bytes, int up);
+
+/* plan() with optional edge / cloud profiles and network model.  tier[i]:
+ * 0 deferred, 1 edge, 2 cloud; cloud_order receives the S_c indices in
+ * order; returns the number placed on the cloud (edge count via *n_edge). */
+int64_t orc_plan_tiers(const orc_fleet* f, const int64_t* payload, int policy, int64_t buckets,
+                       int64_t aging_interval, int64_t stale_threshold,
+                       int64_t default_exec_estimate, int64_t now, const orc_profile* edge,
+                       const orc_profile* cloud, const orc_net* net, int64_t edge_in_flight,
+                       int64_t cloud_in_flight, int32_t* order, uint8_t* tier,
+                       int32_t* cloud_order, uint8_t* refetch, int32_t* skipped_out,
+                       int64_t* n_edge);
+
 #ifdef __cplusplus
 }
 #endif

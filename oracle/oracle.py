@@ -33,6 +33,17 @@ _u8p = ctypes.POINTER(ctypes.c_uint8)
 _f64p = ctypes.POINTER(ctypes.c_double)
 
 
+class _Profile(ctypes.Structure):
+    _fields_ = [("capacity", ctypes.c_int64), ("max_batch", ctypes.c_int64),
+                ("npts", ctypes.c_int32), ("batch", ctypes.POINTER(ctypes.c_int64)),
+                ("latency", ctypes.POINTER(ctypes.c_int64))]
+
+
+class _Net(ctypes.Structure):
+    _fields_ = [("base_latency_us", ctypes.c_int64), ("uplink_bps", ctypes.c_int64),
+                ("downlink_bps", ctypes.c_int64)]
+
+
 class _Fleet(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_int64),
@@ -94,6 +105,15 @@ def lib():
         L.orc_assign_bucket.restype = ctypes.c_int32
         L.orc_assign_bucket.argtypes = [ctypes.c_double, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_int64]
+        L.orc_batch_latency.restype = ctypes.c_int64
+        L.orc_batch_latency.argtypes = [ctypes.POINTER(_Profile), ctypes.c_int64]
+        L.orc_transfer_time.restype = ctypes.c_int64
+        L.orc_transfer_time.argtypes = [ctypes.POINTER(_Net), ctypes.c_int64, ctypes.c_int]
+        L.orc_plan_tiers.restype = ctypes.c_int64
+        L.orc_plan_tiers.argtypes = [ctypes.POINTER(_Fleet), _i64p, ctypes.c_int] + \
+            [ctypes.c_int64] * 5 + [ctypes.POINTER(_Profile), ctypes.POINTER(_Profile),
+                                    ctypes.POINTER(_Net), ctypes.c_int64, ctypes.c_int64,
+                                    _i32p, _u8p, _i32p, _u8p, _i32p, _i64p]
         L.orc_plan.restype = ctypes.c_int64
         L.orc_plan.argtypes = [ctypes.POINTER(_Fleet), ctypes.c_int] + [ctypes.c_int64] * 8 + [
             _i32p, _i64p, _f64p, _i32p, _i64p, _i64p, _u8p, _u8p, _i32p]
@@ -272,3 +292,56 @@ def plan_soa(fleet: dict, policy: str, buckets: int, aging_interval: int,
 
 def nthreads_default() -> int:
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+# --- phase 3 (hybrid placement) ----------------------------------------------
+
+def _profile(d):
+    """Profile mapping (tier, capacity, max_batch, points) -> (struct, keepalive)."""
+    if d is None:
+        return None, None
+    pts = np.asarray(d["points"], np.int64).reshape(-1, 2)
+    b, lat = np.ascontiguousarray(pts[:, 0]), np.ascontiguousarray(pts[:, 1])
+    st = _Profile(int(d["capacity"]), int(d["max_batch"]), len(pts), _p(b, _i64p), _p(lat, _i64p))
+    return st, (b, lat)
+
+
+def batch_latency(profile: dict, batch: int) -> int:
+    st, keep = _profile(profile)
+    return int(lib().orc_batch_latency(ctypes.byref(st), batch))
+
+
+def transfer_time(net: dict, payload: int, up: bool) -> int:
+    n = _Net(int(net["base_latency_us"]), int(net["uplink_bps"]), int(net["downlink_bps"]))
+    return int(lib().orc_transfer_time(ctypes.byref(n), payload, int(up)))
+
+
+def plan_tiers(fleet: dict, payload, policy: str, buckets: int, aging_interval: int,
+               stale_threshold: int, default_exec_estimate: int, now: int, edge, cloud, net,
+               edge_in_flight: int, cloud_in_flight: int) -> dict:
+    """scheduler.py:254-276 plan() with edge / cloud profiles and network (dicts)."""
+    n = int(fleet["n"])
+    arrs = {k: np.ascontiguousarray(fleet[k], v) for k, v in FLEET_FIELDS.items()}
+    f = _Fleet(n, *[_p(arrs[k], _i64p if arrs[k].dtype == np.int64 else _i32p)
+                    for k in ["t_start", "issued_at", "obs_captured_at", "accum_gen", "remaining",
+                              "lexrank", "skipped", "hist_off", "n_exec", "n_gen", "slots"]])
+    pay = np.ascontiguousarray(payload, np.int64)
+    e, ek = _profile(edge)
+    c, ck = _profile(cloud)
+    nt = None if net is None else _Net(int(net["base_latency_us"]), int(net["uplink_bps"]),
+                                       int(net["downlink_bps"]))
+    res = {"order": np.empty(n, np.int32), "tier": np.empty(n, np.uint8),
+           "cloud_order": np.empty(max(n, 1), np.int32), "refetch": np.empty(n, np.uint8),
+           "skipped_out": np.empty(n, np.int32)}
+    n_edge = ctypes.c_int64(0)
+    nc = lib().orc_plan_tiers(
+        ctypes.byref(f), _p(pay, _i64p), POLICY_CODES[policy], buckets, aging_interval,
+        stale_threshold, default_exec_estimate, now,
+        ctypes.byref(e) if e is not None else None, ctypes.byref(c) if c is not None else None,
+        ctypes.byref(nt) if nt is not None else None, edge_in_flight, cloud_in_flight,
+        _p(res["order"], _i32p), _p(res["tier"], _u8p), _p(res["cloud_order"], _i32p),
+        _p(res["refetch"], _u8p), _p(res["skipped_out"], _i32p), ctypes.byref(n_edge))
+    res["n_cloud"] = int(nc)
+    res["n_edge"] = int(n_edge.value)
+    res["cloud_order"] = res["cloud_order"][:nc]
+    return res

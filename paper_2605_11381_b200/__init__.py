@@ -18,7 +18,8 @@ from .core import (ActionChunk, Duration, Interval, LastExecInfo, PendingRequest
                    RoundTimeline, TaskState, TimePoint, exec_duration, exec_end_from_piggyback,
                    us_from_actions, us_from_actions_batch)
 from .divergence import round_optimal_horizon, round_optimal_horizon_batch  # noqa: F401
-from .engines import EngineProfile, ProfileError  # noqa: F401
+from .engines import (EngineProfile, NetworkModel, ProfileError, batch_latency,  # noqa: F401
+                      cloud_round_trip, transfer_time)
 from .horizon import (HorizonPolicyConfig, UpdateMagnitudes, decide_horizon,  # noqa: F401
                       decide_horizon_batch, sweep_thresholds)
 from .scheduler import (DispatchPlan, SchedulerConfig, assign_bucket,  # noqa: F401

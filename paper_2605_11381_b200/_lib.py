@@ -73,6 +73,9 @@ _SIGNATURES = {
                                 ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp, _vp,
                                 ctypes.c_size_t, _vp]),
     "kr_sort_keys": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "kr_transfer_time": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    "kr_place_cloud": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, ctypes.POINTER(KrFleet),
+                                      ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -785,6 +785,62 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
     return KR_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Phase 3: hybrid edge / cloud placement (scheduler.py:160-241)
+// ---------------------------------------------------------------------------
+// engines.py:158-169 transfer_time: base + round_half_up(bytes * 8e6 / bps).
+__global__ void k_transfer_time(const int64_t* payload, int64_t n, int64_t base_us, int64_t bps,
+                                int64_t* out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const unsigned __int128 num = static_cast<unsigned __int128>(payload[i] < 0 ? 0 : payload[i]) * 8000000u;
+        const unsigned __int128 den = static_cast<unsigned __int128>(bps);
+        out[i] = base_us + static_cast<int64_t>((2 * num + den) / (2 * den));
+    }
+}
+
+// The reference walks the requests after the edge prefix in order and offloads
+// one to the cloud iff  cloud_est(req, c) < edge_est  while c = |S_c| < cap.
+// cloud_est = C(c) + up(payload), with C(c) (queue drain + batch latency +
+// downlink) non-decreasing in c, so the test is up_r < T(c) = edge_est - C(c),
+// T non-increasing (host-computed per round).  The greedy scan is therefore
+// "the first request after the last acceptance with up_r < T(c)", searched
+// 1024 requests at a time by one CTA; when no request qualifies at c none can
+// at c + 1 either.  Accepted requests get their skip counter reset and their
+// stale-observation refetch flag (scheduler.py:223-234).
+__global__ void __launch_bounds__(1024) k_place_cloud(const int32_t* order, int n, int n_edge,
+                                                      const int64_t* up, const int64_t* thr,
+                                                      int cap, const int64_t* obs, int32_t* skipped,
+                                                      uint8_t* refetch, int64_t now, int64_t stale,
+                                                      int32_t* cloud_idx, int32_t* n_cloud) {
+    __shared__ int best;
+    int pos = n_edge, c = 0;
+    while (c < cap && pos < n) {
+        const int64_t t = thr[c];
+        int found = INT_MAX;
+        for (int base = pos; base < n; base += blockDim.x) {
+            if (threadIdx.x == 0) best = INT_MAX;
+            __syncthreads();
+            const int r = base + threadIdx.x;
+            if (r < n && up[order[r]] < t) atomicMin(&best, r);
+            __syncthreads();
+            found = best;
+            __syncthreads();
+            if (found != INT_MAX) break;
+        }
+        if (found == INT_MAX) break;  // T only decreases: nothing qualifies later
+        if (threadIdx.x == 0) {
+            const int i = order[found];
+            cloud_idx[c] = i;
+            if (skipped) skipped[i] = 0;
+            if (refetch) refetch[i] = now - obs[i] > stale;
+        }
+        c++;
+        pos = found + 1;
+    }
+    if (threadIdx.x == 0) *n_cloud = c;
+}
+
 static unsigned grid_stream(int64_t n) {
     int64_t b = (n + 255) / 256;
     int64_t cap = static_cast<int64_t>(device_info().sm_count) * 8;
@@ -954,4 +1010,35 @@ extern "C" int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_ke
     int e = check_launch("kr_sort_keys", 2);
     if (e) return e;
     return sort_pairs(w, keys, nullptr, nullptr, n, order, sorted_keys, w.state->st[0], st);
+}
+
+extern "C" int kr_transfer_time(const int64_t* payload, int64_t n, int64_t base_us, int64_t bps,
+                                int64_t* out, void* stream) {
+    if (n < 0 || bps <= 0) return KR_EINVAL;
+    if (n == 0) return KR_OK;
+    if (!payload || !out) return KR_EINVAL;
+    k_transfer_time<<<grid_stream(n), 256, 0, as_stream(stream)>>>(payload, n, base_us, bps, out);
+    return check_launch("kr_transfer_time");
+}
+
+extern "C" int kr_place_cloud(const int32_t* order, int64_t n, int64_t n_edge,
+                              const int64_t* up_us, const int64_t* thresholds, int64_t cap,
+                              const kr_fleet* fleet, const kr_sched* cfg, uint8_t* refetch,
+                              int32_t* cloud_idx, int32_t* n_cloud, void* stream) {
+    if (n < 0 || n_edge < 0 || cap < 0 || n > INT32_MAX) return KR_EINVAL;
+    if (!n_cloud) return KR_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    if (n == 0 || cap == 0 || n_edge >= n) {
+        KR_CUDA_TRY(cudaMemsetAsync(n_cloud, 0, sizeof(int32_t), st));
+        return KR_OK;
+    }
+    if (!order || !up_us || !thresholds || !cloud_idx) return KR_EINVAL;
+    if (refetch && (!fleet || !cfg)) return KR_EINVAL;
+    k_place_cloud<<<1, 1024, 0, st>>>(order, static_cast<int>(n), static_cast<int>(n_edge), up_us,
+                                      thresholds, static_cast<int>(cap),
+                                      fleet ? fleet->obs_captured_at : nullptr,
+                                      fleet ? fleet->skipped : nullptr, refetch,
+                                      cfg ? cfg->now : 0, cfg ? cfg->stale_threshold : 0,
+                                      cloud_idx, n_cloud);
+    return check_launch("kr_place_cloud");
 }

@@ -12,14 +12,18 @@ pending set into the fleet layout, and three CUDA kernels make every decision:
   kr_admit      edge prefix of k = capacity - in_flight, stale-observation
                 refetch mask and the skip-counter side effect
 
+  kr_place_cloud the phase-3 cloud offload scan over the rest of the order
+                (scheduler.py:160-221): per-round thresholds T(c) are host
+                scalars from the engine profiles; per-request uplink times
+                (kr_transfer_time) and the ordered scan run on the device
+
 The host only builds the result objects and mirrors the skip counters into
-`states` as the reference does (scheduler.py:229-234).  The phase-3 cloud tier
-(scheduler.py:160-190, 210-221) is outside this build's decision core: a call
-that would consult it raises NotImplementedError rather than approximating.
+`states` as the reference does (scheduler.py:229-234).
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, replace
 from typing import Iterable, Mapping, Optional, Sequence
 
@@ -28,6 +32,7 @@ import torch
 
 from . import _lib
 from . import device as dev
+from . import engines as eng
 from . import fleet as fl
 from .core import Duration, PendingRequest, TaskState, TimePoint
 from .waiting import _state_fleet
@@ -160,10 +165,6 @@ def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edg
     reqs = _checked_pending(pending, states)
     edge_avail = max(0, edge.capacity - edge_in_flight) if edge is not None else 0
     cloud_avail = max(0, cloud.capacity - cloud_in_flight) if cloud is not None else 0
-    if cloud is not None and net is not None and cloud_avail > 0 and len(reqs) > edge_avail:
-        raise NotImplementedError(
-            "cloud-tier placement (scheduler.py:160-190, 210-221) is not part of the B200 "
-            "decision core; plan with cloud=None or net=None")
     n = len(reqs)
     if n == 0:
         return DispatchPlan(edge=(), cloud=(), deferred=(), refetch_task_ids=frozenset())
@@ -183,6 +184,24 @@ def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edg
     kth_ptr = sorted_keys.data_ptr() + (k - 1) * 16 if 0 < k < n else None
     refetch = torch.empty(n, dtype=torch.uint8, device=u.keys.device)
     fl.admit(u.keys, k, kth_ptr, fleet, sched, None, refetch=refetch)
+    n_cloud = 0
+    cloud_idx = None
+    if cloud is not None and net is not None and cloud_avail > 0 and k < n:
+        # phase 3 (scheduler.py:210-221): per-round thresholds on the host,
+        # per-request uplink times and the ordered offload scan on the device
+        cap = min(cloud_avail, n - k)
+        thr = eng.cloud_thresholds(edge, cloud, net, edge_in_flight, cloud_in_flight, k, cap)
+        payload = dev.tensor(np.array([r.payload_bytes for r in reqs], np.int64), torch.int64)
+        up = eng.transfer_time_batch(net, payload, eng.UP)
+        thr_t = dev.tensor(np.array(thr, np.int64), torch.int64)
+        cloud_idx = torch.empty(cap, dtype=torch.int32, device=u.keys.device)
+        n_cloud_t = torch.zeros(1, dtype=torch.int32, device=u.keys.device)
+        fs = fleet.c_struct()
+        _lib.check(_lib.load().kr_place_cloud(
+            order.data_ptr(), n, k, up.data_ptr(), thr_t.data_ptr(), cap, ctypes.byref(fs),
+            ctypes.byref(sched), refetch.data_ptr(), cloud_idx.data_ptr(), n_cloud_t.data_ptr(),
+            dev.stream()), "kr_place_cloud")
+        n_cloud = int(n_cloud_t.item())
     f = dev.read_flags(flags)
     if f & (_lib.FLAG_KEY_RANGE | _lib.FLAG_RATIO):
         raise ValueError("a pending request falls outside the packed sort-key range "
@@ -190,16 +209,19 @@ def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edg
     order_h = order.cpu().numpy()
     refetch_h = refetch.cpu().numpy()
     skipped_h = fleet.t["skipped"].cpu().numpy()
+    cloud_h = cloud_idx[:n_cloud].cpu().numpy() if n_cloud else np.zeros(0, np.int32)
+    in_cloud = set(int(i) for i in cloud_h)
     s_edge = [reqs[i] for i in order_h[:k]]
+    s_cloud = [reqs[i] for i in cloud_h]
     deferred = []
-    for i in order_h[:k]:
+    for i in order_h:
         states[reqs[i].task_id].skipped = int(skipped_h[i])
     for i in order_h[k:]:
-        r = reqs[i]
-        states[r.task_id].skipped = int(skipped_h[i])
-        deferred.append(replace(r, skipped=int(skipped_h[i])))
+        if int(i) in in_cloud:
+            continue
+        deferred.append(replace(reqs[i], skipped=int(skipped_h[i])))
     refetch_ids = frozenset(reqs[i].task_id for i in np.nonzero(refetch_h)[0])
-    return DispatchPlan(edge=tuple(s_edge), cloud=(), deferred=tuple(deferred),
+    return DispatchPlan(edge=tuple(s_edge), cloud=tuple(s_cloud), deferred=tuple(deferred),
                         refetch_task_ids=refetch_ids)
 
 

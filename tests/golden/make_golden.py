@@ -32,7 +32,7 @@ sys.path.insert(0, REF_SRC)
 
 from roboserve import core, horizon, scheduler, waiting, workload  # noqa: E402
 from roboserve.core import Interval, LastExecInfo, PendingRequest, TaskState  # noqa: E402
-from roboserve.engines import EngineProfile  # noqa: E402
+from roboserve.engines import EngineProfile, NetworkModel  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 
@@ -256,6 +256,72 @@ def gen_plan(rng):
     return instances
 
 
+def random_profile(rng, tier):
+    """A valid saturating profile: lat(b) = base + slope * b (throughput rises to max_batch)."""
+    nb = int(rng.integers(1, 6))
+    batches = sorted(set(int(b) for b in rng.choice([1, 2, 3, 4, 6, 8, 12, 16, 32], nb, replace=False)))
+    base = int(rng.integers(20_000, 400_000))
+    slope = int(rng.integers(1_000, 60_000))
+    pts = tuple((b, base + slope * b) for b in batches)
+    return EngineProfile(tier=tier, capacity=int(rng.integers(1, 40)), max_batch=batches[-1],
+                         points=pts)
+
+
+def gen_plan_cloud(rng):
+    """plan() with a cloud tier and network model (scheduler.py:160-221)."""
+    instances = []
+    for ii in range(80):
+        now = 100_000_000
+        P = int(rng.choice([1, 3, 8, 30, 90, 200]))
+        ids = [f"task-{i:04d}" for i in rng.choice(20000, P, replace=False)]
+        states, pending = {}, []
+        for tid in ids:
+            st = random_state(rng, tid, now)
+            skipped = int(rng.integers(0, 13))
+            st.skipped = skipped
+            states[tid] = st
+            issued = now - int(rng.integers(0, 1_000_000))
+            pending.append(PendingRequest(
+                task_id=tid, round_id=len(st.exec_intervals), issued_at=issued,
+                obs_captured_at=issued - int(rng.integers(0, 300_000)),
+                last_exec_info=LastExecInfo(issued - 1000, int(rng.integers(0, 40))),
+                payload_bytes=int(rng.choice([0, 1_000, 50_000, 300_000, int(rng.integers(0, 2_000_000))])),
+                skipped=skipped))
+        policy = ["kairos", "fifo", "las"][ii % 3]
+        cfg = scheduler.SchedulerConfig(policy=policy, buckets=10, aging_interval=5,
+                                        stale_threshold=int(rng.choice([0, 150_000, 10**9])))
+        edge = None if ii % 9 == 0 else random_profile(rng, "edge")
+        cloud = random_profile(rng, "cloud")
+        net = NetworkModel(base_latency_us=int(rng.integers(1_000, 120_000)),
+                           uplink_bps=int(rng.choice([10**6, 10**7, 10**8, int(rng.integers(10**5, 10**9))])),
+                           downlink_bps=int(rng.choice([10**7, 10**8, int(rng.integers(10**5, 10**9))])))
+        eif = int(rng.integers(0, 12))
+        cif = int(rng.integers(0, 12))
+        before = {t: state_json(s) for t, s in states.items()}
+        order_in = list(pending)
+        rng.shuffle(order_in)
+        plan = scheduler.plan(order_in, states, edge, cloud, net, now, cfg,
+                              edge_in_flight=eif, cloud_in_flight=cif)
+        prof = lambda e: None if e is None else {"tier": e.tier, "capacity": e.capacity,
+                                                  "max_batch": e.max_batch, "points": list(e.points)}
+        instances.append({
+            "now": now, "policy": policy, "buckets": 10, "aging_interval": 5,
+            "stale_threshold": cfg.stale_threshold,
+            "default_exec_estimate": cfg.default_exec_estimate,
+            "edge": prof(edge), "cloud": prof(cloud),
+            "net": {"base_latency_us": net.base_latency_us, "uplink_bps": net.uplink_bps,
+                    "downlink_bps": net.downlink_bps},
+            "edge_in_flight": eif, "cloud_in_flight": cif, "control_hz": 30,
+            "states": list(before.values()), "pending": [req_json(r) for r in order_in],
+            "expected": {
+                "edge": [r.task_id for r in plan.edge],
+                "cloud": [r.task_id for r in plan.cloud],
+                "deferred": [[r.task_id, r.skipped] for r in plan.deferred],
+                "refetch": sorted(plan.refetch_task_ids),
+                "skipped_after": {t: s.skipped for t, s in states.items()}}})
+    return instances
+
+
 def gen_fig4():
     buf = io.StringIO()
     with contextlib.redirect_stdout(buf):
@@ -279,6 +345,8 @@ def main():
     save_divergence(gen_divergence(rng))
     (OUT / "time.json").write_text(json.dumps(gen_time(rng)))
     (OUT / "plan.json").write_text(json.dumps(gen_plan(rng), separators=(",", ":")))
+    (OUT / "plan_cloud.json").write_text(json.dumps(gen_plan_cloud(np.random.default_rng(7)),
+                                                    separators=(",", ":")))
     (OUT / "fig4.json").write_text(json.dumps(gen_fig4(), indent=1))
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".npz", ".json"):

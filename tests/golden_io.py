@@ -80,3 +80,7 @@ def ns_objects(inst):
                                     remaining_actions=r["last_exec_info"][1]))
                for r in inst["pending"]]
     return states, pending
+
+
+def plan_cloud_instances():
+    return json.loads((GOLDEN / "plan_cloud.json").read_text())

@@ -163,3 +163,35 @@ def test_fig4_scenario(kb):
             rounds_done[pick] += 1
             t = t + gen
         assert order == c["kairos"], c["durs"]
+
+
+def test_plan_cloud_golden(kb):
+    """Phase 3: plan() with a cloud tier and network model vs the reference."""
+    for ii, inst in enumerate(golden_io.plan_cloud_instances()):
+        states, pending = golden_io.build_objects(inst, kb)
+        mk = lambda d: None if d is None else kb.EngineProfile(
+            tier=d["tier"], capacity=d["capacity"], max_batch=d["max_batch"],
+            points=tuple(tuple(p) for p in d["points"]))
+        net = kb.NetworkModel(**inst["net"])
+        cfg = kb.SchedulerConfig(policy=inst["policy"], buckets=inst["buckets"],
+                                 aging_interval=inst["aging_interval"],
+                                 stale_threshold=inst["stale_threshold"],
+                                 default_exec_estimate=inst["default_exec_estimate"])
+        p = kb.plan(pending, states, mk(inst["edge"]), mk(inst["cloud"]), net, inst["now"], cfg,
+                    edge_in_flight=inst["edge_in_flight"], cloud_in_flight=inst["cloud_in_flight"])
+        exp = inst["expected"]
+        assert [r.task_id for r in p.edge] == exp["edge"], ii
+        assert [r.task_id for r in p.cloud] == exp["cloud"], ii
+        assert [[r.task_id, r.skipped] for r in p.deferred] == exp["deferred"], ii
+        assert sorted(p.refetch_task_ids) == exp["refetch"], ii
+        assert {t: s.skipped for t, s in states.items()} == exp["skipped_after"], ii
+
+
+def test_engine_reference_goldens(kb):
+    prof = kb.EngineProfile(tier="edge", capacity=4, max_batch=4, points=((1, 150_000), (4, 200_000)))
+    assert kb.batch_latency(prof, 2) == 166_667
+    wan = kb.NetworkModel(base_latency_us=100_000, uplink_bps=10**9, downlink_bps=10**9)
+    assert kb.transfer_time(wan, 1_250_000, "up") == 110_000
+    assert kb.cloud_round_trip(wan, 300_000, 0, 150_000) == 352_400
+    with pytest.raises(kb.ProfileError):
+        kb.EngineProfile(tier="edge", capacity=1, max_batch=2, points=((1, 10), (2, 100)))

@@ -127,3 +127,35 @@ def test_plan_golden():
             assert res["bucket"][i] == it["bucket"]
             assert res["est"][i] == it["est"]
             assert res["need_time"][i] == it["need_time"]
+
+
+def test_plan_cloud_golden():
+    """Phase 3 (hybrid edge / cloud placement) restatement vs the reference."""
+    for ii, inst in enumerate(golden_io.plan_cloud_instances()):
+        states, pending = golden_io.ns_objects(inst)
+        fleet = orc.fleet_from_objects(pending, states)
+        payload = [r["payload_bytes"] for r in inst["pending"]]
+        res = orc.plan_tiers(fleet, payload, inst["policy"], inst["buckets"], inst["aging_interval"],
+                             inst["stale_threshold"], inst["default_exec_estimate"], inst["now"],
+                             inst["edge"], inst["cloud"], inst["net"], inst["edge_in_flight"],
+                             inst["cloud_in_flight"])
+        ids = [r.task_id for r in pending]
+        exp = inst["expected"]
+        order = [ids[i] for i in res["order"]]
+        assert order[:res["n_edge"]] == exp["edge"], ii
+        assert [ids[i] for i in res["cloud_order"]] == exp["cloud"], ii
+        deferred = [[ids[i], int(res["skipped_out"][i])] for i in res["order"] if res["tier"][i] == 0]
+        assert deferred == exp["deferred"], ii
+        assert sorted(ids[i] for i in np.nonzero(res["refetch"])[0]) == exp["refetch"], ii
+        assert {t: int(res["skipped_out"][i]) for i, t in enumerate(ids)} == exp["skipped_after"], ii
+
+
+def test_engine_model_goldens():
+    # reference tests/test_engines.py: interpolation 166,667; transfer 110,000; round trip 352,400
+    prof = {"capacity": 4, "max_batch": 4, "points": [[1, 150_000], [4, 200_000]]}
+    assert orc.batch_latency(prof, 2) == 166_667          # test_engines.py:37-39
+    assert orc.batch_latency(prof, 4) == 200_000          # test_engines.py:34
+    wan = {"base_latency_us": 100_000, "uplink_bps": 10**9, "downlink_bps": 10**9}
+    assert orc.transfer_time(wan, 1_250_000, True) == 110_000   # test_engines.py:93
+    # cloud_round_trip(WAN, 300_000, 0, 150_000) == 352_400 (test_engines.py:120)
+    assert orc.transfer_time(wan, 300_000, True) + 150_000 + orc.transfer_time(wan, 0, False) == 352_400

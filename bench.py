@@ -275,7 +275,7 @@ def run_ours(args, world, rank, local_rank):
         torch.cuda.synchronize()
         breakdown["urgency_plus_admission_graph_ms"] = gd[0].elapsed_time(gd[1])
 
-    e2e = run_e2e(args, world, soa, prev, cand, off, sched) if not args.no_e2e else None
+    e2e, e2e_cold = run_e2e(args, world, soa, prev, cand, off, sched) if not args.no_e2e else (None, None)
 
     if rank != 0:
         return
@@ -302,26 +302,49 @@ def run_ours(args, world, rank, local_rank):
     }
     if e2e:
         line["e2e"] = e2e
+        line["e2e_cold"] = e2e_cold
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     print(json.dumps(line), flush=True)
 
 
-def run_e2e(args, world, soa, prev, cand, off, sched):
-    """Same round through the C ABI from pinned host buffers (copies timed)."""
+def _timed(step, steps, world):
     import torch
     import torch.distributed as dist
+    for _ in range(2):
+        step(0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(steps):
+        step(i)
+    e.record()
+    torch.cuda.synchronize()
+    el = torch.tensor([s.elapsed_time(e) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    return float(el.item())
+
+
+def run_e2e(args, world, soa, prev, cand, off, sched):
+    """The round through the C ABI from pinned host buffers, copies timed.
+
+    Streaming (the headline `e2e`): in a serving loop a round's host inputs are
+    the new action chunk and the per-request scalars that change every round
+    (issued_at, obs_captured_at, remaining actions, overlap offset); the
+    previous chunk is the last round's new chunk and the fleet history are
+    already device-resident.  Each step copies one new chunk (alternating two
+    host chunk sets, so the compared trajectories differ) and those scalars,
+    runs the round, and reads back horizons, need times, admitted / refetch
+    masks, skip counters and the ordered S_e.
+    Cold (`e2e_cold`): every input of the round, history included, is copied."""
+    import torch
     from paper_2605_11381_b200 import fleet as fl, rounds
 
     R = args.robots
-    h_prev = prev.cpu().pin_memory()
-    h_cand = cand.cpu().pin_memory()
-    h_off = off.cpu().pin_memory()
-    h_soa = {k: torch.from_numpy(np.ascontiguousarray(soa[k])).pin_memory()
-             for k in fl.INT_FIELDS64 + fl.INT_FIELDS32 + ("slots",)}
-    d_prev, d_cand, d_off = torch.empty_like(prev), torch.empty_like(cand), torch.empty_like(off)
-    d_soa = {k: torch.empty(v.shape, dtype=v.dtype, device="cuda") for k, v in h_soa.items()}
-    fleet = fl.DeviceFleet.from_tensors(d_soa)
+    graphs = world == 1 and not args.no_graph
     rnd = (rounds.ShardedDecisionRound(R, args.k, sched) if world > 1
            else rounds.DecisionRound(R, args.k, sched))
     outs = {"H": torch.empty(R, dtype=torch.int32).pin_memory(),
@@ -330,23 +353,9 @@ def run_e2e(args, world, soa, prev, cand, off, sched):
             "ref": torch.empty(R, dtype=torch.uint8).pin_memory(),
             "skip": torch.empty(R, dtype=torch.int32).pin_memory(),
             "edge": torch.empty((max(rnd.k, 1), 2), dtype=torch.int64).pin_memory()}
-    h2d = sum(t.numel() * t.element_size() for t in [h_prev, h_cand, h_off, *h_soa.values()])
     d2h = sum(t.numel() * t.element_size() for t in outs.values())
 
-    inputs = rounds.DivergenceInputs(d_prev, d_cand, THR, offset=d_off)
-    graphs = world == 1 and not args.no_graph
-    if graphs:
-        for k, v in h_soa.items():
-            d_soa[k].copy_(v)
-        rnd.capture(fleet, inputs)
-
-    def step():
-        d_prev.copy_(h_prev, non_blocking=True)
-        d_cand.copy_(h_cand, non_blocking=True)
-        d_off.copy_(h_off, non_blocking=True)
-        for k, v in h_soa.items():
-            d_soa[k].copy_(v, non_blocking=True)
-        o = rnd.replay() if graphs else rnd.run(fleet, inputs)
+    def read_back(o, fleet):
         outs["H"].copy_(o.horizon, non_blocking=True)
         outs["need"].copy_(o.need_time, non_blocking=True)
         outs["adm"].copy_(o.admitted, non_blocking=True)
@@ -354,26 +363,78 @@ def run_e2e(args, world, soa, prev, cand, off, sched):
         outs["skip"].copy_(fleet.t["skipped"], non_blocking=True)
         outs["edge"][: o.edge_keys.shape[0]].copy_(o.edge_keys, non_blocking=True)
 
-    steps = max(1, min(args.steps, args.e2e_steps))
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(steps):
-        step()
-    e.record()
-    torch.cuda.synchronize()
-    el = torch.tensor([s.elapsed_time(e) / 1e3], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    t = float(el.item())
-    return {"value": R * world * steps / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    # ---- streaming rounds ----
+    h_chunks = [cand[:, 0].cpu().pin_memory(), prev.cpu().pin_memory()]  # alternate A, B
+    d_chunks = [torch.empty_like(prev), torch.empty_like(prev)]
+    d_chunks[1].copy_(h_chunks[1])
+    fleet = fl.DeviceFleet.from_host(soa)
+    per_round = ("issued_at", "obs_captured_at", "remaining")
+    h_sc = {k: torch.from_numpy(np.ascontiguousarray(soa[k])).pin_memory() for k in per_round}
+    h_off = off.cpu().pin_memory()
+    d_off = torch.empty_like(off)
+    inp = [rounds.DivergenceInputs(d_chunks[1], d_chunks[0], THR, offset=d_off),
+           rounds.DivergenceInputs(d_chunks[0], d_chunks[1], THR, offset=d_off)]
+    if graphs:
+        rnd.run(fleet, inp[0])
+        torch.cuda.synchronize()
+        g_h = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+        for j in range(2):
+            with torch.cuda.graph(g_h[j]):
+                rnd.horizons(inp[j])
+        g_d = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_d):
+            rnd.urgency(fleet)
+            rnd.admit(fleet)
+
+    def stream_step(i):
+        j = i & 1
+        d_chunks[j].copy_(h_chunks[j], non_blocking=True)
+        d_off.copy_(h_off, non_blocking=True)
+        for k, v in h_sc.items():
+            fleet.t[k].copy_(v, non_blocking=True)
+        if graphs:
+            g_h[j].replay()
+            g_d.replay()
+            o = rnd.outputs()
+        else:
+            o = rnd.run(fleet, inp[j])
+        read_back(o, fleet)
+
+    h2d_stream = h_chunks[0].numel() * 4 + h_off.numel() * 4 + sum(
+        v.numel() * v.element_size() for v in h_sc.values())
+    steps = max(2, min(args.steps, args.e2e_steps))
+    t = _timed(stream_step, steps, world)
+    stream = {"value": R * world * steps / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d_stream),
+              "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": 1e3 * t / steps,
+              "path": "streaming round through the C ABI: pinned host -> H2D of the new chunk "
+                      "[R,50,7] fp32 + per-request scalars (issued_at, obs_captured_at, remaining, "
+                      "offset); previous chunk (last round's) and fleet history device-resident; "
+                      "D2H of horizons, need times, masks, skip counters, ordered S_e"}
+
+    # ---- cold rounds: every input copied ----
+    h_prev, h_cand = prev.cpu().pin_memory(), cand.cpu().pin_memory()
+    h_soa = {k: torch.from_numpy(np.ascontiguousarray(soa[k])).pin_memory()
+             for k in fl.INT_FIELDS64 + fl.INT_FIELDS32 + ("slots",)}
+    d_prev, d_cand = torch.empty_like(prev), torch.empty_like(cand)
+    d_soa = {k: torch.empty(v.shape, dtype=v.dtype, device="cuda") for k, v in h_soa.items()}
+    cfleet = fl.DeviceFleet.from_tensors(d_soa)
+    cinp = rounds.DivergenceInputs(d_prev, d_cand, THR, offset=d_off)
+
+    def cold_step(i):
+        d_prev.copy_(h_prev, non_blocking=True)
+        d_cand.copy_(h_cand, non_blocking=True)
+        d_off.copy_(h_off, non_blocking=True)
+        for k, v in h_soa.items():
+            d_soa[k].copy_(v, non_blocking=True)
+        read_back(rnd.run(cfleet, cinp), cfleet)
+
+    h2d_cold = sum(t_.numel() * t_.element_size() for t_ in [h_prev, h_cand, h_off, *h_soa.values()])
+    t = _timed(cold_step, steps, world)
+    cold = {"value": R * world * steps / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d_cold),
             "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": 1e3 * t / steps,
-            "path": "pinned host buffers -> H2D -> decision round (C ABI) -> D2H of horizons, "
-                    "need times, masks, skip counters, ordered S_e"}
+            "path": "every input of the round (both chunks, all fleet state and history) copied "
+                    "from pinned host each step; eager launches"}
+    return stream, cold
 
 
 def main():

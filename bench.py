@@ -221,7 +221,9 @@ def run_ours(args, world, rank, local_rank):
     graphs = world == 1 and not args.no_graph
     n_cap0 = lib.kr_launch_count()
     if graphs:
-        rnd.capture(fleet, inputs)   # CUDA graphs: horizons | urgency + admission
+        # CUDA graphs: horizons | urgency + admission, the latter on a side
+        # stream over `reserve_sms` SMs left free by the horizon kernel
+        rnd.capture(fleet, inputs, reserve_sms=args.reserve_sms)
         per_round = (lib.kr_launch_count() - n_cap0) // 2  # warm-up run + capture
     for _ in range(args.warmup):
         if graphs:
@@ -239,15 +241,12 @@ def run_ours(args, world, rank, local_rank):
         barrier()
         start.record(stream)
         for i in range(args.steps):
-            ev[i][0].record(stream)
             if graphs:
-                rnd.g_horizon.replay()
+                rnd.replay_concurrent(before_horizon=ev[i][0].record, after_horizon=ev[i][1].record)
             else:
+                ev[i][0].record(stream)
                 rnd.horizons(inputs)
-            ev[i][1].record(stream)
-            if graphs:
-                rnd.g_decide.replay()
-            else:
+                ev[i][1].record(stream)
                 rnd.urgency(fleet)
                 rnd.admit(fleet)
         end.record(stream)
@@ -274,6 +273,7 @@ def run_ours(args, world, rank, local_rank):
         gd[0].record(stream); rnd.g_decide.replay(); gd[1].record(stream)
         torch.cuda.synchronize()
         breakdown["urgency_plus_admission_graph_ms"] = gd[0].elapsed_time(gd[1])
+        breakdown["reserve_sms"] = args.reserve_sms
 
     e2e, e2e_cold = run_e2e(args, world, soa, prev, cand, off, sched) if not args.no_e2e else (None, None)
 
@@ -298,6 +298,8 @@ def run_ours(args, world, rank, local_rank):
         "kernels": breakdown,
         "gpu_launches": int(launches),
         "cuda_graphs": bool(graphs),
+        "concurrency": (f"urgency + admission on a side stream over {args.reserve_sms} SMs reserved "
+                        "from the horizon kernel" if graphs and args.reserve_sms > 0 else None),
         "clocks": clk.summary(),
     }
     if e2e:
@@ -448,6 +450,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--reserve-sms", type=int, default=24,
+                    help="SMs left to urgency + admission (side stream) during the horizon kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-robots", type=int, default=16384)

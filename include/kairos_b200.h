@@ -125,7 +125,10 @@ KR_API int kr_horizon_divergence(const void* prev, const void* cand, int dtype, 
                           int32_t S, int32_t Lp, int32_t Lc, int32_t D,
                           const int32_t* offset, const int32_t* len_prev,
                           const int32_t* len_cand, double thr, int32_t* H, double* cos,
-                          void* stream);
+                          int32_t max_sms, void* stream);
+/* max_sms (0 = all): cap the persistent grid to this many SMs so that work on
+ * another stream (urgency + admission, which do not depend on H) can run on
+ * the remaining SMs concurrently. */
 
 /* ---- step 2: execution-aware urgency ---------------------------------- */
 

@@ -386,7 +386,7 @@ static int kernel_regs(K kern) {
 
 template <class Work, class KStaged, class KDirect>
 static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, const Work& w,
-                         cudaStream_t st, const char* name) {
+                         cudaStream_t st, const char* name, int max_sms = 0) {
     size_t smem = stream_smem_bytes(p);
     auto go = [&](auto kern) -> int {
         int per_sm = 0;
@@ -408,7 +408,9 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
         }
         if (per_sm < 1) per_sm = 1;
         int64_t ntiles = (p.R + p.TR - 1) / p.TR;
-        int64_t grid = static_cast<int64_t>(device_info().sm_count) * per_sm;
+        int sms = device_info().sm_count;
+        if (max_sms > 0 && max_sms < sms) sms = max_sms;
+        int64_t grid = static_cast<int64_t>(sms) * per_sm;
         if (grid > ntiles) grid = ntiles;
         if (grid < 1) grid = 1;
         kern<<<static_cast<unsigned>(grid), p.threads + 32, smem, st>>>(p, w);
@@ -467,7 +469,7 @@ extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_
 }
 
 template <typename T>
-static int launch_div(const StreamPlan& p, const DivWork<T, 0>& w0, cudaStream_t st) {
+static int launch_div(const StreamPlan& p, const DivWork<T, 0>& w0, cudaStream_t st, int max_sms) {
     auto with = [&](auto proto) {
         decltype(proto) w{w0.S, w0.Lp, w0.Lc, w0.D, w0.TR, w0.rounds, w0.has_off, w0.has_lp,
                           w0.has_lc, w0.thr, w0.H, w0.cos, w0.thr_f, w0.margin, nullptr, nullptr,
@@ -477,14 +479,14 @@ static int launch_div(const StreamPlan& p, const DivWork<T, 0>& w0, cudaStream_t
     switch (w0.D) {
         case 7:
             return launch_stream(k_horizon_divergence<T, 7, true>, k_horizon_divergence<T, 7, false>,
-                                 p, with(DivWork<T, 7>{}), st, "kr_horizon_divergence");
+                                 p, with(DivWork<T, 7>{}), st, "kr_horizon_divergence", max_sms);
         case 32:
             return launch_stream(k_horizon_divergence<T, 32, true>,
                                  k_horizon_divergence<T, 32, false>, p, with(DivWork<T, 32>{}), st,
-                                 "kr_horizon_divergence");
+                                 "kr_horizon_divergence", max_sms);
         default:
             return launch_stream(k_horizon_divergence<T, 0, true>, k_horizon_divergence<T, 0, false>,
-                                 p, w0, st, "kr_horizon_divergence");
+                                 p, w0, st, "kr_horizon_divergence", max_sms);
     }
 }
 
@@ -492,7 +494,7 @@ extern "C" int kr_horizon_divergence(const void* prev, const void* cand, int dty
                                      int32_t S, int32_t Lp, int32_t Lc, int32_t D,
                                      const int32_t* offset, const int32_t* len_prev,
                                      const int32_t* len_cand, double thr, int32_t* H, double* cos,
-                                     void* stream) {
+                                     int32_t max_sms, void* stream) {
     if (R < 0 || S < 1 || Lp < 0 || Lc < 0 || D < 0 || (dtype != KR_F32 && dtype != KR_F64))
         return KR_EINVAL;
     if (!(thr > 0.0 && thr <= 1.0)) return KR_EINVAL;  // workload.py:483-484
@@ -533,10 +535,10 @@ extern "C" int kr_horizon_divergence(const void* prev, const void* cand, int dty
         DivWork<double, 0> w{S, Lp, Lc, D, p.TR, p.rounds, offset != nullptr, len_prev != nullptr,
                              len_cand != nullptr, thr, H, cos, thr_f, margin, nullptr, nullptr,
                              {}, {}, {}};
-        return launch_div(p, w, st);
+        return launch_div(p, w, st, max_sms);
     }
     DivWork<float, 0> w{S, Lp, Lc, D, p.TR, p.rounds, offset != nullptr, len_prev != nullptr,
                         len_cand != nullptr, thr, H, cos, thr_f, margin, nullptr, nullptr,
                         {}, {}, {}};
-    return launch_div(p, w, st);
+    return launch_div(p, w, st, max_sms);
 }

@@ -67,7 +67,7 @@ def round_optimal_horizon_batch(prev: torch.Tensor, cand: torch.Tensor, sim_thre
     _lib.check(_lib.load().kr_horizon_divergence(
         prev.data_ptr(), cand.data_ptr(), dtype, R, S, Lp, Lc, D, _lib.ptr(offset),
         _lib.ptr(len_prev), _lib.ptr(len_cand), float(sim_threshold), out.data_ptr(),
-        _lib.ptr(cos), dev.stream()), "kr_horizon_divergence")
+        _lib.ptr(cos), 0, dev.stream()), "kr_horizon_divergence")
     return (out, cos) if return_cos else out
 
 

@@ -77,6 +77,7 @@ class DecisionRound:
         self.ws = fl.Workspace(R)
         self.key_stats = fl.new_key_stats(d)
         self.lib = _lib.load()
+        self.max_sms = 0  # divergence grid SM cap (0: all); see capture(concurrent=...)
 
     def horizons(self, h: DivergenceInputs) -> None:
         prev, cand = h.prev, h.cand
@@ -88,7 +89,7 @@ class DecisionRound:
         _lib.check(self.lib.kr_horizon_divergence(
             prev.data_ptr(), cand.data_ptr(), dtype, R, S, Lp, Lc, D, _lib.ptr(h.offset),
             _lib.ptr(h.len_prev), _lib.ptr(h.len_cand), float(h.threshold), self.H.data_ptr(),
-            None, dev.stream()), "kr_horizon_divergence")
+            None, self.max_sms, dev.stream()), "kr_horizon_divergence")
 
     def urgency(self, fleet: fl.DeviceFleet) -> None:
         st = dev.stream()
@@ -114,10 +115,15 @@ class DecisionRound:
         self.admit(fleet)
         return self.outputs()
 
-    def capture(self, fleet: fl.DeviceFleet, h: DivergenceInputs) -> None:
+    def capture(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 0) -> None:
         """Record the round as two CUDA graphs (horizons | urgency + admission)
-        over these fixed device buffers; `replay()` then launches the ~15
-        kernels of a round with two graph launches."""
+        over these fixed device buffers.  With `reserve_sms` > 0 the divergence
+        grid leaves that many SMs free and `replay()` runs the two graphs on two
+        streams: urgency and admission do not depend on this round's horizons
+        (the reference's order uses history, not H), so they overlap the
+        HBM-bound horizon kernel on the reserved SMs."""
+        self.max_sms = 0 if reserve_sms <= 0 else max(1, torch.cuda.get_device_properties(
+            self.H.device).multi_processor_count - reserve_sms)
         self.run(fleet, h)  # warm-up: attribute / occupancy caches, lazy loading
         torch.cuda.synchronize()
         self.g_horizon, self.g_decide = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -126,10 +132,38 @@ class DecisionRound:
         with torch.cuda.graph(self.g_decide):
             self.urgency(fleet)
             self.admit(fleet)
+        self.side = torch.cuda.Stream(device=self.H.device) if reserve_sms > 0 else None
+
+    def replay_concurrent(self, before_horizon=None, after_horizon=None) -> None:
+        """One round from the captured graphs.  With reserved SMs the horizon
+        graph is launched first on the current stream and the urgency +
+        admission graph on the side stream (ordered after all prior work of the
+        current stream, not after the horizons); the current stream joins the
+        side stream at the end.  `before_horizon` / `after_horizon` (callables)
+        may record events around the horizon graph."""
+        main = torch.cuda.current_stream()
+        if self.side is None:
+            if before_horizon:
+                before_horizon(main)
+            self.g_horizon.replay()
+            if after_horizon:
+                after_horizon(main)
+            self.g_decide.replay()
+            return
+        fork = torch.cuda.Event()
+        fork.record(main)
+        if before_horizon:
+            before_horizon(main)
+        self.g_horizon.replay()
+        if after_horizon:
+            after_horizon(main)
+        self.side.wait_event(fork)
+        with torch.cuda.stream(self.side):
+            self.g_decide.replay()
+        main.wait_stream(self.side)
 
     def replay(self) -> RoundOutputs:
-        self.g_horizon.replay()
-        self.g_decide.replay()
+        self.replay_concurrent()
         return self.outputs()
 
 

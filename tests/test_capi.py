@@ -48,7 +48,7 @@ def test_host_only_entry_points():
     # argument validation happens before any device work
     assert lib.kr_horizon_confidence(None, 0, 4, 1, 8, 1.4, 1, None, None, None) == _lib.KR_EINVAL
     assert lib.kr_horizon_divergence(None, None, 0, 4, 1, 8, 8, 7, None, None, None, 0.0, None,
-                                     None, None) == _lib.KR_EINVAL
+                                     None, 0, None) == _lib.KR_EINVAL
     assert lib.kr_horizon_static(0, 8, 3, None, None) == _lib.KR_OK
 
 

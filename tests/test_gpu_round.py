@@ -98,3 +98,26 @@ def test_multi_round_replay_vs_oracle(R, k, rounds_):
         assert np.array_equal(rnd.admitted.cpu().numpy(), res["admitted"]), r
         assert np.array_equal(fleet.t["skipped"].cpu().numpy(), res["skipped_out"]), r
         soa["skipped"] = res["skipped_out"]
+
+
+def test_concurrent_replay_matches_eager():
+    """Urgency + admission on a side stream over reserved SMs, concurrent with
+    the horizon kernel: identical outputs to the sequential eager round."""
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    R, k = 1 << 17, 2048
+    soa = synthetic.fleet_soa(R, seed=8)
+    prev, cand, off = synthetic.chunks(R, seed=9)
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    f1 = fl.DeviceFleet.from_host(soa)
+    r1 = rounds.DecisionRound(R, k, sched)
+    o1 = r1.run(f1, rounds.DivergenceInputs(prev, cand, 0.9, offset=off))
+    eager = [t.clone() for t in (o1.horizon, o1.need_time, o1.admitted, o1.refetch, o1.edge_idx)]
+    f2 = fl.DeviceFleet.from_host(soa)
+    r2 = rounds.DecisionRound(R, k, sched)
+    r2.capture(f2, rounds.DivergenceInputs(prev, cand, 0.9, offset=off), reserve_sms=16)
+    f2.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
+    o2 = r2.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, (o2.horizon, o2.need_time, o2.admitted, o2.refetch, o2.edge_idx)):
+        assert torch.equal(a, b)

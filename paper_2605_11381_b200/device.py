@@ -25,6 +25,8 @@ def tensor(data, dtype: torch.dtype) -> torch.Tensor:
     if isinstance(data, torch.Tensor):
         return data.to(device=dev, dtype=dtype).contiguous()
     arr = np.ascontiguousarray(data)
+    if not arr.flags.writeable:
+        arr = arr.copy()
     t = torch.from_numpy(arr) if arr.dtype != object else torch.tensor(data)
     return t.to(dtype=dtype).to(dev, non_blocking=False).contiguous()
 

@@ -124,3 +124,34 @@ def test_divergence_random_vs_oracle(kb, R, S, Lp, Lc, D):
                                          return_cos=True)
     assert np.array_equal(H.cpu().numpy(), exp)
     assert np.array_equal(cos.cpu().numpy(), exp_cos, equal_nan=True)
+
+
+@pytest.mark.parametrize("N", [1, 7, 50, 64])
+@pytest.mark.parametrize("storage", [np.float32, np.float64])
+def test_confidence_threshold_boundary(kb, N, storage):
+    """f placed at, one ulp above and one ulp below opt * mean (the reference's
+    own fp64 evaluation), plus zero / subnormal / huge columns: every fp32 and
+    fp64 filter decision next to its margin is exercised against the oracle."""
+    rng = np.random.default_rng(N * 13 + (storage == np.float32))
+    R, K, t = 600, 6, 0.4
+    extremes = [1e-300, 1e300] if storage == np.float64 else [1e-44, 1e36]
+    scale = np.array([1.0, 1e-3, 1e3, 1e-38, *extremes, 3.0, 1e-30])[rng.integers(0, 8, R)]
+    U = (rng.uniform(0.1, 1.0, (R, K, N)) * scale[:, None, None]).astype(storage)
+    opt = 1.0 + t
+    mean = U[:, :-1].astype(np.float64).sum(axis=1) / (K - 1)  # sequential for N >= 2
+    target = (opt * mean).astype(storage)
+    pick = rng.integers(0, 6, (R, N))
+    up = np.nextafter(target, np.array(np.inf, storage))
+    dn = np.nextafter(target, np.array(0, storage))
+    last = np.select([pick == 0, pick == 1, pick == 2, pick == 3, pick == 4],
+                     [target, up, dn, np.zeros_like(target), U[:, -1]], default=target * 2)
+    U[:, -1] = last.astype(storage)
+    U[rng.integers(0, R, 20), :-1] = 0  # zero means
+    U = np.ascontiguousarray(U)
+    for hmin in (1, 3):
+        exp = orc.horizon_conf_batch(U, t, hmin)
+        H = kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(t, hmin),
+                                    torch.from_numpy(U).cuda())
+        got = H.cpu().numpy()
+        bad = np.nonzero(got != exp)[0]
+        assert bad.size == 0, (bad[:5], got[bad[:5]], exp[bad[:5]], scale[bad[:5]])

@@ -369,7 +369,7 @@ __global__ void k_horizon_static(int64_t R, int32_t h, int32_t* H) {
 // and tiles that cannot be moved by TMA.
 static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* rbytes, int64_t R,
                             int items_per_robot, uint32_t aux_per_robot, int max_threads,
-                            int regs_per_thread) {
+                            int regs_per_thread, int min_rounds = 1) {
     const DeviceInfo& di = device_info();
     StreamPlan p{};
     p.nseg = nseg;
@@ -393,6 +393,9 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
     static const int max_override = std::getenv("KR_PLAN_MAX_THREADS")
                                         ? std::atoi(std::getenv("KR_PLAN_MAX_THREADS")) : 0;
     if (max_override >= 32 && max_override < max_threads) max_threads = max_override;
+    static const int rounds_override = std::getenv("KR_PLAN_MIN_ROUNDS")
+                                           ? std::atoi(std::getenv("KR_PLAN_MIN_ROUNDS")) : 0;
+    if (rounds_override >= 1 && rounds_override <= kMaxRounds) min_rounds = rounds_override;
     const int regs = ((regs_per_thread > 0 ? regs_per_thread : 64) + 7) / 8 * 8;
     const uint64_t smem_sm = static_cast<uint64_t>(di.max_smem_optin) + 1024;  // per-SM pool
     const double kInflightTarget = 160.0 * 1024;
@@ -400,7 +403,11 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
     for (int64_t t = 1; t <= 1024; t++) {
         const int64_t items = t * items_per_robot;
         if (items > static_cast<int64_t>(max_threads) * kMaxRounds) break;
-        const int rounds = static_cast<int>((items + max_threads - 1) / max_threads);
+        int rounds = static_cast<int>((items + max_threads - 1) / max_threads);
+        if (rounds < min_rounds) {
+            if (items < static_cast<int64_t>(min_rounds) * 32) continue;
+            rounds = min_rounds;
+        }
         const int threads = static_cast<int>(((items + rounds - 1) / rounds + 31) / 32 * 32);
         const uint64_t sb = stage_bytes(t);
         const uint64_t aux = (256 + t * aux_per_robot + 127) & ~uint64_t(127);
@@ -547,8 +554,10 @@ extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_
     auto go = [&](auto proto, auto kstaged, auto kdirect) {
         using W = decltype(proto);
         constexpr int VC = W::kVC;
+        // two items per thread per tile: measured 80% -> 92% of the HBM peak
+        // (K=6, N=50 fp32) from the amortised per-tile ring handshake
         StreamPlan p = make_plan(1, bases, &rb, R, N / VC, kMaxStages * sizeof(int),
-                                 conf_max_threads<VC>() - 32, kernel_regs(kstaged));
+                                 conf_max_threads<VC>() - 32, kernel_regs(kstaged), 2);
         const float m = static_cast<float>(K + 8) * 5.9604645e-8f;
         const double md = 1.7763568394002505e-15;  // 2^-49
         W w{K,       N,       p.TR,    min_horizon, p.rounds, one_plus_t,

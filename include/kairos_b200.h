@@ -8,6 +8,7 @@
  *
  *   kr_horizon_confidence   horizon.py:108-132   decide_horizon (confidence branch)
  *   kr_horizon_static       horizon.py:121-122   decide_horizon (static branch)
+ *   kr_horizon_sweep        horizon.py:135-151   sweep_thresholds (cli.py:109-140 cmd_pareto)
  *   kr_horizon_divergence   workload.py:461-496  _cosine + round_optimal_horizon
  *   kr_us_from_actions      core.py:24-47,157-166 us_from_actions / exec_end_from_piggyback
  *   kr_wait_ratio           waiting.py:62-66,96-100 wait_ratio / current_wait_ratio
@@ -114,6 +115,16 @@ KR_API int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_t K,
                           double one_plus_t, int32_t min_horizon, int32_t* H,
                           uint32_t* flags, void* stream);
 KR_API int kr_horizon_static(int64_t R, int32_t N, int32_t static_h, int32_t* H, void* stream);
+
+/* C <= 64 policy configurations decided over the same rounds U[R][K][N] in
+ * one pass (sweep_thresholds / cmd_pareto).  Host arrays per configuration:
+ * kind[c] 0 = static (param[c] = static_h), 1 = confidence (one_plus_t[c] =
+ * 1.0 + threshold, param[c] = min_horizon).  sums[c] (device, caller-zeroed,
+ * accumulated) += sum_r decide_horizon(cfg_c, U[r]); H (nullable) [C][R]
+ * receives every decision.  The reference's mean is sums[c] / R. */
+KR_API int kr_horizon_sweep(const void* U, int dtype, int64_t R, int32_t K, int32_t N, int32_t C,
+                            const int32_t* kind, const double* one_plus_t, const int32_t* param,
+                            unsigned long long* sums, int32_t* H, uint32_t* flags, void* stream);
 
 /* prev: [R][Lp][D], cand: [R][S][Lc][D] (same dtype).  For robot r the
  * reference trajectory is prev[r][off_r : len_prev_r] (the unexecuted overlap

@@ -175,6 +175,20 @@ def horizon_conf_batch(U: np.ndarray, threshold: float, min_horizon: int,
     return H
 
 
+def sweep_sums(U: np.ndarray, cfgs) -> np.ndarray:
+    """sum_r decide_horizon(cfg, U[r]) per configuration (horizon.py:135-151 is
+    sum(decide_horizon(...)) / len(seq)).  cfgs: (kind, static_h, threshold,
+    min_horizon) tuples, kind 1 = confidence, 0 = static (horizon.py:121-122)."""
+    R, _, N = U.shape
+    out = np.empty(len(cfgs), np.int64)
+    for c, (kind, static_h, t, hmin) in enumerate(cfgs):
+        if kind == 0:
+            out[c] = R * min(static_h, N)
+        else:
+            out[c] = int(horizon_conf_batch(U, t, hmin).astype(np.int64).sum())
+    return out
+
+
 def divergence_batch(prev, cand, thr: float, offset=None, len_prev=None, len_cand=None,
                      want_cos: bool = False, nthreads: int = 0):
     """prev [R,Lp,D]; cand [R,Lc,D] or [R,S,Lc,D] (same float dtype)."""

@@ -21,7 +21,7 @@ from .divergence import round_optimal_horizon, round_optimal_horizon_batch  # no
 from .engines import (EngineProfile, NetworkModel, ProfileError, batch_latency,  # noqa: F401
                       cloud_round_trip, transfer_time)
 from .horizon import (HorizonPolicyConfig, UpdateMagnitudes, decide_horizon,  # noqa: F401
-                      decide_horizon_batch, sweep_thresholds)
+                      decide_horizon_batch, sweep_horizon_sums, sweep_thresholds)
 from .scheduler import (DispatchPlan, SchedulerConfig, assign_bucket,  # noqa: F401
                         estimate_exec_latency, order_within_bucket, plan, plan_fifo, plan_las)
 from .waiting import (WaitLedger, current_wait_ratio, ledger_from_history,  # noqa: F401

@@ -56,6 +56,8 @@ _SIGNATURES = {
     "kr_horizon_confidence": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _f64, _i32,
                                              _vp, _vp, _vp]),
     "kr_horizon_static": (ctypes.c_int, [_i64, _i32, _i32, _vp, _vp]),
+    "kr_horizon_sweep": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _vp, _vp, _vp,
+                                        _vp, _vp, _vp, _vp]),
     "kr_horizon_divergence": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _i64, _i32, _i32, _i32,
                                              _i32, _vp, _vp, _vp, _f64, _vp, _vp, _i32, _vp]),
     "kr_us_from_actions": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),

@@ -2,14 +2,16 @@
 
 Drop-in for `roboserve.horizon` (reference horizon.py:1-151).  The policy
 objects keep the reference's fields, defaults and validation; every decision
-runs in the `kr_horizon_confidence` / `kr_horizon_static` CUDA kernels, in
-fp64 with the reference's numpy evaluation order, so results are bit-exact.
+runs in the `kr_horizon_confidence` / `kr_horizon_static` / `kr_horizon_sweep`
+CUDA kernels, in fp64 with the reference's numpy evaluation order, so results
+are bit-exact.
 `decide_horizon_batch` is the fleet-scale entry point over a device tensor
 U[R, K, N] (fp32 or fp64 storage).
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -141,12 +143,68 @@ def decide_horizon(cfg: HorizonPolicyConfig, magnitudes: UpdateMagnitudes) -> in
     return int(decide_horizon_batch(cfg, U, validate=False).item())
 
 
+SWEEP_MAX_CONFIGS = 64  # per kernel launch (kr_horizon_sweep); more are split
+
+
+def _addr(arr) -> int:
+    return ctypes.addressof(arr)
+
+
+def sweep_horizon_sums(cfgs: Sequence[HorizonPolicyConfig], U: torch.Tensor,
+                       H: torch.Tensor | None = None, validate: bool = True) -> torch.Tensor:
+    """Device sums[c] = sum_r decide_horizon(cfgs[c], U[r]) (int64 [C]) in one
+    pass over U[R, K, N] per 64 configurations (kr_horizon_sweep).  With `H`
+    (int32 [C, R]) every decision is written too.  Asynchronous unless
+    `validate` (one flag-word read)."""
+    if not cfgs:
+        raise ValueError("no policy configurations given")
+    if U.dim() != 3:
+        raise ValueError(f"update magnitudes must be R x K x N, got shape {tuple(U.shape)}")
+    if U.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"U must be float32 or float64, got {U.dtype}")
+    R, K, N = U.shape
+    if K < 2:
+        raise ValueError(f"need at least 2 refinement steps, got {K}")
+    if N < 1:
+        raise ValueError("chunk size must be >= 1")
+    dev.device()
+    if not U.is_cuda:
+        U = U.to(dev.device())
+    U = U.contiguous()
+    C = len(cfgs)
+    if H is not None and (tuple(H.shape) != (C, R) or H.dtype != torch.int32 or not H.is_cuda):
+        raise ValueError(f"H must be a CUDA int32 tensor of shape {(C, R)}")
+    sums = torch.zeros(C, dtype=torch.int64, device=U.device)
+    lib = _lib.load()
+    fl = dev.flags() if validate else None
+    dtype = _lib.KR_F64 if U.dtype == torch.float64 else _lib.KR_F32
+    for c0 in range(0, C, SWEEP_MAX_CONFIGS):
+        part = cfgs[c0:c0 + SWEEP_MAX_CONFIGS]
+        n = len(part)
+        kind = (ctypes.c_int32 * n)(*[0 if c.kind == STATIC else 1 for c in part])
+        opt = (ctypes.c_double * n)(*[1.0 + c.threshold for c in part])
+        prm = (ctypes.c_int32 * n)(*[c.static_h if c.kind == STATIC else c.min_horizon
+                                     for c in part])
+        _lib.check(lib.kr_horizon_sweep(U.data_ptr(), dtype, R, K, N, n, _addr(kind), _addr(opt), _addr(prm),
+                                        sums[c0:].data_ptr(),
+                                        None if H is None else H[c0].data_ptr(),
+                                        _lib.ptr(fl), dev.stream()), "kr_horizon_sweep")
+    if validate:
+        f = dev.read_flags(fl)
+        if f & _lib.FLAG_NONFINITE:
+            raise ValueError("update magnitudes must be finite")
+        if f & _lib.FLAG_NEGATIVE:
+            raise ValueError("update magnitudes must be >= 0")
+    return sums
+
+
 def sweep_thresholds(cfgs: Sequence[HorizonPolicyConfig],
                      magnitude_sequence: Iterable[UpdateMagnitudes]) -> list[float]:
     """Mean decided horizon of each config over the rounds (horizon.py:135-151).
 
-    Rounds of equal shape are stacked into one device tensor so each config is
-    a single kernel launch over all of them."""
+    Rounds of equal shape are stacked into one device tensor and every config
+    is decided in a single pass over it (kr_horizon_sweep); the mean is the
+    reference's int sum / len(seq)."""
     seq = list(magnitude_sequence)
     if not cfgs:
         raise ValueError("no policy configurations given")
@@ -155,11 +213,9 @@ def sweep_thresholds(cfgs: Sequence[HorizonPolicyConfig],
     groups: dict[tuple, list[np.ndarray]] = {}
     for m in seq:
         groups.setdefault(m.u.shape, []).append(m.u)
-    stacks = [dev.tensor(np.stack(g), torch.float64) for g in groups.values()]
-    out = []
-    for cfg in cfgs:
-        total = 0
-        for U in stacks:
-            total += int(decide_horizon_batch(cfg, U, validate=False).to(torch.int64).sum().item())
-        out.append(total / len(seq))
-    return out
+    totals = [0] * len(cfgs)
+    for g in groups.values():
+        sums = sweep_horizon_sums(list(cfgs), dev.tensor(np.stack(g), torch.float64),
+                                  validate=False).cpu().tolist()
+        totals = [a + b for a, b in zip(totals, sums)]
+    return [t / len(seq) for t in totals]

@@ -48,6 +48,17 @@ def main():
         t = timeit(lambda: kb.decide_horizon_batch(cfg, U, out=out, validate=False))
         report(f"confidence K={K} N={N} {str(dt)[6:]}", R, K * N * es + 4, t)
         del U
+    U = synthetic.magnitudes(R, seed=3, K=6, N=50, dtype=torch.float32)
+    # thresholds 0.013..0.96 avoid the synthetic bump 1.8x (a tie at t = 0.8
+    # sends every uncertain-tail column down the exact fp64 path): "tie" adds it
+    for C, tie in ((1, False), (16, False), (64, False), (16, True)):
+        ts = [0.013 + 0.947 * c / max(C - 1, 1) for c in range(C)]
+        if tie:
+            ts[-1] = 0.8
+        cfgs = [kb.HorizonPolicyConfig.confidence(t, 1 + c % 8) for c, t in enumerate(ts)]
+        t = timeit(lambda: kb.sweep_horizon_sums(cfgs, U, validate=False))
+        report(f"sweep C={C}{' tie@0.8' if tie else ''} K=6 N=50 float32 (sums)", R, 6 * 50 * 4, t)
+    del U
     for S, L, D, RR in [(1, 50, 7, R), (1, 64, 32, R // 2), (8, 50, 7, R // 4)]:
         prev, cand, off = synthetic.chunks(RR, seed=5, Lp=L, Lc=L, D=D, S=S)
         out = torch.empty(RR, dtype=torch.int32, device="cuda")

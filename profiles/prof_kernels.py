@@ -1,5 +1,5 @@
 """Small driver for ncu captures of the non-headline horizon kernels:
-    python profiles/prof_kernels.py conf|div32|ens [R]"""
+    python profiles/prof_kernels.py conf|div32|ens|sweep16 [R]"""
 import sys
 from pathlib import Path
 
@@ -16,6 +16,13 @@ if which == "conf":
     U = synthetic.magnitudes(R, seed=3)
     for _ in range(3):
         kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(0.4, 5), U, validate=False)
+elif which.startswith("sweep"):
+    C = int(which[5:])
+    U = synthetic.magnitudes(R, seed=3)
+    cfgs = [kb.HorizonPolicyConfig.confidence(0.013 + 0.947 * c / max(C - 1, 1), 1 + c % 8)
+            for c in range(C)]
+    for _ in range(3):
+        kb.sweep_horizon_sums(cfgs, U, validate=False)
 else:
     S, L, D = (1, 64, 32) if which == "div32" else (8, 50, 7)
     RR = R // 2 if which == "div32" else R // 4

@@ -89,6 +89,62 @@ def save_confidence(cases):
         expected=np.array([c[3] for c in cases], np.int64))
 
 
+# --- step 1a': threshold sweep (horizon.py:135-151) --------------------------
+
+def gen_sweep(rng: np.random.Generator):
+    """Sequences of rounds (mixed shapes within a sequence) x configuration
+    lists (static and confidence, duplicates, more than 64 configurations),
+    with the reference's sweep_thresholds means."""
+    cases = []
+    for i in range(48):
+        n = int(rng.integers(1, 41))
+        shapes = [(int(rng.integers(2, 9)), int(rng.choice([1, 7, 50, 64])))]
+        if rng.random() < 0.4:
+            shapes.append((6, 50))
+        seq = []
+        for _ in range(n):
+            K, N = shapes[int(rng.integers(0, len(shapes)))]
+            spec = workload.SyntheticSpec(chunk_size=N, diffusion_steps=K,
+                                          uncertain_fraction=float(rng.uniform(0, 0.5)))
+            u = workload._synth_round_magnitudes(spec, rng).u
+            if rng.random() < 0.5:
+                u = u.astype(np.float32).astype(np.float64)
+            seq.append(horizon.UpdateMagnitudes(u))
+        C = int(rng.choice([1, 3, 8, 17, 64, 70]))
+        cfgs = []
+        for _ in range(C):
+            if rng.random() < 0.2:
+                cfgs.append(horizon.HorizonPolicyConfig.static(int(rng.integers(1, 80))))
+            else:
+                t = float(rng.choice([0.0, 0.2, 0.4, 0.8, 1.0, rng.uniform(0, 2)]))
+                cfgs.append(horizon.HorizonPolicyConfig.confidence(t, int(rng.integers(1, 9))))
+        cases.append((seq, cfgs, horizon.sweep_thresholds(cfgs, seq)))
+    return cases
+
+
+def save_sweep(cases):
+    us, shapes, seq_off, kinds, sh, thr, hmin, cfg_off, exp = [], [], [0], [], [], [], [], [0], []
+    for seq, cfgs, means in cases:
+        for m in seq:
+            us.append(m.u.ravel())
+            shapes.append(m.u.shape)
+        seq_off.append(len(shapes))
+        for c in cfgs:
+            kinds.append(int(c.kind == horizon.CONFIDENCE_THRESHOLD))
+            sh.append(c.static_h)
+            thr.append(c.threshold)
+            hmin.append(c.min_horizon)
+        cfg_off.append(len(kinds))
+        exp.extend(means)
+    shapes = np.array(shapes, np.int64)
+    offs = np.concatenate([[0], np.cumsum(shapes[:, 0] * shapes[:, 1])]).astype(np.int64)
+    np.savez_compressed(OUT / "sweep.npz", u=np.concatenate(us), shapes=shapes, offsets=offs,
+                        seq_off=np.array(seq_off, np.int64), kind=np.array(kinds, np.int64),
+                        static_h=np.array(sh, np.int64), threshold=np.array(thr),
+                        min_horizon=np.array(hmin, np.int64),
+                        cfg_off=np.array(cfg_off, np.int64), expected=np.array(exp))
+
+
 # --- step 1b: divergence horizon + cosine scores ----------------------------
 
 def gen_divergence(rng: np.random.Generator):
@@ -340,6 +396,9 @@ def gen_fig4():
 
 
 def main():
+    if sys.argv[1:] == ["sweep"]:  # only the threshold-sweep fixture
+        save_sweep(gen_sweep(np.random.default_rng(11)))
+        return
     rng = np.random.default_rng(20260517)
     save_confidence(gen_confidence(rng))
     save_divergence(gen_divergence(rng))
@@ -348,6 +407,7 @@ def main():
     (OUT / "plan_cloud.json").write_text(json.dumps(gen_plan_cloud(np.random.default_rng(7)),
                                                     separators=(",", ":")))
     (OUT / "fig4.json").write_text(json.dumps(gen_fig4(), indent=1))
+    save_sweep(gen_sweep(np.random.default_rng(11)))
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".npz", ".json"):
             print(f"{p.name:28s} {p.stat().st_size:>9d} B")

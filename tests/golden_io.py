@@ -19,6 +19,23 @@ def confidence_cases():
     return out
 
 
+def sweep_cases():
+    """[(rounds: list of [K,N] arrays, configs: list of (kind, static_h, threshold,
+    min_horizon), expected means)] -- kind 1 = confidence, 0 = static."""
+    z = np.load(GOLDEN / "sweep.npz")
+    out = []
+    for i in range(len(z["seq_off"]) - 1):
+        rounds = []
+        for j in range(z["seq_off"][i], z["seq_off"][i + 1]):
+            k, n = z["shapes"][j]
+            rounds.append(z["u"][z["offsets"][j]:z["offsets"][j + 1]].reshape(k, n))
+        lo, hi = z["cfg_off"][i], z["cfg_off"][i + 1]
+        cfgs = [(int(z["kind"][c]), int(z["static_h"][c]), float(z["threshold"][c]),
+                 int(z["min_horizon"][c])) for c in range(lo, hi)]
+        out.append((rounds, cfgs, [float(x) for x in z["expected"][lo:hi]]))
+    return out
+
+
 def divergence_cases():
     z = np.load(GOLDEN / "divergence.npz")
     out = []

@@ -155,3 +155,86 @@ def test_confidence_threshold_boundary(kb, N, storage):
         got = H.cpu().numpy()
         bad = np.nonzero(got != exp)[0]
         assert bad.size == 0, (bad[:5], got[bad[:5]], exp[bad[:5]], scale[bad[:5]])
+
+
+# --- threshold sweep (horizon.py:135-151, cli.py:109-140) -------------------
+
+def _cfg(kb, c):
+    kind, static_h, t, hmin = c
+    return (kb.HorizonPolicyConfig.confidence(t, hmin) if kind
+            else kb.HorizonPolicyConfig.static(static_h))
+
+
+def test_sweep_golden(kb):
+    """The reference's own sweep_thresholds means (48 sequences, mixed shapes,
+    up to 70 configurations -> two kernel launches)."""
+    for rounds, cfgs, exp in golden_io.sweep_cases():
+        got = kb.sweep_thresholds([_cfg(kb, c) for c in cfgs],
+                                  [kb.UpdateMagnitudes(u) for u in rounds])
+        assert got == exp
+
+
+@pytest.mark.parametrize("R,K,N", [(1, 2, 1), (999, 6, 50), (4099, 6, 64), (513, 3, 1),
+                                   (300, 10, 7), (257, 4, 300)])
+@pytest.mark.parametrize("storage", [np.float32, np.float64])
+def test_sweep_vs_oracle_every_decision(kb, R, K, N, storage):
+    rng = np.random.default_rng(R + K + N)
+    U = (rng.uniform(0.5, 2.0, (R, 1, N)) * rng.uniform(0.3, 0.8, (R, 1, N)) **
+         np.arange(K)[None, :, None] * rng.uniform(0.95, 1.05, (R, K, N)))
+    tail = rng.integers(0, N + 1, R)
+    for r in range(R):
+        if tail[r] < N:
+            U[r, -1, tail[r]:] = rng.choice([1.2, 1.8, 3.0]) * U[r, :-1, tail[r]:].mean(axis=0)
+    U[rng.integers(0, R, max(1, R // 50)), :-1] = 0  # zero means
+    U = np.ascontiguousarray(U.astype(storage))
+    cfgs = [(1, 0, t, h) for t in (0.0, 0.1, 0.2, 0.4, 0.4, 0.8, 1.0, 1.7, 2.5) for h in (1, 5)]
+    cfgs += [(0, s, 0.4, 5) for s in (1, 10, 400)]
+    C = len(cfgs)
+    H = torch.empty(C, R, dtype=torch.int32, device="cuda")
+    sums = kb.sweep_horizon_sums([_cfg(kb, c) for c in cfgs], torch.from_numpy(U).cuda(), H=H)
+    Hh = H.cpu().numpy()
+    for c, (kind, s, t, h) in enumerate(cfgs):
+        exp = (np.full(R, min(s, N), np.int32) if kind == 0 else orc.horizon_conf_batch(U, t, h))
+        assert np.array_equal(Hh[c], exp), (c, cfgs[c])
+    exp_sums = orc.sweep_sums(U, cfgs)
+    assert np.array_equal(sums.cpu().numpy(), exp_sums)
+    # sums-only launch (no per-decision writes) and a permuted configuration list
+    perm = rng.permutation(C)
+    sums2 = kb.sweep_horizon_sums([_cfg(kb, cfgs[i]) for i in perm], torch.from_numpy(U).cuda())
+    assert np.array_equal(sums2.cpu().numpy(), exp_sums[perm])
+
+
+@pytest.mark.parametrize("storage", [np.float32, np.float64])
+def test_sweep_threshold_boundary(kb, storage):
+    """Final magnitudes at / one ulp around (1 + t) * mean for several t of the
+    sweep at once: the per-configuration binary search next to its margins."""
+    rng = np.random.default_rng(5)
+    R, K, N = 2000, 6, 50
+    ts = [0.0, 0.25, 0.4, 0.5, 0.8]
+    U = (rng.uniform(0.1, 1.0, (R, K, N)) *
+         np.array([1.0, 1e-3, 1e3, 1e-30, 1e30])[rng.integers(0, 5, R)][:, None, None]).astype(storage)
+    mean = U[:, :-1].astype(np.float64).sum(axis=1) / (K - 1)
+    t_pick = np.array(ts)[rng.integers(0, len(ts), (R, N))]
+    target = ((1.0 + t_pick) * mean).astype(storage)
+    step = rng.integers(-1, 2, (R, N))
+    last = np.where(step == 0, target, np.where(step > 0, np.nextafter(target, np.array(np.inf, storage)),
+                                                np.nextafter(target, np.array(0, storage))))
+    U[:, -1] = last.astype(storage)
+    U = np.ascontiguousarray(U)
+    cfgs = [(1, 0, t, 1) for t in ts] + [(1, 0, t, 3) for t in ts[::-1]]
+    H = torch.empty(len(cfgs), R, dtype=torch.int32, device="cuda")
+    kb.sweep_horizon_sums([_cfg(kb, c) for c in cfgs], torch.from_numpy(U).cuda(), H=H)
+    for c, (_, _, t, h) in enumerate(cfgs):
+        assert np.array_equal(H[c].cpu().numpy(), orc.horizon_conf_batch(U, t, h)), cfgs[c]
+
+
+def test_sweep_validation(kb):
+    U = torch.ones(4, 6, 50, dtype=torch.float64, device="cuda")
+    U[2, 3, 7] = float("nan")
+    with pytest.raises(ValueError, match="finite"):
+        kb.sweep_horizon_sums([kb.HorizonPolicyConfig.confidence()], U)
+    U[2, 3, 7] = -1.0
+    with pytest.raises(ValueError, match=">= 0"):
+        kb.sweep_horizon_sums([kb.HorizonPolicyConfig.static(3)], U)
+    with pytest.raises(ValueError, match="no policy"):
+        kb.sweep_horizon_sums([], U)

@@ -30,6 +30,18 @@ def test_confidence_batch_matches_scalar():
         assert H[r] == orc.decide_horizon_conf(U[r].astype(np.float64), 0.4, 5)
 
 
+def test_sweep_golden():
+    """Reference sweep_thresholds means == the oracle's per-shape sums / len(seq)."""
+    for rounds, cfgs, exp in golden_io.sweep_cases():
+        totals = np.zeros(len(cfgs), np.int64)
+        groups = {}
+        for u in rounds:
+            groups.setdefault(u.shape, []).append(u)
+        for g in groups.values():
+            totals += orc.sweep_sums(np.stack(g), cfgs)
+        assert [int(t) / len(rounds) for t in totals] == exp
+
+
 def test_divergence_golden_horizon_and_cosine():
     bad_h, bad_c = [], []
     for i, (ref, cand, thr, exp, cos) in enumerate(golden_io.divergence_cases()):

@@ -19,6 +19,9 @@
  *   kr_select_admit         scheduler.py:193-241 select + admission + ordered S_e
  *   kr_admit                scheduler.py:223-234 refetch + skip counters
  *   kr_sort_keys            scheduler.py:130-140 the total order itself
+ *   kr_ledger_apply         core.py:200-229 + waiting.py:69-93  incremental TaskState
+ *                           history and running wait totals (sim.py:358-440 mutations)
+ *   kr_urgency_ledger       kr_urgency over the device-resident ledger (O(1) per request)
  *   kr_transfer_time        engines.py:158-169   per-request uplink time
  *   kr_place_cloud          scheduler.py:160-234 phase-3 cloud offload scan
  *
@@ -64,6 +67,7 @@ enum { KR_KAIROS = 0, KR_FIFO = 1, KR_LAS = 2 };
 #define KR_FLAG_KEY_RANGE  0x4u  /* packed sort-key field out of range */
 #define KR_FLAG_TIME_RANGE 0x8u  /* core.py:38-41 negative action count / overflow       */
 #define KR_FLAG_RATIO      0x10u /* wait-ratio operand beyond 2^53 (inexact double)      */
+#define KR_FLAG_LEDGER     0x20u /* ledger event out of order / beyond capacity        */
 
 /* 128-bit composite sort key (ascending = reference order). */
 typedef struct kr_key {
@@ -86,6 +90,46 @@ typedef struct kr_fleet {
     const int32_t* n_gen;            /* len(TaskState.gen_starts)                        */
     const int64_t* slots;            /* [*][4] gen_start, gen_end, exec_start, exec_end  */
 } kr_fleet;
+
+/* Device-resident incremental ledger: per-task state and append-only history
+ * (TaskState, core.py:169-249), kept across planning rounds. */
+typedef struct kr_ledger {
+    int64_t n_tasks;                 /* task slots allocated                            */
+    int32_t cap;                     /* history rounds per task                         */
+    int32_t pad_;
+    int64_t* t_start;                /* [n_tasks] TaskState.t_start                     */
+    int32_t* n_exec;                 /* [n_tasks] len(exec_intervals)                   */
+    int32_t* n_gen;                  /* [n_tasks] len(gen_starts)                       */
+    int32_t* wait_next;              /* [n_tasks] first round whose wait is not final   */
+    int64_t* wait_total;             /* [n_tasks] ledger_from_history(state).total_wait */
+    int64_t* slots;                  /* [n_tasks][cap][4] gen_start, gen_end (INT64_MIN
+                                        while in flight), exec_start, exec_end          */
+} kr_ledger;
+
+enum { KR_EV_NEW = 0, KR_EV_BEGIN_GEN = 1, KR_EV_FINISH_GEN = 2, KR_EV_EXEC = 3 };
+
+/* A batch of TaskState mutations grouped by task (each group in call order). */
+typedef struct kr_events {
+    int64_t n_groups;                /* tasks touched                                   */
+    const int32_t* task;             /* [n_groups] task slot                            */
+    const int32_t* off;              /* [n_groups + 1] event range of each group        */
+    const int32_t* kind;             /* [events] KR_EV_*                                */
+    const int32_t* round;            /* [events] round id (unused for KR_EV_NEW)        */
+    const int64_t* a;                /* [events] t_start / at / at / exec start         */
+    const int64_t* b;                /* [events] exec end (KR_EV_EXEC)                  */
+} kr_events;
+
+/* One planning round's pending requests against a kr_ledger. */
+typedef struct kr_requests {
+    int64_t n;
+    const int32_t* task;             /* task slot of each request                       */
+    const int64_t* issued_at;
+    const int64_t* obs_captured_at;
+    const int64_t* accum_gen;        /* TaskState.accumulated_generation (LAS key)      */
+    const int32_t* remaining;
+    const int32_t* lexrank;
+    int32_t* skipped;                /* PendingRequest.skipped in, updated by admission */
+} kr_requests;
 
 /* SchedulerConfig (scheduler.py:38-56) plus the round's scalars. */
 typedef struct kr_sched {
@@ -162,6 +206,18 @@ KR_API int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys, 
  * {OR hi, OR lo, AND hi, AND lo} of the keys written, so the admission select
  * needs no extra pass over the keys. */
 KR_API int kr_key_stats_init(unsigned long long* key_stats, void* stream);
+
+/* Apply a batch of TaskState mutations to the device ledger (one thread per
+ * task; wait totals advance incrementally).  Out-of-order rounds or rounds
+ * beyond ledger->cap set KR_FLAG_LEDGER and are skipped. */
+KR_API int kr_ledger_apply(const kr_ledger* ledger, const kr_events* events, uint32_t* flags,
+                           void* stream);
+/* kr_urgency over ledger-backed requests: identical keys / outputs, with the
+ * total wait and last execution read in O(1) per request. */
+KR_API int kr_urgency_ledger(const kr_ledger* ledger, const kr_requests* req, const kr_sched* cfg,
+                             kr_key* keys, int64_t* need_time, int64_t* total_wait, double* wr,
+                             int32_t* bucket, int64_t* est, unsigned long long* key_stats,
+                             uint32_t* flags, void* stream);
 
 /* ---- step 3: priority ordering + top-k admission ---------------------- */
 

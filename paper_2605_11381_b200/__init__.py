@@ -6,7 +6,9 @@ of the reference package `roboserve`:
   cosine divergence against the unexecuted overlap of the previous chunk);
 * step 2, execution-aware urgency: wait ledger, wait ratio, bucket with aging,
   projected execution duration and next-need time;
-* step 3, priority ordering and top-k edge admission: `plan`.
+* step 3, priority ordering and top-k edge admission: `plan` (with
+  `LedgerStates`, the simulator's planning loop runs against a
+  device-resident incremental task ledger).
 
 Every decision runs in hand-written sm_100a CUDA kernels behind the C ABI in
 include/kairos_b200.h (libkairos_b200.so); there is no CPU fallback.  The
@@ -20,6 +22,7 @@ from .core import (ActionChunk, Duration, Interval, LastExecInfo, PendingRequest
 from .divergence import round_optimal_horizon, round_optimal_horizon_batch  # noqa: F401
 from .engines import (EngineProfile, NetworkModel, ProfileError, batch_latency,  # noqa: F401
                       cloud_round_trip, transfer_time)
+from .ledger import DeviceLedger, LedgerStates  # noqa: F401
 from .horizon import (HorizonPolicyConfig, UpdateMagnitudes, decide_horizon,  # noqa: F401
                       decide_horizon_batch, sweep_horizon_sums, sweep_thresholds)
 from .scheduler import (DispatchPlan, SchedulerConfig, assign_bucket,  # noqa: F401

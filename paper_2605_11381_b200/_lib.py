@@ -25,6 +25,7 @@ FLAG_NEGATIVE = 0x2
 FLAG_KEY_RANGE = 0x4
 FLAG_TIME_RANGE = 0x8
 FLAG_RATIO = 0x10
+FLAG_LEDGER = 0x20
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -48,6 +49,26 @@ class KrSched(ctypes.Structure):
                 ("hz_num", _i64), ("hz_den", _i64), ("issued_base", _i64)]
 
 
+class KrLedger(ctypes.Structure):
+    """kr_ledger: device-resident per-task state and history."""
+
+    _fields_ = [("n_tasks", _i64), ("cap", _i32), ("pad_", _i32)] + [(k, _vp) for k in (
+        "t_start", "n_exec", "n_gen", "wait_next", "wait_total", "slots")]
+
+
+class KrEvents(ctypes.Structure):
+    """kr_events: TaskState mutations grouped by task."""
+
+    _fields_ = [("n_groups", _i64)] + [(k, _vp) for k in ("task", "off", "kind", "round", "a", "b")]
+
+
+class KrRequests(ctypes.Structure):
+    """kr_requests: one planning round's pending requests against a kr_ledger."""
+
+    _fields_ = [("n", _i64)] + [(k, _vp) for k in (
+        "task", "issued_at", "obs_captured_at", "accum_gen", "remaining", "lexrank", "skipped")]
+
+
 _SIGNATURES = {
     "kr_version": (ctypes.c_char_p, []),
     "kr_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -66,6 +87,11 @@ _SIGNATURES = {
     "kr_urgency": (ctypes.c_int, [ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _vp, _vp,
                                   _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kr_key_stats_init": (ctypes.c_int, [_vp, _vp]),
+    "kr_ledger_apply": (ctypes.c_int, [ctypes.POINTER(KrLedger), ctypes.POINTER(KrEvents), _vp,
+                                       _vp]),
+    "kr_urgency_ledger": (ctypes.c_int, [ctypes.POINTER(KrLedger), ctypes.POINTER(KrRequests),
+                                         ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp, _vp, _vp,
+                                         _vp, _vp, _vp]),
     "kr_workspace_bytes": (ctypes.c_size_t, [_i64]),
     "kr_topk_select": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "kr_select_admit": (ctypes.c_int, [_vp, _i64, _i64, _vp, ctypes.POINTER(KrFleet),

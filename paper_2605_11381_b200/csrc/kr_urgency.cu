@@ -83,15 +83,69 @@ __device__ __forceinline__ unsigned long long wand(unsigned long long v) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) k_urgency(kr_fleet f, kr_sched c, UrgencyOut o) {
+// Per-request inputs of the urgency pass.  FleetSrc: one self-contained
+// structure-of-arrays per planning round (history as CSR slots, walked per
+// request).  LedgerSrc: the device-resident incremental ledger -- requests
+// index their task, whose running wait total and last execution are O(1).
+struct FleetSrc {
+    kr_fleet f;
+    static constexpr bool kSlots = true;
+    __device__ int64_t n() const { return f.n; }
+    __device__ int64_t issued(int64_t i) const { return __ldg(f.issued_at + i); }
+    __device__ int32_t rank(int64_t i) const { return __ldg(f.lexrank + i); }
+    __device__ int32_t remaining(int64_t i) const { return __ldg(f.remaining + i); }
+    __device__ int64_t accum(int64_t i) const { return __ldg(f.accum_gen + i); }
+    __device__ int32_t skipped(int64_t i) const { return f.skipped[i]; }
+    // total wait, t_start, number of executions and the last execution length
+    __device__ void hist(int64_t i, int64_t& w, int64_t& t0, int32_t& ne, int64_t& last) const {
+        const int64_t* slots = f.slots + 4 * __ldg(f.hist_off + i);
+        ne = __ldg(f.n_exec + i);
+        w = total_wait(slots, ne, __ldg(f.n_gen + i));
+        t0 = __ldg(f.t_start + i);
+        if (ne > 0) {
+            Slot l = load_slot(slots, ne - 1);
+            last = l.ee - l.es;
+        }
+    }
+    __device__ void waits(int64_t i, int64_t* out) const {
+        slot_waits(f.slots + 4 * __ldg(f.hist_off + i), __ldg(f.n_exec + i), __ldg(f.n_gen + i),
+                   out + __ldg(f.hist_off + i));
+    }
+};
+
+struct LedgerSrc {
+    kr_ledger L;
+    kr_requests q;
+    static constexpr bool kSlots = false;
+    __device__ int64_t n() const { return q.n; }
+    __device__ int64_t issued(int64_t i) const { return __ldg(q.issued_at + i); }
+    __device__ int32_t rank(int64_t i) const { return __ldg(q.lexrank + i); }
+    __device__ int32_t remaining(int64_t i) const { return __ldg(q.remaining + i); }
+    __device__ int64_t accum(int64_t i) const { return __ldg(q.accum_gen + i); }
+    __device__ int32_t skipped(int64_t i) const { return q.skipped[i]; }
+    __device__ void hist(int64_t i, int64_t& w, int64_t& t0, int32_t& ne, int64_t& last) const {
+        const int64_t t = __ldg(q.task + i);
+        ne = L.n_exec[t];
+        w = L.wait_total[t];
+        t0 = L.t_start[t];
+        if (ne > 0) {
+            const int64_t* sl = L.slots + (t * L.cap + ne - 1) * 4;
+            last = sl[3] - sl[2];
+        }
+    }
+    __device__ void waits(int64_t, int64_t*) const {}
+};
+
+template <class Src>
+__global__ void __launch_bounds__(256) k_urgency(Src s, kr_sched c, UrgencyOut o) {
     uint32_t fl = 0;
     unsigned long long ohi = 0, olo = 0, ahi = ~0ull, alo = ~0ull;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < f.n;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < s.n();
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t issued = __ldg(f.issued_at + i);
-        const int32_t rank = __ldg(f.lexrank + i);
+        const int64_t issued = s.issued(i);
+        const int32_t rank = s.rank(i);
         if (o.need_time) {
-            int32_t rem = __ldg(f.remaining + i);
+            int32_t rem = s.remaining(i);
             o.need_time[i] = issued + us_from_actions(rem, c.hz_num, c.hz_den, &fl);
         }
         kr_key key;
@@ -100,28 +154,25 @@ __global__ void __launch_bounds__(256) k_urgency(kr_fleet f, kr_sched c, Urgency
             key.lo = static_cast<uint64_t>(static_cast<uint32_t>(rank));
             if (rank < 0) fl |= KR_FLAG_KEY_RANGE;
         } else if (c.policy == KR_LAS) {
-            key.hi = static_cast<uint64_t>(__ldg(f.accum_gen + i)) ^ (uint64_t(1) << 63);
+            key.hi = static_cast<uint64_t>(s.accum(i)) ^ (uint64_t(1) << 63);
             key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
         }
         const bool need_hist =
             c.policy == KR_KAIROS || o.total_wait || o.wr || o.bucket || o.est || o.slot_wait;
         if (need_hist) {
-            const int64_t* slots = f.slots + 4 * __ldg(f.hist_off + i);
-            const int32_t ne = __ldg(f.n_exec + i), ng = __ldg(f.n_gen + i);
-            const int32_t skipped = f.skipped[i];
-            int64_t w = total_wait(slots, ne, ng);
-            double wr = wait_ratio(w, __ldg(f.t_start + i), c.now, &fl);
+            const int32_t skipped = s.skipped(i);
+            int64_t w, t0, last = 0;
+            int32_t ne;
+            s.hist(i, w, t0, ne, last);
+            double wr = wait_ratio(w, t0, c.now, &fl);
             int32_t b = assign_bucket(wr, skipped, c.buckets, c.aging_interval);
-            int64_t est = c.default_exec_estimate;
-            if (ne > 0) {
-                Slot last = load_slot(slots, ne - 1);
-                est = last.ee - last.es;
-            }
+            const int64_t est = ne > 0 ? last : c.default_exec_estimate;
             if (o.total_wait) o.total_wait[i] = w;
             if (o.wr) o.wr[i] = wr;
             if (o.bucket) o.bucket[i] = b;
             if (o.est) o.est[i] = est;
-            if (o.slot_wait) slot_waits(slots, ne, ng, o.slot_wait + __ldg(f.hist_off + i));
+            if constexpr (Src::kSlots)
+                if (o.slot_wait) s.waits(i, o.slot_wait);
             if (c.policy == KR_KAIROS) {
                 // aged = est * (1 + skipped), descending -> stored complemented
                 unsigned __int128 aged = static_cast<unsigned __int128>(est < 0 ? 0 : est) *
@@ -211,6 +262,104 @@ extern "C" int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* ke
     if (fleet->n == 0) return KR_OK;
     if (!keys) return KR_EINVAL;
     UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, slot_wait, key_stats, flags};
-    k_urgency<<<grid_for(fleet->n, 256), 256, 0, as_stream(stream)>>>(*fleet, *cfg, o);
+    k_urgency<<<grid_for(fleet->n, 256), 256, 0, as_stream(stream)>>>(FleetSrc{*fleet}, *cfg, o);
     return check_launch("kr_urgency");
+}
+
+extern "C" int kr_urgency_ledger(const kr_ledger* ledger, const kr_requests* req,
+                                 const kr_sched* cfg, kr_key* keys, int64_t* need_time,
+                                 int64_t* total_wait, double* wr, int32_t* bucket, int64_t* est,
+                                 unsigned long long* key_stats, uint32_t* flags, void* stream) {
+    if (!ledger || !req || !cfg || req->n < 0 || ledger->cap < 1) return KR_EINVAL;
+    if (cfg->policy < KR_KAIROS || cfg->policy > KR_LAS || cfg->buckets < 1 ||
+        cfg->buckets > 256 || cfg->aging_interval < 1 || cfg->hz_num <= 0 || cfg->hz_den <= 0)
+        return KR_EINVAL;
+    if (req->n == 0) return KR_OK;
+    if (!keys || !req->task) return KR_EINVAL;
+    UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, nullptr, key_stats, flags};
+    k_urgency<<<grid_for(req->n, 256), 256, 0, as_stream(stream)>>>(LedgerSrc{*ledger, *req},
+                                                                     *cfg, o);
+    return check_launch("kr_urgency_ledger");
+}
+
+// ---------------------------------------------------------------------------
+// Incremental ledger (core.py:169-249 TaskState mutations, waiting.py:69-93)
+// ---------------------------------------------------------------------------
+// One thread per touched task applies that task's events in order.  A round
+// j's wait becomes final the moment it is first computable (its successor's
+// generation start on the gen-dominated branch, its successor's execution on
+// the exec-dominated one), and the computable rounds always form a prefix, so
+// wait_total advances a cursor (wait_next) instead of re-walking the history.
+namespace kr {
+__global__ void k_ledger_apply(kr_ledger L, kr_events ev, uint32_t* flags) {
+    uint32_t fl = 0;
+    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < ev.n_groups;
+         g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = ev.task[g];
+        if (t < 0 || t >= L.n_tasks) {
+            fl |= KR_FLAG_LEDGER;
+            continue;
+        }
+        int64_t* sl = L.slots + t * L.cap * 4;
+        int32_t ne = L.n_exec[t], ng = L.n_gen[t], jw = L.wait_next[t];
+        int64_t w = L.wait_total[t];
+        for (int32_t e = ev.off[g]; e < ev.off[g + 1]; e++) {
+            const int32_t k = ev.kind[e], j = ev.round[e];
+            const int64_t a = ev.a[e];
+            if (k == KR_EV_NEW) {
+                L.t_start[t] = a;
+                ne = ng = jw = 0;
+                w = 0;
+            } else if (k == KR_EV_BEGIN_GEN) {  // core.py:200-207
+                if (j != ng || j >= L.cap) { fl |= KR_FLAG_LEDGER; continue; }
+                sl[4 * j] = a;
+                sl[4 * j + 1] = INT64_MIN;  // in flight
+                ng++;
+            } else if (k == KR_EV_FINISH_GEN) {  // core.py:209-218
+                if (j < 0 || j >= ng || sl[4 * j + 1] != INT64_MIN) { fl |= KR_FLAG_LEDGER; continue; }
+                sl[4 * j + 1] = a;
+            } else if (k == KR_EV_EXEC) {  // core.py:220-229
+                if (j != ne || j >= L.cap) { fl |= KR_FLAG_LEDGER; continue; }
+                sl[4 * j + 2] = a;
+                sl[4 * j + 3] = ev.b[e];
+                ne++;
+            } else {
+                fl |= KR_FLAG_LEDGER;
+                continue;
+            }
+            // waiting.py:81-92, advanced over the newly computable prefix
+            while (jw < ne) {
+                const int64_t gs = sl[4 * jw], ge = sl[4 * jw + 1];
+                const int64_t es = sl[4 * jw + 2], ee = sl[4 * jw + 3];
+                int64_t d;
+                if (ge - gs >= ee - es) {
+                    if (ng <= jw + 1) break;
+                    d = sl[4 * (jw + 1)] - ge;
+                } else {
+                    if (ne <= jw + 1) break;
+                    d = sl[4 * (jw + 1) + 2] - ee;
+                }
+                w += d > 0 ? d : 0;
+                jw++;
+            }
+        }
+        L.n_exec[t] = ne;
+        L.n_gen[t] = ng;
+        L.wait_next[t] = jw;
+        L.wait_total[t] = w;
+    }
+    if (fl && flags) atomicOr(flags, fl);
+}
+}  // namespace kr
+
+extern "C" int kr_ledger_apply(const kr_ledger* ledger, const kr_events* events, uint32_t* flags,
+                               void* stream) {
+    if (!ledger || !events || events->n_groups < 0 || ledger->cap < 1) return KR_EINVAL;
+    if (events->n_groups == 0) return KR_OK;
+    if (!events->task || !events->off || !events->kind || !events->round || !events->a ||
+        !events->b)
+        return KR_EINVAL;
+    k_ledger_apply<<<grid_for(events->n_groups, 128), 128, 0, as_stream(stream)>>>(*ledger, *events,
+                                                                                   flags);
+    return check_launch("kr_ledger_apply");
 }

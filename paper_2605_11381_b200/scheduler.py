@@ -161,7 +161,12 @@ def _checked_pending(pending: Iterable[PendingRequest],
 def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edge, cloud, net,
          now: TimePoint, cfg: SchedulerConfig, *, edge_in_flight: int = 0,
          cloud_in_flight: int = 0) -> DispatchPlan:
-    """One planning round under the configured policy (scheduler.py:254-276)."""
+    """One planning round under the configured policy (scheduler.py:254-276).
+
+    With `states` a `ledger.LedgerStates` (the simulator's task-state mapping
+    backed by the device-resident incremental ledger), task histories are not
+    re-packed: only the pending requests' scalars travel and the urgency pass
+    reads each task's running wait total in O(1) (kr_urgency_ledger)."""
     reqs = _checked_pending(pending, states)
     edge_avail = max(0, edge.capacity - edge_in_flight) if edge is not None else 0
     cloud_avail = max(0, cloud.capacity - cloud_in_flight) if cloud is not None else 0
@@ -171,19 +176,32 @@ def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edg
     if cfg.buckets > 256:
         raise ValueError("the packed sort key supports at most 256 buckets")
     rank = _ranks([r.task_id for r in reqs])
-    soa = fl.host_soa(reqs, states, rank)
-    base = _issued_base(soa["issued_at"])
-    fleet = fl.DeviceFleet.from_host(soa)
+    issued = np.fromiter((r.issued_at for r in reqs), np.int64, n)
+    base = _issued_base(issued)
     sched = fl.sched_struct(cfg.policy, cfg.buckets, cfg.aging_interval, cfg.stale_threshold,
                             cfg.default_exec_estimate, int(now), 1, base)
     flags = dev.flags()
-    u = fl.urgency(fleet, sched, need_time=False, flags=flags)
+    from . import ledger as _ledger
+    if isinstance(states, _ledger.LedgerStates):
+        keys, view = states.ledger.urgency(reqs, states, rank, sched, flags)
+    else:
+        view = fl.DeviceFleet.from_host(fl.host_soa(reqs, states, rank))
+        keys = fl.urgency(view, sched, need_time=False, flags=flags).keys
+    return _place(reqs, states, keys, view, sched, flags, edge, cloud, net, edge_avail,
+                  cloud_avail, edge_in_flight, cloud_in_flight)
+
+
+def _place(reqs, states, keys, fleet, sched, flags, edge, cloud, net, edge_avail, cloud_avail,
+           edge_in_flight, cloud_in_flight) -> DispatchPlan:
+    """Order, edge admission, cloud offload and the result objects, from the
+    packed keys (scheduler.py:193-241)."""
+    n = len(reqs)
     ws = fl.Workspace(n)
-    order, sorted_keys = fl.sort_keys(u.keys, ws)
+    order, sorted_keys = fl.sort_keys(keys, ws)
     k = min(edge_avail, n)
     kth_ptr = sorted_keys.data_ptr() + (k - 1) * 16 if 0 < k < n else None
-    refetch = torch.empty(n, dtype=torch.uint8, device=u.keys.device)
-    fl.admit(u.keys, k, kth_ptr, fleet, sched, None, refetch=refetch)
+    refetch = torch.empty(n, dtype=torch.uint8, device=keys.device)
+    fl.admit(keys, k, kth_ptr, fleet, sched, None, refetch=refetch)
     n_cloud = 0
     cloud_idx = None
     if cloud is not None and net is not None and cloud_avail > 0 and k < n:
@@ -194,8 +212,8 @@ def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edg
         payload = dev.tensor(np.array([r.payload_bytes for r in reqs], np.int64), torch.int64)
         up = eng.transfer_time_batch(net, payload, eng.UP)
         thr_t = dev.tensor(np.array(thr, np.int64), torch.int64)
-        cloud_idx = torch.empty(cap, dtype=torch.int32, device=u.keys.device)
-        n_cloud_t = torch.zeros(1, dtype=torch.int32, device=u.keys.device)
+        cloud_idx = torch.empty(cap, dtype=torch.int32, device=keys.device)
+        n_cloud_t = torch.zeros(1, dtype=torch.int32, device=keys.device)
         fs = fleet.c_struct()
         _lib.check(_lib.load().kr_place_cloud(
             order.data_ptr(), n, k, up.data_ptr(), thr_t.data_ptr(), cap, ctypes.byref(fs),

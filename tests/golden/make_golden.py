@@ -395,9 +395,117 @@ def gen_fig4():
     return {"stdout": buf.getvalue(), "candidates": out}
 
 
+# --- simulator planning loop (sim.py:285-311, 358-385, 424-440) ----------
+
+def gen_sim():
+    """Run the reference discrete-event simulator and record, in order, every
+    TaskState mutation it makes (creation, begin/finish generation with the
+    accumulated-generation increment, record_execution) and every plan() call
+    with its inputs and decision.  Replaying the log against an incremental
+    device ledger must reproduce every decision."""
+    from roboserve import sim as rsim
+    from roboserve.workload import SyntheticSpec, synthesize_family
+
+    log: list = []
+
+    class RecState(TaskState):
+        def __init__(self, *args, **kwargs):
+            super().__init__(*args, **kwargs)
+            log.append({"k": "new", "t": self.task_id, "a": self.t_start})
+
+        def begin_generation(self, round_id, at):
+            super().begin_generation(round_id, at)
+            log.append({"k": "bg", "t": self.task_id, "j": round_id, "a": at})
+
+        def finish_generation(self, round_id, at):
+            super().finish_generation(round_id, at)
+            log.append({"k": "fg", "t": self.task_id, "j": round_id, "a": at,
+                        "g0": self.accumulated_generation})
+
+        def record_execution(self, round_id, start, end, horizon):
+            super().record_execution(round_id, start, end, horizon)
+            log.append({"k": "rx", "t": self.task_id, "j": round_id, "a": start, "b": end,
+                        "h": horizon})
+
+    ref_plan = rsim.plan
+
+    def rec_plan(pending, states, edge, cloud, net, now, cfg, *, edge_in_flight=0,
+                 cloud_in_flight=0):
+        # accumulated_generation of the finished round is added right after
+        # finish_generation: fold the pending increments into the log first
+        open_fg: dict = {}
+        for e in log:
+            if e["k"] == "fg" and "c" not in e:
+                open_fg.setdefault(e["t"], []).append(e)
+        for tid, es in open_fg.items():
+            nxt = [x["g0"] for x in es[1:]] + [states[tid].accumulated_generation]
+            for e, g1 in zip(es, nxt):
+                e["c"] = g1 - e.pop("g0")
+        pending = list(pending)
+        entry = {"k": "plan", "now": now, "eif": edge_in_flight, "cif": cloud_in_flight,
+                 "pending": [req_json(r) for r in pending]}
+        d = ref_plan(pending, states, edge, cloud, net, now, cfg, edge_in_flight=edge_in_flight,
+                     cloud_in_flight=cloud_in_flight)
+        entry["exp"] = {"edge": [r.task_id for r in d.edge], "cloud": [r.task_id for r in d.cloud],
+                        "deferred": [[r.task_id, r.skipped] for r in d.deferred],
+                        "refetch": sorted(d.refetch_task_ids)}
+        log.append(entry)
+        return d
+
+    prof = lambda e: None if e is None else {"tier": e.tier, "capacity": e.capacity,
+                                              "max_batch": e.max_batch, "points": list(e.points)}
+    netj = lambda n: None if n is None else {"base_latency_us": n.base_latency_us,
+                                             "uplink_bps": n.uplink_bps,
+                                             "downlink_bps": n.downlink_bps}
+    edge = EngineProfile(tier="edge", capacity=4, max_batch=4,
+                         points=((1, 120_000), (2, 150_000), (4, 210_000)))
+    cloud = EngineProfile(tier="cloud", capacity=8, max_batch=8,
+                          points=((1, 60_000), (4, 80_000), (8, 110_000)))
+    wan = NetworkModel(base_latency_us=40_000, uplink_bps=50_000_000, downlink_bps=200_000_000)
+    lan = NetworkModel(base_latency_us=2_000, uplink_bps=400_000_000, downlink_bps=800_000_000)
+    scenarios = [
+        ("kairos-edge", scheduler.SchedulerConfig(), edge, None, None, None, 36, 12, "event"),
+        ("kairos-hybrid", scheduler.SchedulerConfig(stale_threshold=100_000), edge, cloud, wan,
+         lan, 48, 16, "event"),
+        ("fifo-edge", scheduler.SchedulerConfig(policy="fifo"), edge, None, None, None, 30, 10,
+         "event"),
+        ("las-hybrid", scheduler.SchedulerConfig(policy="las", buckets=4, aging_interval=2),
+         edge, cloud, wan, None, 30, 10, "event"),
+        ("kairos-interval", scheduler.SchedulerConfig(buckets=16, aging_interval=3), edge, None,
+         None, None, 30, 12, "interval"),
+    ]
+    out = []
+    old_state, old_plan = rsim.TaskState, rsim.plan
+    rsim.TaskState, rsim.plan = RecState, rec_plan
+    try:
+        for i, (name, scfg, e, c, net, enet, ntr, slots, mode) in enumerate(scenarios):
+            log.clear()
+            spec = SyntheticSpec(action_budget=160, uncertain_fraction=0.3)
+            traces = synthesize_family(spec, horizon.HorizonPolicyConfig.confidence(0.4, 5),
+                                       gen_latency=150_000, count=ntr, seed=100 + i)
+            cfg = rsim.SimConfig(scheduler=scfg, edge=e, cloud=c, network=net, edge_network=enet,
+                                 plan_mode=mode, plan_interval_us=40_000)
+            rsim.run_fleet(traces, slots, cfg)
+            for ev in log:  # increments after the last plan() never reach a decision
+                if ev.pop("g0", None) is not None:
+                    ev["c"] = 0
+            out.append({"name": name, "policy": scfg.policy, "buckets": scfg.buckets,
+                        "aging_interval": scfg.aging_interval,
+                        "stale_threshold": scfg.stale_threshold,
+                        "default_exec_estimate": scfg.default_exec_estimate,
+                        "edge": prof(e), "cloud": prof(c), "net": netj(net),
+                        "log": list(log)})
+    finally:
+        rsim.TaskState, rsim.plan = old_state, old_plan
+    return out
+
+
 def main():
     if sys.argv[1:] == ["sweep"]:  # only the threshold-sweep fixture
         save_sweep(gen_sweep(np.random.default_rng(11)))
+        return
+    if sys.argv[1:] == ["sim"]:  # only the simulator replay fixture
+        (OUT / "sim_replay.json").write_text(json.dumps(gen_sim(), separators=(",", ":")))
         return
     rng = np.random.default_rng(20260517)
     save_confidence(gen_confidence(rng))
@@ -408,6 +516,7 @@ def main():
                                                     separators=(",", ":")))
     (OUT / "fig4.json").write_text(json.dumps(gen_fig4(), indent=1))
     save_sweep(gen_sweep(np.random.default_rng(11)))
+    (OUT / "sim_replay.json").write_text(json.dumps(gen_sim(), separators=(",", ":")))
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".npz", ".json"):
             print(f"{p.name:28s} {p.stat().st_size:>9d} B")

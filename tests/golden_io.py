@@ -101,3 +101,45 @@ def ns_objects(inst):
 
 def plan_cloud_instances():
     return json.loads((GOLDEN / "plan_cloud.json").read_text())
+
+
+def sim_scenarios():
+    return json.loads((GOLDEN / "sim_replay.json").read_text())
+
+
+def replay_log(scenario):
+    """Walk a recorded simulator log: yields ("event", entry) for every
+    TaskState mutation and ("plan", entry, states) at each plan() call, with
+    `states` the duck-typed task states (SimpleNamespace) as of that call."""
+    from types import SimpleNamespace as NS
+    states = {}
+    for e in scenario["log"]:
+        k = e["k"]
+        if k == "plan":
+            yield "plan", e, states
+            continue
+        if k == "new":
+            states[e["t"]] = NS(task_id=e["t"], t_start=e["a"], skipped=0,
+                                accumulated_generation=0, gen_starts=[], gen_ends=[],
+                                exec_intervals=[])
+        else:
+            st = states[e["t"]]
+            if k == "bg":
+                st.gen_starts.append(e["a"])
+                st.gen_ends.append(None)
+            elif k == "fg":
+                st.gen_ends[e["j"]] = e["a"]
+                st.accumulated_generation += e["c"]
+            elif k == "rx":
+                st.exec_intervals.append(NS(start=e["a"], end=e["b"]))
+        yield "event", e, states
+
+
+def pending_objects(entry):
+    from types import SimpleNamespace as NS
+    return [NS(task_id=r["task_id"], round_id=r["round_id"], issued_at=r["issued_at"],
+               obs_captured_at=r["obs_captured_at"], payload_bytes=r["payload_bytes"],
+               skipped=r["skipped"],
+               last_exec_info=NS(exec_start=r["last_exec_info"][0],
+                                 remaining_actions=r["last_exec_info"][1]))
+            for r in entry["pending"]]

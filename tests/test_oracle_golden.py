@@ -162,6 +162,34 @@ def test_plan_cloud_golden():
         assert {t: int(res["skipped_out"][i]) for i, t in enumerate(ids)} == exp["skipped_after"], ii
 
 
+def test_sim_replay_golden():
+    """Every plan() decision of five reference simulator runs (edge-only and
+    hybrid, kairos / fifo / las, event-driven and fixed-interval planning),
+    re-derived by the oracle from the recorded TaskState history."""
+    n = 0
+    for sc in golden_io.sim_scenarios():
+        for kind, e, states in golden_io.replay_log(sc):
+            if kind != "plan":
+                continue
+            pending = golden_io.pending_objects(e)
+            fleet = orc.fleet_from_objects(pending, states)
+            res = orc.plan_tiers(fleet, [r.payload_bytes for r in pending], sc["policy"],
+                                 sc["buckets"], sc["aging_interval"], sc["stale_threshold"],
+                                 sc["default_exec_estimate"], e["now"], sc["edge"], sc["cloud"],
+                                 sc["net"], e["eif"], e["cif"])
+            ids = [r.task_id for r in pending]
+            order = [ids[i] for i in res["order"]]
+            exp = e["exp"]
+            assert order[:res["n_edge"]] == exp["edge"], (sc["name"], n)
+            assert [ids[i] for i in res["cloud_order"]] == exp["cloud"], (sc["name"], n)
+            deferred = [[ids[i], int(res["skipped_out"][i])] for i in res["order"][res["n_edge"]:]
+                        if res["tier"][i] == 0]
+            assert deferred == exp["deferred"], (sc["name"], n)
+            assert sorted(ids[i] for i in np.nonzero(res["refetch"])[0]) == exp["refetch"]
+            n += 1
+    assert n > 700
+
+
 def test_engine_model_goldens():
     # reference tests/test_engines.py: interpolation 166,667; transfer 110,000; round trip 352,400
     prof = {"capacity": 4, "max_batch": 4, "points": [[1, 150_000], [4, 200_000]]}

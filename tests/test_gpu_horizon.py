@@ -106,7 +106,8 @@ def test_divergence_golden(kb):
 
 @pytest.mark.parametrize("R,S,Lp,Lc,D", [(1024, 1, 50, 50, 7), (300, 1, 64, 64, 32),
                                          (130, 8, 50, 50, 7), (77, 3, 20, 16, 5),
-                                         (65, 2, 40, 40, 48), (33, 1, 10, 10, 16)])
+                                         (65, 2, 40, 40, 48), (33, 1, 10, 10, 16),
+                                         (700, 4, 64, 64, 32), (5000, 8, 50, 50, 7)])
 def test_divergence_random_vs_oracle(kb, R, S, Lp, Lc, D):
     from paper_2605_11381_b200.divergence import round_optimal_horizon_batch
     rng = np.random.default_rng(R + S + D)

@@ -22,6 +22,7 @@
  *   kr_ledger_apply         core.py:200-229 + waiting.py:69-93  incremental TaskState
  *                           history and running wait totals (sim.py:358-440 mutations)
  *   kr_urgency_ledger       kr_urgency over the device-resident ledger (O(1) per request)
+ *   kr_trace_parse / _load  workload.py:163-262  JSONL task traces -> columns (host code)
  *   kr_transfer_time        engines.py:158-169   per-request uplink time
  *   kr_place_cloud          scheduler.py:160-234 phase-3 cloud offload scan
  *
@@ -56,6 +57,7 @@ typedef enum {
     KR_EINVAL = 1,     /* bad shape / argument (host-side check) */
     KR_ECUDA = 2,      /* CUDA launch / runtime error */
     KR_ENOSPACE = 3,   /* workspace too small */
+    KR_EFORMAT = 4,    /* malformed trace file (kr_trace_*: details in the columns' err_*) */
 } kr_status;
 
 enum { KR_F32 = 0, KR_F64 = 1 };
@@ -266,6 +268,49 @@ KR_API int kr_place_cloud(const int32_t* order, int64_t n, int64_t n_edge, const
                           const int64_t* thresholds, int64_t cap, const kr_fleet* fleet,
                           const kr_sched* cfg, uint8_t* refetch, int32_t* cloud_idx,
                           int32_t* n_cloud, void* stream);
+
+/* ---- trace ingest (host code): JSON Lines task traces -> columns -------- */
+
+/* Columnar view of a parsed trace file (workload.py:60-262 TaskTrace /
+ * RoundRecord).  All pointers are host memory owned by the table. */
+typedef struct kr_trace_columns {
+    int64_t n_traces, n_rounds, n_mag_values, n_traj_rows, n_traj_values;
+    const int64_t* round_off;            /* [n_traces + 1] rounds of trace i            */
+    const char* ids;                     /* task ids, UTF-8, concatenated               */
+    const int64_t* id_off;               /* [n_traces + 1]                               */
+    const double* control_hz;            /* [n_traces]                                   */
+    const uint8_t* control_hz_is_int;    /* [n_traces] the JSON literal was an integer   */
+    const int64_t* obs_payload_bytes;    /* [n_traces]                                   */
+    const int64_t* action_payload_bytes; /* [n_traces]                                   */
+    const uint8_t* success;              /* [n_traces] bool(value)                       */
+    const int32_t* round_id;             /* [n_rounds]                                   */
+    const int32_t* trigger_action_index; /* [n_rounds]                                   */
+    const int32_t* horizon;              /* [n_rounds]                                   */
+    const int32_t* chunk_size;           /* [n_rounds]                                   */
+    const int32_t* mag_k;                /* [n_rounds] K of update_magnitudes (0: none)  */
+    const int32_t* mag_n;                /* [n_rounds] N                                 */
+    const int64_t* mag_off;              /* [n_rounds + 1] offsets into mags (values)    */
+    const double* mags;                  /* K x N row-major per round, concatenated      */
+    const int32_t* traj_rows;            /* [n_rounds] rows of action_trajectory (-1: none) */
+    const int64_t* traj_row0;            /* [n_rounds + 1] first row of each round       */
+    const int64_t* traj_off;             /* [n_traj_rows + 1] offsets into traj (values) */
+    const double* traj;
+    /* KR_EFORMAT: TraceFormatError fields (workload.py:29-54) */
+    int64_t err_line;
+    int32_t err_has_task, err_has_round;
+    const char* err_task;
+    int64_t err_round;
+    const char* err_message;
+} kr_trace_columns;
+
+/* Parse JSON Lines (load_traces semantics: stripped lines, blanks skipped,
+ * the reference's validation order and messages).  *table is always set
+ * (free it with kr_trace_free); KR_EFORMAT leaves the traces before the bad
+ * line in the columns and the error in err_*. */
+KR_API int kr_trace_parse(const char* buf, size_t len, int64_t first_line, void** table);
+KR_API int kr_trace_load(const char* path, void** table);
+KR_API const kr_trace_columns* kr_trace_columns_of(const void* table);
+KR_API void kr_trace_free(void* table);
 
 /* Full argsort of n unique keys (ascending).  Synchronises `stream` once
  * when n exceeds the single-CTA limit (pass plan read back to the host). */

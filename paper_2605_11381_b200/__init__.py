@@ -27,6 +27,9 @@ from .horizon import (HorizonPolicyConfig, UpdateMagnitudes, decide_horizon,  # 
                       decide_horizon_batch, sweep_horizon_sums, sweep_thresholds)
 from .scheduler import (DispatchPlan, SchedulerConfig, assign_bucket,  # noqa: F401
                         estimate_exec_latency, order_within_bucket, plan, plan_fifo, plan_las)
+from .traces import (RoundRecord, TaskTrace, TraceColumns, TraceFormatError,  # noqa: F401
+                     load_trace_columns, load_trace_dir, load_traces, pareto_rows, store_traces,
+                     trace_from_dict, trace_to_dict)
 from .waiting import (WaitLedger, current_wait_ratio, ledger_from_history,  # noqa: F401
                       round_wait, wait_ratio)
 

@@ -16,7 +16,7 @@ import torch
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libkairos_b200.so"
 
-KR_OK, KR_EINVAL, KR_ECUDA, KR_ENOSPACE = 0, 1, 2, 3
+KR_OK, KR_EINVAL, KR_ECUDA, KR_ENOSPACE, KR_EFORMAT = 0, 1, 2, 3, 4
 KR_F32, KR_F64 = 0, 1
 KR_KAIROS, KR_FIFO, KR_LAS = 0, 1, 2
 
@@ -69,6 +69,21 @@ class KrRequests(ctypes.Structure):
         "task", "issued_at", "obs_captured_at", "accum_gen", "remaining", "lexrank", "skipped")]
 
 
+class KrTraceColumns(ctypes.Structure):
+    """kr_trace_columns: columnar view of a parsed trace file (host memory)."""
+
+    _fields_ = ([(k, _i64) for k in ("n_traces", "n_rounds", "n_mag_values", "n_traj_rows",
+                                      "n_traj_values")] +
+                [(k, _vp) for k in (
+                    "round_off", "ids", "id_off", "control_hz", "control_hz_is_int",
+                    "obs_payload_bytes", "action_payload_bytes", "success", "round_id",
+                    "trigger_action_index", "horizon", "chunk_size", "mag_k", "mag_n", "mag_off",
+                    "mags", "traj_rows", "traj_row0", "traj_off", "traj")] +
+                [("err_line", _i64), ("err_has_task", _i32), ("err_has_round", _i32),
+                 ("err_task", ctypes.c_char_p), ("err_round", _i64),
+                 ("err_message", ctypes.c_char_p)])
+
+
 _SIGNATURES = {
     "kr_version": (ctypes.c_char_p, []),
     "kr_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -102,6 +117,11 @@ _SIGNATURES = {
                                 ctypes.c_size_t, _vp]),
     "kr_sort_keys": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "kr_transfer_time": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    "kr_trace_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, _i64,
+                                      ctypes.POINTER(_vp)]),
+    "kr_trace_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "kr_trace_columns_of": (ctypes.POINTER(KrTraceColumns), [_vp]),
+    "kr_trace_free": (None, [_vp]),
     "kr_place_cloud": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, ctypes.POINTER(KrFleet),
                                       ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp]),
 }

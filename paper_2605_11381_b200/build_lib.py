@@ -21,7 +21,7 @@ INCLUDE = PKG.parent / "include"
 OUT = PKG / "libkairos_b200.so"
 OBJ = PKG / "build"
 
-SOURCES = ["kr_capi.cu", "kr_horizon.cu", "kr_urgency.cu", "kr_select.cu"]
+SOURCES = ["kr_capi.cu", "kr_horizon.cu", "kr_urgency.cu", "kr_select.cu", "kr_ingest.cpp"]
 HEADERS = ["kr_common.cuh", "kr_host.cuh", "kr_stream.cuh"]
 
 NVCC_FLAGS = [

@@ -51,6 +51,7 @@ extern "C" const char* kr_status_string(int status) {
         case KR_EINVAL: return "invalid argument";
         case KR_ECUDA: return "CUDA error";
         case KR_ENOSPACE: return "workspace too small";
+        case KR_EFORMAT: return "malformed trace data";
         default: return "unknown status";
     }
 }

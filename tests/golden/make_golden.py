@@ -500,7 +500,98 @@ def gen_sim():
     return out
 
 
+# --- trace ingest + pareto (workload.py:163-262, cli.py:104-140) ------------
+
+def gen_traces():
+    """Trace files written by the reference's store_traces, the reference's
+    `roboserve pareto` CSV over them, and malformed variants with the
+    reference load_traces' TraceFormatError fields."""
+    import copy
+    import tempfile
+
+    from roboserve import cli
+    from roboserve.workload import SyntheticSpec, synthesize_family
+
+    tdir = OUT / "traces"
+    tdir.mkdir(exist_ok=True)
+    conf = horizon.HorizonPolicyConfig.confidence(0.4, 5)
+    fams = [
+        ("a_arms.jsonl", SyntheticSpec(chunk_size=16, diffusion_steps=6, action_budget=60,
+                                       success_rate=0.7), 6, True),
+        ("b_humanoid.jsonl", SyntheticSpec(chunk_size=32, diffusion_steps=10, control_hz=50.0,
+                                           action_budget=80, uncertain_fraction=0.35), 5, False),
+        ("c_mixed.jsonl", SyntheticSpec(chunk_size=16, diffusion_steps=6, action_budget=40,
+                                        control_hz=29.97, bump_factor=2.5), 4, True),
+    ]
+    for i, (name, spec, count, traj) in enumerate(fams):
+        fam = synthesize_family(spec, conf, gen_latency=80_000, count=count, seed=300 + i,
+                                id_prefix=name[0], with_trajectories=traj, trajectory_dim=3)
+        workload.store_traces(fam, tdir / name)
+    pareto = {}
+    with tempfile.TemporaryDirectory() as td:
+        for key, args in (("default", []),
+                          ("custom", ["--static-grid", "1,7,16,40", "--threshold-grid",
+                                      "0,0.05,0.4,0.8,1.5,2.5", "--h-min", "3"])):
+            out = Path(td) / f"{key}.csv"
+            with contextlib.redirect_stdout(io.StringIO()):
+                rc = cli.main(["pareto", "--traces", str(tdir), "--out", str(out), *args])
+            assert rc == 0
+            pareto[key] = {"args": args, "csv": out.read_text()}
+    # malformed variants of one valid trace line
+    base = workload.trace_to_dict(workload.load_traces(tdir / "a_arms.jsonl")[0])
+    def mut(f):
+        d = copy.deepcopy(base)
+        f(d)
+        return json.dumps(d, separators=(",", ":"))
+    good = json.dumps(base, separators=(",", ":"))
+    texts = {
+        "broken_json": good + "\n{broken\n",
+        "not_object": "\n\n[1, 2]\n",
+        "extra_data": good + " 7\n",
+        "missing_control_hz": mut(lambda d: d.pop("control_hz")),
+        "missing_rounds": mut(lambda d: d.pop("rounds")),
+        "missing_round_field": mut(lambda d: d["rounds"][1].pop("horizon")),
+        "horizon_bounds": mut(lambda d: d["rounds"][0].__setitem__("horizon", 99)),
+        "horizon_zero": mut(lambda d: d["rounds"][1].__setitem__("horizon", 0)),
+        "neg_round_id": mut(lambda d: d["rounds"][0].__setitem__("round_id", -1)),
+        "neg_trigger": mut(lambda d: d["rounds"][1].__setitem__("trigger_action_index", -2)),
+        "noncontiguous": mut(lambda d: d["rounds"][1].__setitem__("round_id", 5)),
+        "trigger_bound": mut(lambda d: d["rounds"][1].__setitem__(
+            "trigger_action_index", d["rounds"][0]["horizon"])),
+        "no_rounds": mut(lambda d: d.__setitem__("rounds", [])),
+        "zero_hz": mut(lambda d: d.__setitem__("control_hz", 0)),
+        "neg_payload": mut(lambda d: d.__setitem__("obs_payload_bytes", -1)),
+        "empty_task": mut(lambda d: d.__setitem__("task_id", "")),
+        "neg_magnitude": mut(lambda d: d["rounds"][0]["update_magnitudes"][1].__setitem__(2, -0.5)),
+        "nan_magnitude": mut(lambda d: d["rounds"][1]["update_magnitudes"][0].__setitem__(
+            0, float("nan"))),
+        "one_d_magnitudes": mut(lambda d: d["rounds"][0].__setitem__("update_magnitudes", [1.0, 2.0])),
+        "k1_magnitudes": mut(lambda d: d["rounds"][0].__setitem__("update_magnitudes", [[1.0, 2.0]])),
+        "empty_magnitudes": mut(lambda d: d["rounds"][0].__setitem__("update_magnitudes", [])),
+        "three_d": mut(lambda d: d["rounds"][0].__setitem__("update_magnitudes", [[[1.0]], [[2.0]]])),
+        "blank_lines_ok": "\n  \n" + good + "\n\n" + good.replace('"a-0000"', '"a-9999"') + "\n",
+        "second_line_bad": good + "\n" + mut(lambda d: d.__setitem__("success", None)).replace(
+            '"round_id":0', '"round_id":3', 1) + "\n",
+    }
+    errors = []
+    with tempfile.TemporaryDirectory() as td:
+        for name, text in texts.items():
+            f = Path(td) / "x.jsonl"
+            f.write_text(text)
+            try:
+                loaded = workload.load_traces(f)
+                errors.append({"name": name, "text": text, "ok": [workload.trace_to_dict(t) for t in loaded]})
+            except workload.TraceFormatError as e:
+                errors.append({"name": name, "text": text, "error": str(e), "raw": e.raw_message,
+                               "line": e.line, "task_id": e.task_id, "round_id": e.round_id})
+    (OUT / "traces_expected.json").write_text(json.dumps({"pareto": pareto, "cases": errors},
+                                                         indent=0))
+
+
 def main():
+    if sys.argv[1:] == ["traces"]:  # only the trace-ingest fixtures
+        gen_traces()
+        return
     if sys.argv[1:] == ["sweep"]:  # only the threshold-sweep fixture
         save_sweep(gen_sweep(np.random.default_rng(11)))
         return
@@ -517,6 +608,7 @@ def main():
     (OUT / "fig4.json").write_text(json.dumps(gen_fig4(), indent=1))
     save_sweep(gen_sweep(np.random.default_rng(11)))
     (OUT / "sim_replay.json").write_text(json.dumps(gen_sim(), separators=(",", ":")))
+    gen_traces()
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".npz", ".json"):
             print(f"{p.name:28s} {p.stat().st_size:>9d} B")

@@ -143,3 +143,10 @@ def pending_objects(entry):
                last_exec_info=NS(exec_start=r["last_exec_info"][0],
                                  remaining_actions=r["last_exec_info"][1]))
             for r in entry["pending"]]
+
+
+TRACES_DIR = GOLDEN / "traces"
+
+
+def traces_expected():
+    return json.loads((GOLDEN / "traces_expected.json").read_text())

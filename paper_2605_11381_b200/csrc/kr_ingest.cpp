@@ -11,12 +11,14 @@
 //
 // Host code only (no CUDA); compiled into libkairos_b200.so.
 #include <cerrno>
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/kairos_b200.h"
@@ -32,6 +34,8 @@ struct JVal {
     double d = 0.0;      // Float, or Int converted
     std::string s;       // Str
     std::vector<JVal> a;  // Arr elements / Obj values
+    std::vector<double> nums;  // Arr of numbers only (the bulk payload): values, no DOM nodes
+    bool numeric = false;      // Arr stored in `nums`
     std::vector<std::string> keys;  // Obj keys (duplicate keys: the last wins, as in Python)
 
     const JVal* get(const char* k) const {
@@ -46,7 +50,7 @@ struct JVal {
             case Int: return big ? d != 0.0 : i != 0;
             case Float: return d != 0.0;
             case Str: return !s.empty();
-            case Arr: return !a.empty();
+            case Arr: return numeric ? !nums.empty() : !a.empty();
             case Obj: return !a.empty();
         }
         return false;
@@ -129,18 +133,42 @@ class Reader {
                 while (p_ < e_ && *p_ >= '0' && *p_ <= '9') p_++;
             }
         }
-        std::string tok(s, p_);
+        // from_chars: correctly rounded like float(str), no allocation
+        std::from_chars(s, p_, v.d, std::chars_format::general);
         if (is_float) {
             v.kind = JVal::Float;
-            v.d = std::strtod(tok.c_str(), nullptr);  // correctly rounded, as float(str)
         } else {
             v.kind = JVal::Int;
-            errno = 0;
-            long long x = std::strtoll(tok.c_str(), nullptr, 10);
-            v.big = errno == ERANGE;
+            long long x = 0;
+            auto r = std::from_chars(s, p_, x);
+            v.big = r.ec == std::errc::result_out_of_range;
             v.i = x;
-            v.d = std::strtod(tok.c_str(), nullptr);
         }
+    }
+    // a bare number literal (no NaN / Infinity) at the cursor, as a double
+    bool fast_number(double& d) {
+        const char* s = p_;
+        const char* q = p_;
+        if (q < e_ && *q == '-') q++;
+        if (q >= e_ || !(*q >= '0' && *q <= '9')) return false;
+        if (*q == '0') q++;
+        else
+            while (q < e_ && *q >= '0' && *q <= '9') q++;
+        if (q < e_ && *q == '.' && q + 1 < e_ && q[1] >= '0' && q[1] <= '9') {
+            q++;
+            while (q < e_ && *q >= '0' && *q <= '9') q++;
+        }
+        if (q < e_ && (*q == 'e' || *q == 'E')) {
+            const char* t = q + 1;
+            if (t < e_ && (*t == '+' || *t == '-')) t++;
+            if (t < e_ && *t >= '0' && *t <= '9') {
+                q = t;
+                while (q < e_ && *q >= '0' && *q <= '9') q++;
+            }
+        }
+        std::from_chars(s, q, d, std::chars_format::general);
+        p_ = q;
+        return true;
     }
     static void put_utf8(std::string& o, uint32_t cp) {
         if (cp < 0x80) {
@@ -218,6 +246,26 @@ class Reader {
         if (p_ < e_ && *p_ == ']') {
             p_++;
             return;
+        }
+        // arrays of plain numbers (magnitude / trajectory rows) skip the DOM
+        const char* start = p_;
+        double d;
+        if (fast_number(d)) {
+            v.numeric = true;
+            v.nums.push_back(d);
+            for (;;) {
+                ws();
+                if (p_ < e_ && *p_ == ']') { p_++; return; }
+                if (p_ < e_ && *p_ == ',') {
+                    p_++;
+                    ws();
+                    if (fast_number(d)) { v.nums.push_back(d); continue; }
+                }
+                break;  // something else: re-parse generically
+            }
+            v.numeric = false;
+            v.nums.clear();
+            p_ = start;
         }
         for (;;) {
             ws();
@@ -310,12 +358,14 @@ int64_t need_int(const JVal& v, const char* name) {
 }
 
 // UpdateMagnitudes(np.asarray(data)) (horizon.py:26-61): shape, then checks.
+size_t arr_len(const JVal& v) { return v.numeric ? v.nums.size() : v.a.size(); }
+
 void parse_mags(const JVal& v, Table& t, int32_t& K, int32_t& N) {
     std::vector<int64_t> shape;
     const JVal* cur = &v;
     while (cur->kind == JVal::Arr) {  // numpy's shape discovery along the first elements
-        shape.push_back(static_cast<int64_t>(cur->a.size()));
-        if (cur->a.empty()) break;
+        shape.push_back(static_cast<int64_t>(arr_len(*cur)));
+        if (cur->numeric || cur->a.empty()) break;
         cur = &cur->a[0];
     }
     auto shape_str = [&]() {
@@ -330,12 +380,13 @@ void parse_mags(const JVal& v, Table& t, int32_t& K, int32_t& N) {
     // rectangular check for the 2-D case (ragged / non-numeric: numpy's own error)
     if (shape.size() == 2) {
         for (const JVal& row : v.a) {
-            if (row.kind != JVal::Arr || static_cast<int64_t>(row.a.size()) != shape[1])
+            if (row.kind != JVal::Arr || static_cast<int64_t>(arr_len(row)) != shape[1])
                 throw FormatError{"bad update_magnitudes: the update magnitudes are not a "
                                   "rectangular array"};
-            for (const JVal& x : row.a)
-                if (!x.is_num())
-                    throw FormatError{"bad update_magnitudes: non-numeric update magnitude"};
+            if (!row.numeric)
+                for (const JVal& x : row.a)
+                    if (!x.is_num())
+                        throw FormatError{"bad update_magnitudes: non-numeric update magnitude"};
         }
     }
     if (shape.size() != 2)
@@ -345,19 +396,23 @@ void parse_mags(const JVal& v, Table& t, int32_t& K, int32_t& N) {
         throw FormatError{"bad update_magnitudes: need at least 2 refinement steps, got " +
                           py_int(shape[0])};
     if (shape[1] < 1) throw FormatError{"bad update_magnitudes: chunk size must be >= 1"};
+    const size_t m0 = t.mags.size();
+    for (const JVal& row : v.a) {
+        if (row.numeric) t.mags.insert(t.mags.end(), row.nums.begin(), row.nums.end());
+        else
+            for (const JVal& x : row.a) t.mags.push_back(x.num());
+    }
     bool finite = true, nonneg = true;
-    for (const JVal& row : v.a)
-        for (const JVal& x : row.a) {
-            double d = x.num();
-            finite = finite && std::isfinite(d);
-            nonneg = nonneg && !(d < 0);
-        }
+    for (size_t k = m0; k < t.mags.size(); k++) {
+        const double d = t.mags[k];
+        finite = finite && std::isfinite(d);
+        nonneg = nonneg && !(d < 0);
+    }
+    if (!finite || !nonneg) t.mags.resize(m0);
     if (!finite) throw FormatError{"bad update_magnitudes: update magnitudes must be finite"};
     if (!nonneg) throw FormatError{"bad update_magnitudes: update magnitudes must be >= 0"};
     K = static_cast<int32_t>(shape[0]);
     N = static_cast<int32_t>(shape[1]);
-    for (const JVal& row : v.a)
-        for (const JVal& x : row.a) t.mags.push_back(x.num());
 }
 
 void add_trace(const JVal& d, Table& t) {
@@ -379,6 +434,7 @@ void add_trace(const JVal& d, Table& t) {
     };
     const JVal& rounds = *d.get("rounds");
     if (rounds.kind != JVal::Arr) throw with_task(FormatError{"rounds must be a list"});
+    if (rounds.numeric) throw with_task(FormatError{"round must be a JSON object"});
     // snapshot for rollback of this trace's rows on error
     const size_t r0 = t.round_id.size();
     const size_t m0 = t.mags.size(), tr0 = t.traj.size(), tro0 = t.traj_off.size();
@@ -403,12 +459,17 @@ void add_trace(const JVal& d, Table& t) {
             const JVal* tj = r.get("action_trajectory");
             if (tj && tj->kind != JVal::Null) {
                 if (tj->kind != JVal::Arr) throw FormatError{"action_trajectory must be a list"};
+                if (tj->numeric) throw FormatError{"action_trajectory rows must be lists"};
                 rows = static_cast<int32_t>(tj->a.size());
                 for (const JVal& row : tj->a) {
                     if (row.kind != JVal::Arr) throw FormatError{"action_trajectory rows must be lists"};
-                    for (const JVal& x : row.a) {
-                        if (!x.is_num()) throw FormatError{"non-numeric action_trajectory value"};
-                        t.traj.push_back(x.num());
+                    if (row.numeric) {
+                        t.traj.insert(t.traj.end(), row.nums.begin(), row.nums.end());
+                    } else {
+                        for (const JVal& x : row.a) {
+                            if (!x.is_num()) throw FormatError{"non-numeric action_trajectory value"};
+                            t.traj.push_back(x.num());
+                        }
                     }
                     t.traj_off.push_back(static_cast<int64_t>(t.traj.size()));
                 }
@@ -523,15 +584,11 @@ void finalize(Table& t) {
 
 }  // namespace
 
-extern "C" int kr_trace_parse(const char* buf, size_t len, int64_t first_line, void** table) {
-    if (!table || (!buf && len)) return KR_EINVAL;
-    Table* t = new (std::nothrow) Table();
-    if (!t) return KR_EINVAL;
-    *table = t;
-    int64_t line = first_line > 0 ? first_line : 1;
-    const char* p = buf;
-    const char* end = buf + len;
-    int status = KR_OK;
+namespace {
+
+// load_traces' loop (workload.py:233-250) over [p, end): stripped lines,
+// blanks skipped, the first error stops the range.
+int parse_range(const char* p, const char* end, int64_t line, Table& t) {
     while (p < end) {
         const char* nl = static_cast<const char*>(std::memchr(p, '\n', static_cast<size_t>(end - p)));
         const char* le = nl ? nl : end;
@@ -545,33 +602,124 @@ extern "C" int kr_trace_parse(const char* buf, size_t len, int64_t first_line, v
             try {
                 Reader(a, b).parse(v);
             } catch (JsonError& e) {
-                t->err = FormatError{"invalid JSON: " + e.msg};
-                t->err_line = line;
-                status = KR_EFORMAT;
-                break;
+                t.err = FormatError{"invalid JSON: " + e.msg};
+                t.err_line = line;
+                return KR_EFORMAT;
             }
             if (v.kind != JVal::Obj) {
-                t->err = FormatError{"trace line must be a JSON object"};
-                t->err_line = line;
-                status = KR_EFORMAT;
-                break;
+                t.err = FormatError{"trace line must be a JSON object"};
+                t.err_line = line;
+                return KR_EFORMAT;
             }
             try {
-                add_trace(v, *t);
+                add_trace(v, t);
             } catch (FormatError& e) {
-                t->err = e;
-                t->err_line = line;
-                status = KR_EFORMAT;
-                break;
+                t.err = e;
+                t.err_line = line;
+                return KR_EFORMAT;
             } catch (std::bad_alloc&) {
-                t->err = FormatError{"out of memory"};
-                t->err_line = line;
-                status = KR_EFORMAT;
-                break;
+                t.err = FormatError{"out of memory"};
+                t.err_line = line;
+                return KR_EFORMAT;
             }
         }
         line++;
         p = nl ? nl + 1 : end;
+    }
+    return KR_OK;
+}
+
+template <class V>
+void append_shifted(V& dst, const V& src, typename V::value_type shift) {  // offsets: skip src[0]
+    for (size_t k = 1; k < src.size(); k++) dst.push_back(src[k] + shift);
+}
+template <class V>
+void append(V& dst, const V& src) { dst.insert(dst.end(), src.begin(), src.end()); }
+
+void merge(Table& d, const Table& s) {
+    append_shifted(d.round_off, s.round_off, static_cast<int64_t>(d.round_id.size()));
+    append_shifted(d.id_off, s.id_off, static_cast<int64_t>(d.ids.size()));
+    append_shifted(d.mag_off, s.mag_off, static_cast<int64_t>(d.mags.size()));
+    append_shifted(d.traj_row0, s.traj_row0, static_cast<int64_t>(d.traj_off.size() - 1));
+    append_shifted(d.traj_off, s.traj_off, static_cast<int64_t>(d.traj.size()));
+    append(d.obs, s.obs); append(d.act, s.act); append(d.hz, s.hz); append(d.hz_int, s.hz_int);
+    append(d.success, s.success); d.ids += s.ids;
+    append(d.round_id, s.round_id); append(d.trigger, s.trigger); append(d.horizon, s.horizon);
+    append(d.chunk, s.chunk); append(d.mag_k, s.mag_k); append(d.mag_n, s.mag_n);
+    append(d.traj_rows, s.traj_rows); append(d.mags, s.mags); append(d.traj, s.traj);
+}
+
+int ingest_threads(size_t len) {
+    static const int env = std::getenv("KR_INGEST_THREADS") ? std::atoi(std::getenv("KR_INGEST_THREADS")) : 0;
+    int hw = static_cast<int>(std::thread::hardware_concurrency());
+    int n = env > 0 ? env : (hw > 0 ? hw : 1);
+    const int by_size = static_cast<int>(len >> 20) + 1;  // >= 1 MB per thread
+    return n < by_size ? n : by_size;
+}
+
+}  // namespace
+
+// Lines are independent, so the buffer is cut at line boundaries into one
+// range per host thread; the ranges' tables are concatenated in order, and the
+// first range that fails decides the error (as the sequential loop would).
+extern "C" int kr_trace_parse(const char* buf, size_t len, int64_t first_line, void** table) {
+    if (!table || (!buf && len)) return KR_EINVAL;
+    if (len == 0) buf = "";
+    Table* t = new (std::nothrow) Table();
+    if (!t) return KR_EINVAL;
+    *table = t;
+    const int64_t line0 = first_line > 0 ? first_line : 1;
+    const char* end = buf + len;
+    const int nt = ingest_threads(len);
+    if (nt <= 1) {
+        const int st = parse_range(buf, end, line0, *t);
+        finalize(*t);
+        return st;
+    }
+    std::vector<const char*> cut{buf};
+    for (int k = 1; k < nt; k++) {
+        const char* c = buf + len / nt * k;
+        if (c <= cut.back()) continue;
+        const char* nl = static_cast<const char*>(std::memchr(c, '\n', static_cast<size_t>(end - c)));
+        if (!nl) break;
+        cut.push_back(nl + 1);
+    }
+    cut.push_back(end);
+    const size_t nr = cut.size() - 1;
+    std::vector<Table> part(nr);
+    std::vector<int> st(nr, KR_OK);
+    std::vector<int64_t> lines(nr + 1, 0);
+    {
+        std::vector<std::thread> th;
+        for (size_t r = 0; r < nr; r++)
+            th.emplace_back([&, r] {
+                const char* q = cut[r];
+                int64_t n = 0;
+                while ((q = static_cast<const char*>(std::memchr(q, '\n', static_cast<size_t>(cut[r + 1] - q))))) {
+                    n++;
+                    q++;
+                }
+                lines[r + 1] = n;
+            });
+        for (auto& x : th) x.join();
+    }
+    lines[0] = line0;
+    for (size_t r = 1; r <= nr; r++) lines[r] += lines[r - 1];
+    {
+        std::vector<std::thread> th;
+        for (size_t r = 0; r < nr; r++)
+            th.emplace_back([&, r] { st[r] = parse_range(cut[r], cut[r + 1], lines[r], part[r]); });
+        for (auto& x : th) x.join();
+    }
+    int status = KR_OK;
+    for (size_t r = 0; r < nr; r++) {
+        merge(*t, part[r]);
+        if (st[r] != KR_OK) {
+            t->err = part[r].err;
+            t->err_line = part[r].err_line;
+            status = st[r];
+            break;
+        }
     }
     finalize(*t);
     return status;

@@ -84,3 +84,33 @@ def test_empty_and_roundtrip(tmp_path):
     q = tmp_path / "rt.jsonl"
     tr.store_traces(traces, q)
     assert q.read_text() == (golden_io.TRACES_DIR / "c_mixed.jsonl").read_text()
+
+
+def test_multithreaded_parse_order_and_first_error():
+    """A multi-MB buffer is split across host threads: traces come back in file
+    order, line numbers count across the cuts, and the earliest bad line wins."""
+    lines = [l for f in sorted(golden_io.TRACES_DIR.glob("*.jsonl"))
+             for l in f.read_text().splitlines() if l.strip()]
+    body = []
+    for i in range(400):
+        d = json.loads(lines[i % len(lines)])
+        d["task_id"] = f"task-{i:05d}"
+        body.append(json.dumps(d, separators=(",", ":")))
+        if i % 7 == 0:
+            body.append("   ")  # blank lines still count
+    text = "\n".join(body) + "\n"
+    assert len(text) > 4 << 20
+    cols = tr.parse_jsonl(text)
+    assert cols.task_ids == [f"task-{i:05d}" for i in range(400)]
+    assert [tr.trace_to_dict(t) for t in tr._objects(cols)] == \
+        [json.loads(b) for b in body if b.strip()]
+    # two bad lines in different thirds of the file: the first one is reported
+    bad = list(body)
+    i1, i2 = len(bad) // 3 + 5, 2 * len(bad) // 3
+    bad[i2] = "{broken"
+    bad[i1] = bad[i1].replace('"horizon":', '"horizon":0,"x":', 1)
+    d1 = json.loads(bad[i1])
+    with pytest.raises(tr.TraceFormatError) as info:
+        tr.parse_jsonl("\n".join(bad) + "\n")
+    assert info.value.line == i1 + 1
+    assert info.value.task_id == d1["task_id"]

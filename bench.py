@@ -218,7 +218,9 @@ def run_ours(args, world, rank, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    graphs = world == 1 and not args.no_graph
+    graphs = world == 1 and not args.no_graph and not args.eager
+    # N > 1 (or --eager): the same overlap eagerly (the NCCL all-gather stays outside graphs)
+    overlap = not graphs and args.reserve_sms > 0 and not args.no_graph
     n_cap0 = lib.kr_launch_count()
     if graphs:
         # CUDA graphs: horizons | urgency + admission, the latter on a side
@@ -228,6 +230,8 @@ def run_ours(args, world, rank, local_rank):
     for _ in range(args.warmup):
         if graphs:
             rnd.replay()
+        elif overlap:
+            rnd.run_overlapped(fleet, inputs, args.reserve_sms)
         else:
             rnd.run(fleet, inputs)
     barrier()
@@ -243,6 +247,9 @@ def run_ours(args, world, rank, local_rank):
         for i in range(args.steps):
             if graphs:
                 rnd.replay_concurrent(before_horizon=ev[i][0].record, after_horizon=ev[i][1].record)
+            elif overlap:
+                rnd.run_overlapped(fleet, inputs, args.reserve_sms, before_horizon=ev[i][0].record,
+                                   after_horizon=ev[i][1].record)
             else:
                 ev[i][0].record(stream)
                 rnd.horizons(inputs)
@@ -298,8 +305,9 @@ def run_ours(args, world, rank, local_rank):
         "kernels": breakdown,
         "gpu_launches": int(launches),
         "cuda_graphs": bool(graphs),
-        "concurrency": (f"urgency + admission on a side stream over {args.reserve_sms} SMs reserved "
-                        "from the horizon kernel" if graphs and args.reserve_sms > 0 else None),
+        "concurrency": (f"urgency + admission{' + NCCL candidate all-gather' if world > 1 else ''} "
+                        f"on a side stream over {args.reserve_sms} SMs reserved from the horizon "
+                        "kernel" if (graphs or overlap) and args.reserve_sms > 0 else None),
         "clocks": clk.summary(),
     }
     if e2e:
@@ -450,6 +458,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="N=1: the N>1 path (eager launches, side-stream overlap) instead of graphs")
     ap.add_argument("--reserve-sms", type=int, default=24,
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -166,6 +166,33 @@ class DecisionRound:
         self.replay_concurrent()
         return self.outputs()
 
+    def run_overlapped(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 24,
+                       before_horizon=None, after_horizon=None) -> RoundOutputs:
+        """One eager round with the graph path's overlap: the horizon kernel on
+        the current stream over all but `reserve_sms` SMs, urgency + admission
+        (for a sharded round: local select, the NCCL all-gather of candidates,
+        global select, local admission) on a side stream concurrently; the
+        current stream joins the side stream at the end.  The sharded round's
+        collective runs here because NCCL work stays outside CUDA graphs."""
+        n_sm = torch.cuda.get_device_properties(self.H.device).multi_processor_count
+        self.max_sms = 0 if reserve_sms <= 0 else max(1, n_sm - reserve_sms)
+        if getattr(self, "side", None) is None:
+            self.side = torch.cuda.Stream(device=self.H.device)
+        main = torch.cuda.current_stream()
+        fork = torch.cuda.Event()
+        fork.record(main)
+        if before_horizon:
+            before_horizon(main)
+        self.horizons(h)
+        if after_horizon:
+            after_horizon(main)
+        self.side.wait_event(fork)
+        with torch.cuda.stream(self.side):
+            self.urgency(fleet)
+            self.admit(fleet)
+        main.wait_stream(self.side)
+        return self.outputs()
+
 
 def sharded_topk(keys, n_local: int, k: int, sizes: list, ops, group=None):
     """Exact global top-k admission over robot-sharded keys (host protocol).

@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, sizes, k, q):
+def _worker(rank, world, port, sizes, k, q, overlap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -48,22 +48,34 @@ def _worker(rank, world, port, sizes, k, q):
         sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, base)
         fleet = fl.DeviceFleet.from_host(mine)
         rnd = rounds.ShardedDecisionRound(sizes[rank], k, sched)
-        rnd.urgency(fleet)
-        rnd.admit(fleet)
+        H = None
+        if overlap:  # the bench's N > 1 path: horizons || (urgency + sharded admission)
+            prev, cand, off = synthetic.chunks(sum(sizes), seed=22)
+            sl = slice(lo, lo + sizes[rank])
+            inputs = rounds.DivergenceInputs(prev[sl].contiguous(), cand[sl].contiguous(), 0.9,
+                                             offset=off[sl].contiguous())
+            rnd.run_overlapped(fleet, inputs, reserve_sms=24)
+            H = rnd.H.cpu().numpy()
+        else:
+            rnd.urgency(fleet)
+            rnd.admit(fleet)
         torch.cuda.synchronize()
         q.put((rank, rnd.admitted.cpu().numpy(), fleet.t["skipped"].cpu().numpy(),
-               rnd.global_edge[: rnd.k_global].cpu().numpy()))
+               rnd.global_edge[: rnd.k_global].cpu().numpy(), H))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sizes,k", [([30000, 20000], 4096), ([100, 5000], 300), ([2000, 2000], 3990)])
-def test_sharded_round_matches_single_gpu(sizes, k):
+@pytest.mark.parametrize("sizes,k,overlap", [([30000, 20000], 4096, False),
+                                             ([100, 5000], 300, False),
+                                             ([2000, 2000], 3990, False),
+                                             ([30000, 20000], 4096, True)])
+def test_sharded_round_matches_single_gpu(sizes, k, overlap):
     from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, len(sizes), port, sizes, k, q))
+    procs = [ctx.Process(target=_worker, args=(r, len(sizes), port, sizes, k, q, overlap))
              for r in range(len(sizes))]
     for p in procs:
         p.start()
@@ -76,9 +88,15 @@ def test_sharded_round_matches_single_gpu(sizes, k):
                             int(soa["issued_at"].min()))
     fleet = fl.DeviceFleet.from_host(soa)
     ref = rounds.DecisionRound(sum(sizes), k, sched)
-    ref.urgency(fleet)
-    ref.admit(fleet)
+    if overlap:
+        prev, cand, off = synthetic.chunks(sum(sizes), seed=22)
+        ref.run(fleet, rounds.DivergenceInputs(prev, cand, 0.9, offset=off))
+    else:
+        ref.urgency(fleet)
+        ref.admit(fleet)
     torch.cuda.synchronize()
+    if overlap:
+        assert np.array_equal(np.concatenate([r[4] for r in res]), ref.H.cpu().numpy())
     adm = np.concatenate([r[1] for r in res])
     skp = np.concatenate([r[2] for r in res])
     assert np.array_equal(adm, ref.admitted.cpu().numpy())

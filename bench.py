@@ -239,6 +239,8 @@ def run_ours(args, world, rank, local_rank):
     # timed region: K whole rounds; divergence kernel bracketed by events
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = lib.kr_launch_count()
     with ClockSampler(local_rank) as clk:
@@ -246,7 +248,8 @@ def run_ours(args, world, rank, local_rank):
         start.record(stream)
         for i in range(args.steps):
             if graphs:
-                rnd.replay_concurrent(before_horizon=ev[i][0].record, after_horizon=ev[i][1].record)
+                rnd.replay_concurrent(before_horizon=ev[i][0].record, after_horizon=ev[i][1].record,
+                                      before_side=sev[i][0].record, after_side=sev[i][1].record)
             elif overlap:
                 rnd.run_overlapped(fleet, inputs, args.reserve_sms, before_horizon=ev[i][0].record,
                                    after_horizon=ev[i][1].record)
@@ -280,6 +283,9 @@ def run_ours(args, world, rank, local_rank):
         gd[0].record(stream); rnd.g_decide.replay(); gd[1].record(stream)
         torch.cuda.synchronize()
         breakdown["urgency_plus_admission_graph_ms"] = gd[0].elapsed_time(gd[1])
+        if args.reserve_sms > 0:  # the side stream inside the timed rounds (concurrent)
+            breakdown["side_stream_ms_in_round"] = statistics.mean(
+                a.elapsed_time(b) for a, b in sev)
         breakdown["reserve_sms"] = args.reserve_sms
 
     e2e, e2e_cold = run_e2e(args, world, soa, prev, cand, off, sched) if not args.no_e2e else (None, None)

@@ -134,7 +134,8 @@ class DecisionRound:
             self.admit(fleet)
         self.side = torch.cuda.Stream(device=self.H.device) if reserve_sms > 0 else None
 
-    def replay_concurrent(self, before_horizon=None, after_horizon=None) -> None:
+    def replay_concurrent(self, before_horizon=None, after_horizon=None, before_side=None,
+                          after_side=None) -> None:
         """One round from the captured graphs.  With reserved SMs the horizon
         graph is launched first on the current stream and the urgency +
         admission graph on the side stream (ordered after all prior work of the
@@ -159,7 +160,11 @@ class DecisionRound:
             after_horizon(main)
         self.side.wait_event(fork)
         with torch.cuda.stream(self.side):
+            if before_side:
+                before_side(self.side)
             self.g_decide.replay()
+            if after_side:
+                after_side(self.side)
         main.wait_stream(self.side)
 
     def replay(self) -> RoundOutputs:

@@ -1,6 +1,7 @@
-for cfg in "0 0" "0 1" "0 2" "256 4" "384 2" "192 1"; do
+# sweep-kernel tile sweep (debug knobs KR_SWEEP_G / KR_SWEEP_TR), run under gpurun
+for cfg in "4 88" "4 48" "4 40" "4 24" "8 44" "8 24" "8 12"; do
   set -- $cfg
-  echo "max_threads=$1 min_rounds=$2"
-  KR_PLAN_MAX_THREADS=$1 KR_PLAN_MIN_ROUNDS=$2 KR_TRACE_PLAN=1 python profiles/prof_kernels.py sweep16 2>&1 | grep sweep | sort -u | head -2
-  KR_PLAN_MAX_THREADS=$1 KR_PLAN_MIN_ROUNDS=$2 python profiles/kernel_sweep.py 2>&1 | grep "sweep C=16 K"
+  echo "G=$1 TR=$2"
+  KR_SWEEP_G=$1 KR_SWEEP_TR=$2 KR_TRACE_PLAN=1 python profiles/prof_kernels.py sweep16 2>&1 | grep sweep | sort -u | head -2
+  KR_SWEEP_G=$1 KR_SWEEP_TR=$2 python profiles/kernel_sweep.py 2>&1 | grep "sweep C=16 K"
 done

@@ -319,6 +319,8 @@ def run_ours(args, world, rank, local_rank):
     if e2e:
         line["e2e"] = e2e
         line["e2e_cold"] = e2e_cold
+    if world == 1 and not args.no_configs:
+        line["other_configs"] = other_configs()
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
     print(json.dumps(line), flush=True)
@@ -342,6 +344,88 @@ def _timed(step, steps, world):
     if world > 1:
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
     return float(el.item())
+
+
+def other_configs(reps: int = 200):
+    """The other BASELINE.json configs on this GPU, each one whole decision
+    round (horizons + urgency + top-k admission) replayed as one CUDA graph.
+    configs[1] and [2] are L2-resident (labelled); configs[3] streams from HBM.
+    configs[0] (the paper's Fig. 4 scenario) is a correctness case
+    (tests/test_gpu_scheduler.py), configs[4] is the headline above."""
+    import torch
+    from paper_2605_11381_b200 import _lib, device as dev, fleet as fl, rounds, synthetic
+
+    lib = _lib.load()
+    out = {}
+
+    def div_into(Hslice, prev, cand, off):
+        R, Lp, D = prev.shape
+        S, Lc = cand.shape[1], cand.shape[2]
+        _lib.check(lib.kr_horizon_divergence(prev.data_ptr(), cand.data_ptr(), _lib.KR_F32, R, S,
+                                             Lp, Lc, D, off.data_ptr(), None, None, THR,
+                                             Hslice.data_ptr(), None, 0, dev.stream()),
+                   "kr_horizon_divergence")
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        for _ in range(10):
+            g.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / reps
+
+    def sched_for(soa):
+        return fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                               int(soa["issued_at"].min()))
+
+    # configs[1]: 1k robots, 50x7 @ 30 Hz, k = 64
+    R = 1024
+    soa = synthetic.fleet_soa(R, seed=11)
+    fleet = fl.DeviceFleet.from_host(soa)
+    prev, cand, off = synthetic.chunks(R, seed=12)
+    rnd = rounds.DecisionRound(R, 64, sched_for(soa))
+    inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
+    t = timed(lambda: rnd.run(fleet, inp))
+    out["configs[1] 1k robots 50x7 k=64"] = {
+        "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t, "l2": "resident (0.3 MB inputs)"}
+    # configs[2]: 16k mixed fleet, two homogeneous tensors, 64-step chunks, k = 1024
+    R = 16384
+    soa = synthetic.fleet_soa(R, seed=13)
+    fleet = fl.DeviceFleet.from_host(soa)
+    pa, ca, oa = synthetic.chunks(R // 2, seed=14, Lp=64, Lc=64, D=7)
+    ph, chh, oh = synthetic.chunks(R // 2, seed=15, Lp=64, Lc=64, D=32)
+    rnd = rounds.DecisionRound(R, 1024, sched_for(soa))
+
+    def mixed():
+        div_into(rnd.H[: R // 2], pa, ca, oa)
+        div_into(rnd.H[R // 2:], ph, chh, oh)
+        rnd.urgency(fleet)
+        rnd.admit(fleet)
+    t = timed(mixed)
+    out["configs[2] 16k mixed (8k arms 64x7 + 8k humanoids 64x32) k=1024"] = {
+        "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
+        "l2": "resident (85 MB inputs < 126 MB L2)"}
+    # configs[3]: 64k robots, 8-sample ensembles 50x7, k = 8192 (one GPU's whole fleet)
+    R = 65536
+    soa = synthetic.fleet_soa(R, seed=16)
+    fleet = fl.DeviceFleet.from_host(soa)
+    prev, cand, off = synthetic.chunks(R, seed=17, S=8)
+    rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
+    inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
+    t = timed(lambda: rnd.run(fleet, inp))
+    out["configs[3] 64k robots S=8 ensembles 50x7 k=8192"] = {
+        "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
+        "l2": "streams from HBM (826 MB inputs)"}
+    return out
 
 
 def run_e2e(args, world, soa, prev, cand, off, sched):
@@ -469,6 +553,8 @@ def main():
     ap.add_argument("--reserve-sms", type=int, default=24,
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other BASELINE configs' round latencies")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-robots", type=int, default=16384)
     args = ap.parse_args()

@@ -13,7 +13,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("R,k,S,D", [(1 << 15, 1024, 1, 7), (5000, 64, 8, 7), (3000, 300, 1, 32),
-                                     (777, 777, 1, 7), (1000, 0, 1, 7)])
+                                     (777, 777, 1, 7), (1000, 0, 1, 7), (1024, 64, 1, 7),
+                                     (4096, 4000, 1, 7)])
 def test_decision_round_vs_oracle(R, k, S, D):
     from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
     soa = synthetic.fleet_soa(R, seed=R + k)

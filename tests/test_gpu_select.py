@@ -86,7 +86,9 @@ def _skewed(n, rng, mode):
 @pytest.mark.parametrize("n,k,mode", [(1 << 20, 8192, "kairos"), (300000, 1024, "kairos"),
                                       (20000, 6000, "dense_low_bin"), (4096, 100, "few_bits"),
                                       (70000, 69999, "kairos"), (50, 49, "few_bits"),
-                                      (1 << 16, 1 << 15, "kairos")])
+                                      (1 << 16, 1 << 15, "kairos"), (2, 1, "kairos"),
+                                      (1024, 64, "kairos"), (4096, 4095, "few_bits"),
+                                      (4097, 4000, "kairos")])
 def test_select_admit_fused(n, k, mode):
     from paper_2605_11381_b200 import fleet as fl
     rng = np.random.default_rng(n + k)

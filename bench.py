@@ -225,13 +225,13 @@ def run_ours(args, world, rank, local_rank):
     if graphs:
         # CUDA graphs: horizons | urgency + admission, the latter on a side
         # stream over `reserve_sms` SMs left free by the horizon kernel
-        rnd.capture(fleet, inputs, reserve_sms=args.reserve_sms)
+        rnd.capture(fleet, inputs, reserve_sms=args.reserve_sms, layout=args.layout)
         per_round = (lib.kr_launch_count() - n_cap0) // 2  # warm-up run + capture
     for _ in range(args.warmup):
         if graphs:
             rnd.replay()
         elif overlap:
-            rnd.run_overlapped(fleet, inputs, args.reserve_sms)
+            rnd.run_overlapped(fleet, inputs, args.reserve_sms, layout=args.layout)
         else:
             rnd.run(fleet, inputs)
     barrier()
@@ -252,7 +252,7 @@ def run_ours(args, world, rank, local_rank):
                                       before_side=sev[i][0].record, after_side=sev[i][1].record)
             elif overlap:
                 rnd.run_overlapped(fleet, inputs, args.reserve_sms, before_horizon=ev[i][0].record,
-                                   after_horizon=ev[i][1].record)
+                                   after_horizon=ev[i][1].record, layout=args.layout)
             else:
                 ev[i][0].record(stream)
                 rnd.horizons(inputs)
@@ -287,6 +287,7 @@ def run_ours(args, world, rank, local_rank):
             breakdown["side_stream_ms_in_round"] = statistics.mean(
                 a.elapsed_time(b) for a, b in sev)
         breakdown["reserve_sms"] = args.reserve_sms
+        breakdown["layout"] = args.layout
 
     e2e, e2e_cold = run_e2e(args, world, soa, prev, cand, off, sched) if not args.no_e2e else (None, None)
 
@@ -311,9 +312,11 @@ def run_ours(args, world, rank, local_rank):
         "kernels": breakdown,
         "gpu_launches": int(launches),
         "cuda_graphs": bool(graphs),
-        "concurrency": (f"urgency + admission{' + NCCL candidate all-gather' if world > 1 else ''} "
-                        f"on a side stream over {args.reserve_sms} SMs reserved from the horizon "
-                        "kernel" if (graphs or overlap) and args.reserve_sms > 0 else None),
+        "concurrency": ((f"urgency on the whole GPU, then " if args.layout == "urgency_first" else "")
+                        + f"{'admission' if args.layout == 'urgency_first' else 'urgency + admission'}"
+                        f"{' + NCCL candidate all-gather' if world > 1 else ''} on a side stream over "
+                        f"{args.reserve_sms} SMs reserved from the horizon kernel"
+                        if (graphs or overlap) and args.reserve_sms > 0 else None),
         "clocks": clk.summary(),
     }
     if e2e:
@@ -550,8 +553,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--eager", action="store_true",
                     help="N=1: the N>1 path (eager launches, side-stream overlap) instead of graphs")
-    ap.add_argument("--reserve-sms", type=int, default=24,
+    ap.add_argument("--reserve-sms", type=int, default=12,
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
+    ap.add_argument("--layout", choices=["split", "urgency_first"], default="urgency_first",
+                    help="graph layout of the round (see rounds.DecisionRound.capture)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the other BASELINE configs' round latencies")

@@ -115,23 +115,40 @@ class DecisionRound:
         self.admit(fleet)
         return self.outputs()
 
-    def capture(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 0) -> None:
-        """Record the round as two CUDA graphs (horizons | urgency + admission)
-        over these fixed device buffers.  With `reserve_sms` > 0 the divergence
-        grid leaves that many SMs free and `replay()` runs the two graphs on two
-        streams: urgency and admission do not depend on this round's horizons
-        (the reference's order uses history, not H), so they overlap the
-        HBM-bound horizon kernel on the reserved SMs."""
+    def capture(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 0,
+                layout: str = "split") -> None:
+        """Record the round as CUDA graphs over these fixed device buffers.
+
+        layout "split": horizons | urgency + admission.  With `reserve_sms` > 0
+        the divergence grid leaves that many SMs free and `replay()` runs the
+        two graphs on two streams: urgency and admission do not depend on this
+        round's horizons (the reference's order uses history, not H), so they
+        overlap the HBM-bound horizon kernel on the reserved SMs.
+        layout "urgency_first": the HBM-streaming urgency pass first on the
+        whole GPU, then the horizon kernel on all but `reserve_sms` SMs while
+        the latency-bound admission (select, admit, sort of S_e) runs on the
+        side stream."""
+        if layout not in ("split", "urgency_first"):
+            raise ValueError(f"unknown round layout {layout!r}")
+        self.layout = layout
         self.max_sms = 0 if reserve_sms <= 0 else max(1, torch.cuda.get_device_properties(
             self.H.device).multi_processor_count - reserve_sms)
         self.run(fleet, h)  # warm-up: attribute / occupancy caches, lazy loading
         torch.cuda.synchronize()
         self.g_horizon, self.g_decide = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        self.g_urgency = None
         with torch.cuda.graph(self.g_horizon):
             self.horizons(h)
-        with torch.cuda.graph(self.g_decide):
-            self.urgency(fleet)
-            self.admit(fleet)
+        if layout == "urgency_first":
+            self.g_urgency = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.g_urgency):
+                self.urgency(fleet)
+            with torch.cuda.graph(self.g_decide):
+                self.admit(fleet)
+        else:
+            with torch.cuda.graph(self.g_decide):
+                self.urgency(fleet)
+                self.admit(fleet)
         self.side = torch.cuda.Stream(device=self.H.device) if reserve_sms > 0 else None
 
     def replay_concurrent(self, before_horizon=None, after_horizon=None, before_side=None,
@@ -143,6 +160,8 @@ class DecisionRound:
         side stream at the end.  `before_horizon` / `after_horizon` (callables)
         may record events around the horizon graph."""
         main = torch.cuda.current_stream()
+        if self.g_urgency is not None:
+            self.g_urgency.replay()  # the side stream forks after it
         if self.side is None:
             if before_horizon:
                 before_horizon(main)
@@ -171,12 +190,15 @@ class DecisionRound:
         self.replay_concurrent()
         return self.outputs()
 
-    def run_overlapped(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 24,
-                       before_horizon=None, after_horizon=None) -> RoundOutputs:
-        """One eager round with the graph path's overlap: the horizon kernel on
-        the current stream over all but `reserve_sms` SMs, urgency + admission
-        (for a sharded round: local select, the NCCL all-gather of candidates,
-        global select, local admission) on a side stream concurrently; the
+    def run_overlapped(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 12,
+                       before_horizon=None, after_horizon=None,
+                       layout: str = "urgency_first") -> RoundOutputs:
+        """One eager round with the graph path's overlap (see `capture`): the
+        horizon kernel on the current stream over all but `reserve_sms` SMs and
+        the admission (for a sharded round: local select, the NCCL all-gather
+        of candidates, global select, local admission) on a side stream
+        concurrently -- preceded on the current stream by the urgency pass
+        ("urgency_first") or running it on the side stream too ("split"); the
         current stream joins the side stream at the end.  The sharded round's
         collective runs here because NCCL work stays outside CUDA graphs."""
         n_sm = torch.cuda.get_device_properties(self.H.device).multi_processor_count
@@ -184,6 +206,8 @@ class DecisionRound:
         if getattr(self, "side", None) is None:
             self.side = torch.cuda.Stream(device=self.H.device)
         main = torch.cuda.current_stream()
+        if layout == "urgency_first":
+            self.urgency(fleet)
         fork = torch.cuda.Event()
         fork.record(main)
         if before_horizon:
@@ -193,7 +217,8 @@ class DecisionRound:
             after_horizon(main)
         self.side.wait_event(fork)
         with torch.cuda.stream(self.side):
-            self.urgency(fleet)
+            if layout != "urgency_first":
+                self.urgency(fleet)
             self.admit(fleet)
         main.wait_stream(self.side)
         return self.outputs()

@@ -101,9 +101,11 @@ def test_multi_round_replay_vs_oracle(R, k, rounds_):
         soa["skipped"] = res["skipped_out"]
 
 
-def test_concurrent_replay_matches_eager():
-    """Urgency + admission on a side stream over reserved SMs, concurrent with
-    the horizon kernel: identical outputs to the sequential eager round."""
+@pytest.mark.parametrize("layout,reserve", [("split", 16), ("urgency_first", 12)])
+def test_concurrent_replay_matches_eager(layout, reserve):
+    """Urgency + admission (or admission after a whole-GPU urgency pass) on a
+    side stream over reserved SMs, concurrent with the horizon kernel:
+    identical outputs to the sequential eager round."""
     from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
     R, k = 1 << 17, 2048
     soa = synthetic.fleet_soa(R, seed=8)
@@ -116,7 +118,8 @@ def test_concurrent_replay_matches_eager():
     eager = [t.clone() for t in (o1.horizon, o1.need_time, o1.admitted, o1.refetch, o1.edge_idx)]
     f2 = fl.DeviceFleet.from_host(soa)
     r2 = rounds.DecisionRound(R, k, sched)
-    r2.capture(f2, rounds.DivergenceInputs(prev, cand, 0.9, offset=off), reserve_sms=16)
+    r2.capture(f2, rounds.DivergenceInputs(prev, cand, 0.9, offset=off), reserve_sms=reserve,
+               layout=layout)
     f2.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
     o2 = r2.replay()
     torch.cuda.synchronize()

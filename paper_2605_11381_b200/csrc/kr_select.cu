@@ -622,16 +622,16 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
     }
 }
 
-// Small fleets (n <= kSmallAdmit): the whole select + admission + ordered S_e
-// in one CTA -- bitonic sort of all (key, index) pairs in shared memory, then
-// rank < k is admission (keys are unique, so this is key <= kth).  One launch
-// instead of the radix select's dozen, for latency-bound rounds such as
-// configs[1] (1k robots).
-constexpr int kSmallAdmit = 4096;
-constexpr int kSmallThreads = 1024;
+// Small fleets (n <= kSmallAdmit): sort all n (key, index) pairs with the
+// run sort (runs of 256 in shared memory on n / 256 CTAs, then the parallel
+// rank merge) and apply rank < k as admission (keys are unique, so this is
+// key <= kth) -- three short parallel launches instead of the radix select's
+// dozen, for latency-bound rounds such as configs[1] (1k robots).
+constexpr int kSmallAdmit = 8192;
 
 struct SmallAdmitArgs {
-    const kr_key* keys;
+    const kr_key* sorted_keys;
+    const int32_t* sorted_idx;
     int n, k;
     const int64_t* obs;  // nullable
     int32_t* skipped;    // nullable
@@ -643,50 +643,19 @@ struct SmallAdmitArgs {
     kr_key* kth_out;     // nullable
 };
 
-__global__ void __launch_bounds__(kSmallThreads) k_small_select_admit(SmallAdmitArgs a) {
-    extern __shared__ __align__(16) unsigned char small_smem[];
-    unsigned np2 = 1;
-    while (np2 < static_cast<unsigned>(a.n)) np2 <<= 1;
-    kr_key* sk = reinterpret_cast<kr_key*>(small_smem);
-    int32_t* si = reinterpret_cast<int32_t*>(sk + np2);
-    for (unsigned i = threadIdx.x; i < np2; i += blockDim.x) {
-        if (i < static_cast<unsigned>(a.n)) {
-            sk[i] = a.keys[i];
-            si[i] = static_cast<int32_t>(i);
-        } else {
-            sk[i] = kr_key{~0ull, ~0ull};
-            si[i] = INT_MAX;
-        }
-    }
-    __syncthreads();
-    for (unsigned kk = 2; kk <= np2; kk <<= 1) {
-        for (unsigned j = kk >> 1; j > 0; j >>= 1) {
-            for (unsigned t = threadIdx.x; t < np2 / 2; t += blockDim.x) {
-                const unsigned i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-                const unsigned l = i | j;
-                const bool up = (i & kk) == 0;
-                const kr_key ka = sk[i], kb = sk[l];
-                const int32_t ia = si[i], ib = si[l];
-                if (pair_gt(ka, ia, kb, ib) == up) {
-                    sk[i] = kb; sk[l] = ka;
-                    si[i] = ib; si[l] = ia;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (int p = threadIdx.x; p < a.n; p += blockDim.x) {
-        const int32_t j = si[p];
+__global__ void __launch_bounds__(256) k_small_apply(SmallAdmitArgs a) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.n; p += gridDim.x * blockDim.x) {
+        const int32_t j = a.sorted_idx[p];
         const bool in = p < a.k;
         if (a.admitted) a.admitted[j] = in;
         if (a.refetch) a.refetch[j] = in && (a.now - __ldg(a.obs + j) > a.stale);
         if (a.skipped) a.skipped[j] = in ? 0 : a.skipped[j] + 1;
         if (in) {
             if (a.edge_idx) a.edge_idx[p] = j;
-            if (a.edge_keys) a.edge_keys[p] = sk[p];
+            if (a.edge_keys) a.edge_keys[p] = a.sorted_keys[p];
         }
+        if (a.kth_out && p == a.k - 1) *a.kth_out = a.sorted_keys[p];
     }
-    if (a.kth_out && threadIdx.x == 0) *a.kth_out = sk[a.k - 1];
 }
 
 // ---------------------------------------------------------------------------
@@ -1002,9 +971,13 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
         return kr_admit(keys, n, k, kth_ptr, fleet, cfg, admitted, refetch, edge_idx, edge_keys,
                         ws, ws_bytes, stream);
     }
-    if (n <= kSmallAdmit) {  // one CTA: sort everything, rank < k is admission
+    if (n <= kSmallAdmit) {  // sort everything (run sort), rank < k is admission
+        Workspace w = carve(ws, n);
+        int e = sort_pairs(w, keys, nullptr, nullptr, n, w.sidx[0], w.skeys[0], nullptr, st);
+        if (e) return e;
         SmallAdmitArgs a{};
-        a.keys = keys;
+        a.sorted_keys = w.skeys[0];
+        a.sorted_idx = w.sidx[0];
         a.n = static_cast<int>(n);
         a.k = static_cast<int>(k);
         a.obs = fleet ? fleet->obs_captured_at : nullptr;
@@ -1016,17 +989,7 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
         a.edge_idx = edge_idx;
         a.edge_keys = edge_keys;
         a.kth_out = kth_out;
-        unsigned np2 = 1;
-        while (np2 < static_cast<unsigned>(n)) np2 <<= 1;
-        const size_t smem = np2 * (sizeof(kr_key) + sizeof(int32_t));
-        static std::atomic<int> smem_set{0};
-        if (smem_set.load() < static_cast<int>(smem)) {
-            KR_CUDA_TRY(cudaFuncSetAttribute(k_small_select_admit,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kSmallAdmit * static_cast<int>(sizeof(kr_key) + sizeof(int32_t))));
-            smem_set.store(kSmallAdmit * static_cast<int>(sizeof(kr_key) + sizeof(int32_t)));
-        }
-        k_small_select_admit<<<1, kSmallThreads, smem, st>>>(a);
+        k_small_apply<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(a);
         return check_launch("kr_select_admit(small)");
     }
     Workspace w = carve(ws, n);

@@ -416,7 +416,7 @@ def other_configs(reps: int = 200):
     t = timed(mixed)
     out["configs[2] 16k mixed (8k arms 64x7 + 8k humanoids 64x32) k=1024"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
-        "l2": "resident (85 MB inputs < 126 MB L2)"}
+        "l2": "163 MB of chunks (> 126 MB L2): mostly streamed from HBM"}
     # configs[3]: 64k robots, 8-sample ensembles 50x7, k = 8192 (one GPU's whole fleet)
     R = 65536
     soa = synthetic.fleet_soa(R, seed=16)

@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
 // rank merge) and apply rank < k as admission (keys are unique, so this is
 // key <= kth) -- three short parallel launches instead of the radix select's
 // dozen, for latency-bound rounds such as configs[1] (1k robots).
-constexpr int kSmallAdmit = 8192;
+constexpr int kSmallAdmit = 8192;  // measured: at 16k the rank merge (64 runs) loses to the select
 
 struct SmallAdmitArgs {
     const kr_key* sorted_keys;

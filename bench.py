@@ -206,7 +206,7 @@ def run_ours(args, world, rank, local_rank):
     prev, cand, off = synthetic.chunks(R, seed=2000 + rank)
     base = synthetic.NOW - (1 << 39)
     sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, base)
-    if world > 1:
+    if world > 1 or args.force_sharded:
         rnd = rounds.ShardedDecisionRound(R, args.k, sched)
     else:
         rnd = rounds.DecisionRound(R, args.k, sched)
@@ -218,7 +218,7 @@ def run_ours(args, world, rank, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    graphs = world == 1 and not args.no_graph and not args.eager
+    graphs = world == 1 and not args.no_graph and not args.eager and not args.force_sharded
     # N > 1 (or --eager): the same overlap eagerly (the NCCL all-gather stays outside graphs)
     overlap = not graphs and args.reserve_sms > 0 and not args.no_graph
     n_cap0 = lib.kr_launch_count()
@@ -557,6 +557,9 @@ def main():
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
     ap.add_argument("--layout", choices=["split", "urgency_first"], default="urgency_first",
                     help="graph layout of the round (see rounds.DecisionRound.capture)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="diagnostic: the N>1 sharded round (local select, all-gather, global "
+                         "select) on a one-rank process group")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the other BASELINE configs' round latencies")
@@ -571,15 +574,20 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, world, rank, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or args.force_sharded:
             import torch.distributed as dist
             dist.destroy_process_group()
 

@@ -19,6 +19,7 @@
  *   kr_select_admit         scheduler.py:193-241 select + admission + ordered S_e
  *   kr_admit                scheduler.py:223-234 refetch + skip counters
  *   kr_sort_keys            scheduler.py:130-140 the total order itself
+ *   kr_merge_runs           sharded admission: W sorted local top-k' lists -> global S_e
  *   kr_ledger_apply         core.py:200-229 + waiting.py:69-93  incremental TaskState
  *                           history and running wait totals (sim.py:358-440 mutations)
  *   kr_urgency_ledger       kr_urgency over the device-resident ledger (O(1) per request)
@@ -253,6 +254,13 @@ KR_API int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
                            const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
                            int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* workspace,
                            size_t workspace_bytes, void* stream);
+/* Sharded admission (rounds.sharded_topk): `runs` holds W ascending runs of
+ * `len` keys each (every rank's local top-k' candidates, all-ones padded, as
+ * all-gathered).  Writes the k smallest keys overall, in order, to out_keys
+ * (nullable) and the k-th smallest to kth_out (nullable); k <= W * len. */
+KR_API int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t k, kr_key* out_keys,
+                         kr_key* kth_out, void* stream);
+
 /* ---- phase 3: hybrid edge / cloud placement --------------------------- */
 
 /* out[i] = base_us + round_half_up(payload[i] * 8e6 / bps)   (engines.py:158-169) */

@@ -658,6 +658,44 @@ __global__ void __launch_bounds__(256) k_small_apply(SmallAdmitArgs a) {
     }
 }
 
+// Merge of W sorted candidate runs (the sharded round's all-gathered local
+// top-k' lists, sentinel-padded to equal length): every element's global rank
+// = its index in its run + the number of smaller elements in each other run
+// (binary search; one lane per run, a warp per element; ties -- the all-ones
+// sentinels -- broken by position).  Ranks < k are the global S_e in order;
+// rank k - 1 is the global k-th key.
+__global__ void __launch_bounds__(256) k_merge_runs(const kr_key* runs, int W, int len, int k,
+                                                    kr_key* out_keys, kr_key* kth_out) {
+    const int m = W * len;
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < m; e += gridDim.x * wpb) {
+        const kr_key x = runs[e];
+        const int own = e / len;
+        int c = 0;
+        for (int r = lane; r < W; r += 32) {
+            if (r == own) continue;
+            int lo = r * len, hi = lo + len;
+            const int start = lo;
+            while (lo < hi) {  // elements of run r ordered before (x, e)
+                const int mid = (lo + hi) >> 1;
+                if (pair_gt(x, e, runs[mid], mid)) lo = mid + 1;
+                else hi = mid;
+            }
+            c += lo - start;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            const int rank = c + (e - own * len);
+            if (rank < k) {
+                if (out_keys) out_keys[rank] = x;
+                if (kth_out && rank == k - 1) *kth_out = x;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // sorting the admitted set (generic paths)
 // ---------------------------------------------------------------------------
@@ -931,6 +969,22 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
                                const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
                                int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* ws,
                                size_t ws_bytes, void* stream);
+
+extern "C" int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t k,
+                             kr_key* out_keys, kr_key* kth_out, void* stream) {
+    if (W < 1 || len < 0 || k < 0 || k > static_cast<int64_t>(W) * len ||
+        static_cast<int64_t>(W) * len > INT_MAX)
+        return KR_EINVAL;
+    if (k == 0 || len == 0) return KR_OK;
+    if (!runs) return KR_EINVAL;
+    const int64_t m = static_cast<int64_t>(W) * len;
+    int64_t blocks = (m + 7) / 8;
+    const int64_t cap = static_cast<int64_t>(device_info().sm_count) * 64;
+    if (blocks > cap) blocks = cap;
+    k_merge_runs<<<static_cast<unsigned>(blocks), 256, 0, as_stream(stream)>>>(
+        runs, W, static_cast<int>(len), static_cast<int>(k), out_keys, kth_out);
+    return check_launch("kr_merge_runs");
+}
 
 extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth,
                               const unsigned long long* key_stats, void* ws, size_t ws_bytes,

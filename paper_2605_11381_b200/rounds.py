@@ -229,24 +229,25 @@ def sharded_topk(keys, n_local: int, k: int, sizes: list, ops, group=None):
 
     `ops` supplies the device primitives (product: `CudaShardOps`; the CPU
     tests plug in a numpy twin to exercise this protocol under gloo):
-      local_candidates(keys, kl, kg) -> [kg, 2] local top-kl keys, sentinel-padded
-      all_gather(cand)               -> [W * kg, 2]
-      kth(keys, k)                   -> k-th smallest key (device handle)
-      sorted_leq(keys, k, kth)       -> the keys <= kth, ascending ([k, 2])
+      local_candidates(keys, kl, kg) -> [kg, 2] local top-kl keys ascending,
+                                        sentinel-padded
+      all_gather(cand)               -> [W * kg, 2] (W sorted runs)
+      merge(runs, W, kg, want_kth)   -> (global S_e keys [kg, 2] in order,
+                                         the kg-th key or None)
       apply(keys, k, kth)            -> local admission (masks, skip counters)
+    Exact: the global top-kg is a subset of the union of the local top-kl
+    lists, so merging the sorted runs and keeping ranks < kg gives it in order.
     Returns (k_global, global ordered S_e keys).
     """
     world = len(sizes)
-    kg = min(k, sum(sizes))
+    total = sum(sizes)
+    kg = min(k, total)
     kl = min(kg, n_local)
     cand = ops.local_candidates(keys, kl, kg)
     gathered = ops.all_gather(cand)
-    m = kg * world
-    if world == 1:
-        kth = ops.kth(keys, kl) if 0 < kl < n_local else None
-    else:
-        kth = ops.kth(gathered, kg) if 0 < kg < m else None
-    edge = ops.sorted_leq(gathered, kg, kth) if kg > 0 else None
+    edge, kth = None, None
+    if kg > 0:
+        edge, kth = ops.merge(gathered, world, kg, kg < total)
     ops.apply(keys, kg, kth)
     return kg, edge
 
@@ -259,18 +260,15 @@ class CudaShardOps:
         self.fleet = fleet
 
     def local_candidates(self, keys, kl, kg):
+        # fused select + gather + sort of the local top-kl (no side effects:
+        # no fleet / masks), sentinel padding beyond kl
         r, st = self.r, dev.stream()
         r.cand.fill_(ALL_ONES)
         if kl > 0:
-            kth_ptr = None
-            if kl < r.R:
-                _lib.check(r.lib.kr_topk_select(keys.data_ptr(), r.R, kl, r.kth_local.data_ptr(),
-                                                None, r.ws.ptr(), r.ws.nbytes, st),
-                           "kr_topk_select")
-                kth_ptr = r.kth_local.data_ptr()
-            _lib.check(r.lib.kr_admit(keys.data_ptr(), r.R, kl, kth_ptr, None, None, None, None,
-                                      None, r.cand.data_ptr(), r.ws.ptr(), r.ws.nbytes, st),
-                       "kr_admit(local candidates)")
+            _lib.check(r.lib.kr_select_admit(keys.data_ptr(), r.R, kl, r.key_stats.data_ptr(),
+                                             None, None, None, None, None, r.cand.data_ptr(),
+                                             None, r.ws.ptr(), r.ws.nbytes, st),
+                       "kr_select_admit(local candidates)")
         return r.cand
 
     def all_gather(self, cand):
@@ -282,20 +280,12 @@ class CudaShardOps:
             dist.all_gather(parts, cand, group=self.r.group)
         return self.r.gathered
 
-    def kth(self, keys, k):
+    def merge(self, runs, W, kg, want_kth):
         r = self.r
-        ws = r.ws if keys is r.keys else r.ws_merge
-        out = r.kth_local if keys is r.keys else r.kth_global
-        _lib.check(r.lib.kr_topk_select(keys.data_ptr(), keys.shape[0], k, out.data_ptr(), None,
-                                        ws.ptr(), ws.nbytes, dev.stream()), "kr_topk_select")
-        return out
-
-    def sorted_leq(self, keys, k, kth):
-        r = self.r
-        _lib.check(r.lib.kr_admit(keys.data_ptr(), keys.shape[0], k, _lib.ptr(kth), None, None,
-                                  None, None, None, r.global_edge.data_ptr(), r.ws_merge.ptr(),
-                                  r.ws_merge.nbytes, dev.stream()), "kr_admit(merge)")
-        return r.global_edge[:k]
+        _lib.check(r.lib.kr_merge_runs(runs.data_ptr(), W, kg, kg, r.global_edge.data_ptr(),
+                                       r.kth_global.data_ptr() if want_kth else None,
+                                       dev.stream()), "kr_merge_runs")
+        return r.global_edge[:kg], (r.kth_global if want_kth else None)
 
     def apply(self, keys, k, kth):
         r = self.r
@@ -325,10 +315,8 @@ class ShardedDecisionRound(DecisionRound):
         d = self.H.device
         self.cand = fl.new_keys(kg, d)
         self.gathered = fl.new_keys(kg * self.world, d)
-        self.kth_local = fl.new_keys(1, d)
         self.kth_global = fl.new_keys(1, d)
         self.global_edge = fl.new_keys(kg, d)
-        self.ws_merge = fl.Workspace(kg * self.world)
 
     def admit(self, fleet: fl.DeviceFleet) -> None:
         sharded_topk(self.keys, self.R, self.k_request, self.sizes, CudaShardOps(self, fleet),

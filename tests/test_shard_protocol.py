@@ -37,12 +37,9 @@ class NumpyShardOps:
         dist.all_gather(outs, t)
         return torch.cat(outs).numpy().view(np.uint64)
 
-    def kth(self, keys, k):
-        return keys[_sorted_idx(keys)[k - 1]]
-
-    def sorted_leq(self, keys, k, kth):
-        s = keys[_sorted_idx(keys)]
-        return s[:k]
+    def merge(self, runs, W, kg, want_kth):
+        s = runs[_sorted_idx(runs)]
+        return s[:kg], (s[kg - 1] if want_kth else None)
 
     def apply(self, keys, k, kth):
         if k == 0:

@@ -116,3 +116,37 @@ def test_select_admit_fused(n, k, mode):
         assert np.array_equal(edge_idx.cpu().numpy(), exp[:k])
         assert np.array_equal(edge_keys.cpu().numpy().view(np.uint64), keys[exp[:k]])
         assert np.array_equal(kth.cpu().numpy().view(np.uint64)[0], keys[exp[k - 1]])
+
+
+@pytest.mark.parametrize("W,len_,fill", [(1, 50, 50), (8, 1024, 700), (3, 257, 0), (32, 64, 64),
+                                         (40, 16, 9)])
+def test_merge_runs(W, len_, fill):
+    """kr_merge_runs over W ascending runs, each with `fill` real keys then the
+    all-ones sentinel padding (a sharded round's all-gathered candidates)."""
+    from paper_2605_11381_b200 import _lib, device as dev, fleet as fl
+    rng = np.random.default_rng(W * 1000 + len_)
+    runs = np.full((W, len_, 2), np.iinfo(np.uint64).max, np.uint64)
+    real = []
+    for w in range(W):
+        f = int(rng.integers(0, fill + 1)) if fill else 0
+        hi = rng.integers(0, 4, f, dtype=np.uint64) << np.uint64(60)
+        lo = (rng.integers(0, 1 << 30, f, dtype=np.uint64) << np.uint64(24)) | \
+            np.uint64(w * len_) + np.arange(f, dtype=np.uint64)  # unique keys
+        k = np.stack([hi, lo], 1)
+        k = k[_order(k)]
+        runs[w, :f] = k
+        real.append(k)
+    allreal = np.concatenate(real) if real else np.zeros((0, 2), np.uint64)
+    exp = allreal[_order(allreal)]
+    t = torch.from_numpy(runs.reshape(-1, 2).view(np.int64)).cuda()
+    for kk in sorted({1, max(1, len(exp) // 2), max(1, len(exp)), min(W * len_, len(exp) + 3)}):
+        out = fl.new_keys(kk)
+        kth = fl.new_keys(1)
+        _lib.check(_lib.load().kr_merge_runs(t.data_ptr(), W, len_, kk, out.data_ptr(),
+                                             kth.data_ptr(), dev.stream()), "kr_merge_runs")
+        got = out.cpu().numpy().view(np.uint64)
+        n_real = min(kk, len(exp))
+        assert np.array_equal(got[:n_real], exp[:n_real])
+        assert (got[n_real:] == np.iinfo(np.uint64).max).all()
+        assert np.array_equal(kth.cpu().numpy().view(np.uint64)[0],
+                              exp[kk - 1] if kk <= len(exp) else np.array([np.iinfo(np.uint64).max] * 2, np.uint64))

@@ -152,10 +152,6 @@ def store_traces(traces: Iterable[TaskTrace], path: str | Path) -> None:
 _Cols = _lib.KrTraceColumns
 
 
-def _native():
-    return _lib.load()
-
-
 def _arr(ptr, n, dtype) -> np.ndarray:
     if n == 0 or not ptr:
         return np.zeros(0, dtype)
@@ -234,7 +230,7 @@ def _columns(c: _Cols) -> TraceColumns:
 
 
 def _finish(status: int, handle: ctypes.c_void_p, line_override=None) -> TraceColumns:
-    lib = _native()
+    lib = _lib.load()
     try:
         c = lib.kr_trace_columns_of(handle).contents
         if status == _lib.KR_EFORMAT:
@@ -253,7 +249,7 @@ def parse_jsonl(text: str | bytes, first_line: int = 1, line_override=None) -> T
     """JSON Lines text -> TraceColumns (load_traces semantics)."""
     data = text.encode("utf-8", "surrogatepass") if isinstance(text, str) else bytes(text)
     h = ctypes.c_void_p()
-    st = _native().kr_trace_parse(data, len(data), first_line, ctypes.byref(h))
+    st = _lib.load().kr_trace_parse(data, len(data), first_line, ctypes.byref(h))
     return _finish(st, h, line_override)
 
 
@@ -264,7 +260,7 @@ def load_trace_columns(path: str | Path) -> TraceColumns:
     parts = []
     for f in files:
         h = ctypes.c_void_p()
-        st = _native().kr_trace_load(str(f).encode(), ctypes.byref(h))
+        st = _lib.load().kr_trace_load(str(f).encode(), ctypes.byref(h))
         if st == _lib.KR_EINVAL and not h.value:
             raise FileNotFoundError(str(f))
         parts.append(_finish(st, h))

@@ -428,6 +428,18 @@ def other_configs(reps: int = 200):
     out["configs[3] 64k robots S=8 ensembles 50x7 k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (826 MB inputs)"}
+    # the headline fleet with the confidence policy (paper default t=0.4, H_min=5)
+    from paper_2605_11381_b200 import HorizonPolicyConfig
+    R = 1 << 20
+    soa = synthetic.fleet_soa(R, seed=18)
+    fleet = fl.DeviceFleet.from_host(soa)
+    U = synthetic.magnitudes(R, seed=19)
+    rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
+    inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))
+    t = timed(lambda: rnd.run(fleet, inp))
+    out["configs[4] per-GPU share, confidence policy (U 2^20 x 6 x 50 fp32), k=8192"] = {
+        "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
+        "l2": "streams from HBM (1.26 GB of magnitudes)", "layout": "serial eager-graph round"}
     return out
 
 

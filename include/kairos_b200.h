@@ -157,10 +157,11 @@ KR_API unsigned long long kr_launch_count(void);
 /* ---- step 1: execution-horizon selection ------------------------------ */
 
 /* U: [R][K][N] fp32 (dtype KR_F32) or fp64, row-major.  H[r] = decide_horizon.
- * one_plus_t = 1.0 + threshold computed on the host in fp64 (horizon.py:127). */
+ * one_plus_t = 1.0 + threshold computed on the host in fp64 (horizon.py:127).
+ * max_sms (0 = all) caps the persistent grid as for kr_horizon_divergence. */
 KR_API int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_t K, int32_t N,
                           double one_plus_t, int32_t min_horizon, int32_t* H,
-                          uint32_t* flags, void* stream);
+                          uint32_t* flags, int32_t max_sms, void* stream);
 KR_API int kr_horizon_static(int64_t R, int32_t N, int32_t static_h, int32_t* H, void* stream);
 
 /* C <= 64 policy configurations decided over the same rounds U[R][K][N] in

@@ -90,7 +90,7 @@ _SIGNATURES = {
     "kr_last_error": (ctypes.c_char_p, []),
     "kr_launch_count": (ctypes.c_ulonglong, []),
     "kr_horizon_confidence": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _f64, _i32,
-                                             _vp, _vp, _vp]),
+                                             _vp, _vp, _i32, _vp]),
     "kr_horizon_static": (ctypes.c_int, [_i64, _i32, _i32, _vp, _vp]),
     "kr_horizon_sweep": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _vp, _vp, _vp,
                                         _vp, _vp, _vp, _vp]),

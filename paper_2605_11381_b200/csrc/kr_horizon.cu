@@ -263,7 +263,7 @@ extern "C" int kr_horizon_static(int64_t R, int32_t N, int32_t static_h, int32_t
 
 extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_t K, int32_t N,
                                      double one_plus_t, int32_t min_horizon, int32_t* H,
-                                     uint32_t* flags, void* stream) {
+                                     uint32_t* flags, int32_t max_sms, void* stream) {
     if (R < 0 || K < 2 || N < 1 || min_horizon < 1 || (dtype != KR_F32 && dtype != KR_F64))
         return KR_EINVAL;
     if (R == 0) return KR_OK;
@@ -287,7 +287,7 @@ extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_
             c1,      1.f + m, 1.f - m, one_plus_t / static_cast<double>(K - 1),
             1.0 + md, 1.0 - md, H,     flags,       nullptr,  {},
             {}};
-        return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_confidence");
+        return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_confidence", max_sms);
     };
     // columns per thread: vector loads need N % VC == 0 and a 16-byte aligned base
     const bool al = (reinterpret_cast<uintptr_t>(U) & 15u) == 0;

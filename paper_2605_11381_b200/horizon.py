@@ -95,7 +95,8 @@ class HorizonPolicyConfig:
 
 
 def decide_horizon_batch(cfg: HorizonPolicyConfig, U: torch.Tensor,
-                         out: torch.Tensor | None = None, validate: bool = True) -> torch.Tensor:
+                         out: torch.Tensor | None = None, validate: bool = True,
+                         max_sms: int = 0) -> torch.Tensor:
     """H[r] = decide_horizon(cfg, U[r]) for a device tensor U[R, K, N].
 
     fp32 storage is upcast exactly; all arithmetic is fp64.  With
@@ -126,7 +127,7 @@ def decide_horizon_batch(cfg: HorizonPolicyConfig, U: torch.Tensor,
     fl = dev.flags() if validate else None
     dtype = _lib.KR_F64 if U.dtype == torch.float64 else _lib.KR_F32
     _lib.check(lib.kr_horizon_confidence(U.data_ptr(), dtype, R, K, N, 1.0 + cfg.threshold,
-                                         cfg.min_horizon, out.data_ptr(), _lib.ptr(fl),
+                                         cfg.min_horizon, out.data_ptr(), _lib.ptr(fl), max_sms,
                                          dev.stream()), "kr_horizon_confidence")
     if validate:
         f = dev.read_flags(fl)

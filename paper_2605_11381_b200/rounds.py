@@ -58,6 +58,13 @@ class DivergenceInputs:
     len_cand: torch.Tensor | None = None
 
 
+@dataclass
+class ConfidenceInputs:
+    """The confidence-threshold (or static) policy over update magnitudes."""
+    U: torch.Tensor                    # [R, K, N] fp32 / fp64
+    cfg: object                        # horizon.HorizonPolicyConfig
+
+
 class DecisionRound:
     """Preallocated single-GPU decision round over R robots, budget k."""
 
@@ -79,7 +86,11 @@ class DecisionRound:
         self.lib = _lib.load()
         self.max_sms = 0  # divergence grid SM cap (0: all); see capture(concurrent=...)
 
-    def horizons(self, h: DivergenceInputs) -> None:
+    def horizons(self, h) -> None:
+        if isinstance(h, ConfidenceInputs):
+            from .horizon import decide_horizon_batch
+            decide_horizon_batch(h.cfg, h.U, out=self.H, validate=False, max_sms=self.max_sms)
+            return
         prev, cand = h.prev, h.cand
         if cand.dim() == 3:
             cand = cand.unsqueeze(1)

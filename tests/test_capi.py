@@ -46,7 +46,7 @@ def test_host_only_entry_points():
     assert lib.kr_status_string(0) == b"ok"
     assert lib.kr_workspace_bytes(1 << 20) > 64 * (1 << 20)
     # argument validation happens before any device work
-    assert lib.kr_horizon_confidence(None, 0, 4, 1, 8, 1.4, 1, None, None, None) == _lib.KR_EINVAL
+    assert lib.kr_horizon_confidence(None, 0, 4, 1, 8, 1.4, 1, None, None, 0, None) == _lib.KR_EINVAL
     assert lib.kr_horizon_divergence(None, None, 0, 4, 1, 8, 8, 7, None, None, None, 0.0, None,
                                      None, 0, None) == _lib.KR_EINVAL
     assert lib.kr_horizon_static(0, 8, 3, None, None) == _lib.KR_OK

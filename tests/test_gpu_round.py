@@ -125,3 +125,33 @@ def test_concurrent_replay_matches_eager(layout, reserve):
     torch.cuda.synchronize()
     for a, b in zip(eager, (o2.horizon, o2.need_time, o2.admitted, o2.refetch, o2.edge_idx)):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("storage", [torch.float32, torch.float64])
+def test_confidence_round_vs_oracle(storage):
+    """A decision round with the confidence-threshold policy (update
+    magnitudes) instead of the divergence horizon, eager and as the captured
+    urgency-first concurrent graphs."""
+    from paper_2605_11381_b200 import HorizonPolicyConfig, fleet as fl, rounds, synthetic
+    R, k = 1 << 16, 1024
+    soa = synthetic.fleet_soa(R, seed=31)
+    U = synthetic.magnitudes(R, seed=32, dtype=storage)
+    cfg = HorizonPolicyConfig.confidence(0.4, 5)
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    H = orc.horizon_conf_batch(U.cpu().numpy(), 0.4, 5)
+    res = orc.plan_soa(soa, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+    for graph in (False, True):
+        fleet = fl.DeviceFleet.from_host(soa)
+        rnd = rounds.DecisionRound(R, k, sched)
+        inp = rounds.ConfidenceInputs(U, cfg)
+        if graph:
+            rnd.capture(fleet, inp, reserve_sms=12, layout="urgency_first")
+            fleet.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
+            out = rnd.replay()
+        else:
+            out = rnd.run(fleet, inp)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.horizon.cpu().numpy(), H)
+        assert np.array_equal(out.edge_idx.cpu().numpy(), res["order"][:k])
+        assert np.array_equal(fleet.t["skipped"].cpu().numpy(), res["skipped_out"])

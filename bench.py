@@ -361,14 +361,6 @@ def other_configs(reps: int = 200):
     lib = _lib.load()
     out = {}
 
-    def div_into(Hslice, prev, cand, off):
-        R, Lp, D = prev.shape
-        S, Lc = cand.shape[1], cand.shape[2]
-        _lib.check(lib.kr_horizon_divergence(prev.data_ptr(), cand.data_ptr(), _lib.KR_F32, R, S,
-                                             Lp, Lc, D, off.data_ptr(), None, None, THR,
-                                             Hslice.data_ptr(), None, 0, dev.stream()),
-                   "kr_horizon_divergence")
-
     def timed(fn):
         fn()
         torch.cuda.synchronize()
@@ -407,16 +399,13 @@ def other_configs(reps: int = 200):
     pa, ca, oa = synthetic.chunks(R // 2, seed=14, Lp=64, Lc=64, D=7)
     ph, chh, oh = synthetic.chunks(R // 2, seed=15, Lp=64, Lc=64, D=32)
     rnd = rounds.DecisionRound(R, 1024, sched_for(soa))
-
-    def mixed():
-        div_into(rnd.H[: R // 2], pa, ca, oa)
-        div_into(rnd.H[R // 2:], ph, chh, oh)
-        rnd.urgency(fleet)
-        rnd.admit(fleet)
-    t = timed(mixed)
+    inp = rounds.MixedInputs([(0, rounds.DivergenceInputs(pa, ca, THR, offset=oa)),
+                              (R // 2, rounds.DivergenceInputs(ph, chh, THR, offset=oh))])
+    t = timed(lambda: rnd.run(fleet, inp))
     out["configs[2] 16k mixed (8k arms 64x7 + 8k humanoids 64x32) k=1024"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
-        "l2": "163 MB of chunks (> 126 MB L2): mostly streamed from HBM"}
+        "l2": "163 MB of chunks (> 126 MB L2): mostly streamed from HBM",
+        "layout": "the two groups' horizon kernels on forked streams, then urgency + admission"}
     # configs[3]: 64k robots, 8-sample ensembles 50x7, k = 8192 (one GPU's whole fleet)
     R = 65536
     soa = synthetic.fleet_soa(R, seed=16)

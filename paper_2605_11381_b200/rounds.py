@@ -65,6 +65,15 @@ class ConfidenceInputs:
     cfg: object                        # horizon.HorizonPolicyConfig
 
 
+@dataclass
+class MixedInputs:
+    """A heterogeneous fleet: horizon inputs per contiguous robot group, e.g.
+    arms (64x7) and humanoids (64x32) as two homogeneous tensors (configs[2]).
+    groups: [(first robot, DivergenceInputs | ConfidenceInputs)], covering
+    the fleet.  The groups' horizon kernels run concurrently on forked streams."""
+    groups: list
+
+
 class DecisionRound:
     """Preallocated single-GPU decision round over R robots, budget k."""
 
@@ -87,9 +96,35 @@ class DecisionRound:
         self.max_sms = 0  # divergence grid SM cap (0: all); see capture(concurrent=...)
 
     def horizons(self, h) -> None:
+        if isinstance(h, MixedInputs):
+            self._horizons_mixed(h)
+            return
+        self._horizon_into(self.H, h)
+
+    def _horizons_mixed(self, h: MixedInputs) -> None:
+        main = torch.cuda.current_stream()
+        if len(h.groups) == 1:
+            start, g = h.groups[0]
+            self._horizon_into(self.H[start:], g)
+            return
+        if not hasattr(self, "group_streams"):
+            self.group_streams = []
+        while len(self.group_streams) < len(h.groups):
+            self.group_streams.append(torch.cuda.Stream(device=self.H.device))
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for (start, g), st in zip(h.groups, self.group_streams):
+            st.wait_event(fork)
+            with torch.cuda.stream(st):
+                self._horizon_into(self.H[start:], g)
+        for st in self.group_streams[: len(h.groups)]:
+            main.wait_stream(st)
+
+    def _horizon_into(self, H: torch.Tensor, h) -> None:
         if isinstance(h, ConfidenceInputs):
             from .horizon import decide_horizon_batch
-            decide_horizon_batch(h.cfg, h.U, out=self.H, validate=False, max_sms=self.max_sms)
+            decide_horizon_batch(h.cfg, h.U, out=H[: h.U.shape[0]], validate=False,
+                                 max_sms=self.max_sms)
             return
         prev, cand = h.prev, h.cand
         if cand.dim() == 3:
@@ -99,7 +134,7 @@ class DecisionRound:
         dtype = _lib.KR_F64 if prev.dtype == torch.float64 else _lib.KR_F32
         _lib.check(self.lib.kr_horizon_divergence(
             prev.data_ptr(), cand.data_ptr(), dtype, R, S, Lp, Lc, D, _lib.ptr(h.offset),
-            _lib.ptr(h.len_prev), _lib.ptr(h.len_cand), float(h.threshold), self.H.data_ptr(),
+            _lib.ptr(h.len_prev), _lib.ptr(h.len_cand), float(h.threshold), H.data_ptr(),
             None, self.max_sms, dev.stream()), "kr_horizon_divergence")
 
     def urgency(self, fleet: fl.DeviceFleet) -> None:

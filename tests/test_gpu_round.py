@@ -155,3 +155,38 @@ def test_confidence_round_vs_oracle(storage):
         assert np.array_equal(out.horizon.cpu().numpy(), H)
         assert np.array_equal(out.edge_idx.cpu().numpy(), res["order"][:k])
         assert np.array_equal(fleet.t["skipped"].cpu().numpy(), res["skipped_out"])
+
+
+def test_mixed_fleet_round_vs_oracle():
+    """configs[2]-style heterogeneous fleet: arms (64x7 divergence), humanoids
+    (64x32 divergence) and a confidence-policy group in one round, the groups'
+    horizon kernels on forked streams; eager and captured."""
+    from paper_2605_11381_b200 import HorizonPolicyConfig, fleet as fl, rounds, synthetic
+    na, nh, nc, k = 3000, 2000, 1500, 700
+    R = na + nh + nc
+    soa = synthetic.fleet_soa(R, seed=41)
+    pa, ca, oa = synthetic.chunks(na, seed=42, Lp=64, Lc=64, D=7)
+    ph, chh, oh = synthetic.chunks(nh, seed=43, Lp=64, Lc=64, D=32)
+    U = synthetic.magnitudes(nc, seed=44)
+    inp = rounds.MixedInputs([(0, rounds.DivergenceInputs(pa, ca, 0.9, offset=oa)),
+                              (na, rounds.DivergenceInputs(ph, chh, 0.9, offset=oh)),
+                              (na + nh, rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5)))])
+    H = np.concatenate([
+        orc.divergence_batch(pa.cpu().numpy(), ca.cpu().numpy(), 0.9, oa.cpu().numpy()),
+        orc.divergence_batch(ph.cpu().numpy(), chh.cpu().numpy(), 0.9, oh.cpu().numpy()),
+        orc.horizon_conf_batch(U.cpu().numpy(), 0.4, 5)])
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    res = orc.plan_soa(soa, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+    for graph in (False, True):
+        fleet = fl.DeviceFleet.from_host(soa)
+        rnd = rounds.DecisionRound(R, k, sched)
+        if graph:
+            rnd.capture(fleet, inp, reserve_sms=12, layout="urgency_first")
+            fleet.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
+            out = rnd.replay()
+        else:
+            out = rnd.run(fleet, inp)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.horizon.cpu().numpy(), H)
+        assert np.array_equal(out.edge_idx.cpu().numpy(), res["order"][:k])

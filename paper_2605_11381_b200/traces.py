@@ -134,10 +134,23 @@ def trace_to_dict(trace: TaskTrace) -> dict:
             "rounds": [_round_to_dict(r) for r in trace.rounds]}
 
 
+def _jsonable(x):
+    if isinstance(x, np.ndarray):
+        return x.tolist()
+    if isinstance(x, np.generic):
+        return x.item()
+    if isinstance(x, UpdateMagnitudes):
+        return x.u.tolist()
+    if isinstance(x, tuple):
+        return list(x)
+    raise TypeError(f"cannot serialise {type(x).__name__} in a trace")
+
+
 def trace_from_dict(data: dict, line: int = 0) -> TaskTrace:
-    """One decoded trace object -> TaskTrace, through the native validator."""
-    return _objects(parse_jsonl(json.dumps(data, allow_nan=True), first_line=line,
-                                line_override=line))[0]
+    """One decoded trace object -> TaskTrace, through the native validator
+    (numpy arrays are accepted where the reference's np.asarray would be)."""
+    return _objects(parse_jsonl(json.dumps(data, allow_nan=True, default=_jsonable),
+                                first_line=line, line_override=line))[0]
 
 
 def store_traces(traces: Iterable[TaskTrace], path: str | Path) -> None:

@@ -182,10 +182,15 @@ def sweep_horizon_sums(cfgs: Sequence[HorizonPolicyConfig], U: torch.Tensor,
     for c0 in range(0, C, SWEEP_MAX_CONFIGS):
         part = cfgs[c0:c0 + SWEEP_MAX_CONFIGS]
         n = len(part)
-        kind = (ctypes.c_int32 * n)(*[0 if c.kind == STATIC else 1 for c in part])
-        opt = (ctypes.c_double * n)(*[1.0 + c.threshold for c in part])
-        prm = (ctypes.c_int32 * n)(*[c.static_h if c.kind == STATIC else c.min_horizon
-                                     for c in part])
+        # a NaN / +inf threshold never trips (f > NaN and f > inf are false), so
+        # the reference decides N for every round: a static cell of N
+        never = [c.kind != STATIC and not np.isfinite(1.0 + c.threshold) for c in part]
+        kind = (ctypes.c_int32 * n)(*[0 if c.kind == STATIC or nv else 1
+                                      for c, nv in zip(part, never)])
+        opt = (ctypes.c_double * n)(*[1.0 if nv else 1.0 + c.threshold
+                                      for c, nv in zip(part, never)])
+        prm = (ctypes.c_int32 * n)(*[N if nv else (c.static_h if c.kind == STATIC else c.min_horizon)
+                                     for c, nv in zip(part, never)])
         _lib.check(lib.kr_horizon_sweep(U.data_ptr(), dtype, R, K, N, n, _addr(kind), _addr(opt), _addr(prm),
                                         sums[c0:].data_ptr(),
                                         None if H is None else H[c0].data_ptr(),

@@ -239,3 +239,21 @@ def test_sweep_validation(kb):
         kb.sweep_horizon_sums([kb.HorizonPolicyConfig.static(3)], U)
     with pytest.raises(ValueError, match="no policy"):
         kb.sweep_horizon_sums([], U)
+
+
+def test_nonfinite_thresholds(kb):
+    """HorizonPolicyConfig accepts NaN / +inf thresholds (only t < 0 is rejected,
+    horizon.py:86); f > (1 + t) * m is then never true, so every round decides N."""
+    rng = np.random.default_rng(9)
+    U = rng.uniform(0.0, 2.0, (300, 6, 50))
+    U[:, -1, 30:] *= 5.0
+    Ut = torch.from_numpy(U).cuda()
+    for t in (float("nan"), float("inf")):
+        cfg = kb.HorizonPolicyConfig.confidence(t, 5)
+        exp = orc.horizon_conf_batch(U, t, 5)
+        assert (exp == 50).all()
+        assert np.array_equal(kb.decide_horizon_batch(cfg, Ut).cpu().numpy(), exp)
+        cells = [cfg, kb.HorizonPolicyConfig.confidence(0.4, 5), cfg]
+        sums = kb.sweep_horizon_sums(cells, Ut).cpu().numpy()
+        assert sums[0] == sums[2] == 300 * 50
+        assert sums[1] == orc.horizon_conf_batch(U, 0.4, 5).sum()

@@ -16,8 +16,10 @@ def main(src, dst, cmd):
             out.append((d["Kernel Name"], float(d["Metric Value"])))
     idx = [i for i, (n, _) in enumerate(out) if "k_horizon_divergence" in n]
     last = out[idx[-1]:]
-    ends = [i for i, (n, _) in enumerate(last) if "k_run_merge" in n or "k_small_apply" in n]
-    if ends:  # one round: up to the ordered S_e (later launches belong to the next timing)
+    # one round: up to the ordered S_e (later launches belong to the next timing)
+    ends = [i for i, (n, _) in enumerate(last) if "k_small_apply" in n] or \
+        [i for i, (n, _) in enumerate(last) if "k_run_merge" in n]
+    if ends:
         last = last[:ends[0] + 1]
     tot = sum(v for _, v in last)
     with open(dst, "w") as f:

@@ -191,6 +191,90 @@ struct SweepWork {
         return fl;
     }
 
+    // One chunk of 32 VC columns of robot `rob`: trip counts, the warp's
+    // max-scan continuing from `carry`, the steps; returns the chunk's
+    // running max (the next chunk's carry).
+    __device__ __forceinline__ int chunk(const T* rob, int n0c, int carry, int64_t r,
+                                         uint32_t& fl) const {
+        const int Kr = KC > 0 ? KC : K;
+        const int lane = threadIdx.x & 31;
+        const int n0 = n0c + lane * VC;
+        const bool valid = n0 < N;
+        int j[VC];
+#pragma unroll
+        for (int c = 0; c < VC; c++) j[c] = 0;
+        if (valid) {
+            const T* col = rob + n0;
+            T sf[VC], fin[VC];
+            uint32_t mx = 0;
+            if constexpr (KC > 0) {
+                T x[KC][VC];
+#pragma unroll
+                for (int k = 0; k < KC; k++) CW::load_row(col + k * N, x[k]);
+#pragma unroll
+                for (int k = 0; k < KC; k++)
+#pragma unroll
+                    for (int c = 0; c < VC; c++) mx = max(mx, CW::sexp(x[k][c]));
+#pragma unroll
+                for (int c = 0; c < VC; c++) {
+                    sf[c] = x[0][c];
+#pragma unroll
+                    for (int k = 1; k < KC - 1; k++) sf[c] = CW::add_rn(sf[c], x[k][c]);
+                    fin[c] = x[KC - 1][c];
+                }
+            } else {
+                for (int k = 0; k < Kr; k++) {
+                    T x[VC];
+                    CW::load_row(col + k * N, x);
+#pragma unroll
+                    for (int c = 0; c < VC; c++) {
+                        mx = max(mx, CW::sexp(x[c]));
+                        if (k == 0) sf[c] = x[c];
+                        else if (k < Kr - 1) sf[c] = CW::add_rn(sf[c], x[c]);
+                        else fin[c] = x[c];
+                    }
+                }
+            }
+            const bool bad = mx >= CW::kBad;
+            bool und[VC];
+            T rho[VC];
+#pragma unroll
+            for (int c = 0; c < VC; c++) {
+                j[c] = filter(sf[c], fin[c], rho[c], und[c]);
+                und[c] = und[c] || bad;
+            }
+            if (bad) fl |= check_all(col);
+#pragma unroll
+            for (int c = 0; c < VC; c++)
+                if (und[c]) {
+                    int jj = bad ? -1 : search(sf[c], rho[c]);
+                    if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
+                    j[c] = jj;
+                }
+        }
+        __syncwarp();
+        int jt = carry;
+#pragma unroll
+        for (int c = 0; c < VC; c++) jt = max(jt, j[c]);
+        // inclusive max-scan over the lanes (columns ascend with the lane)
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, jt, d);
+            if (lane >= d) jt = max(jt, o);
+        }
+        int cur = __shfl_up_sync(0xffffffffu, jt, 1);
+        if (lane == 0) cur = carry;
+        if (valid && jt > cur) {
+#pragma unroll
+            for (int c = 0; c < VC; c++)
+                if (j[c] > cur) {
+                    step(cur, j[c], n0 + c, r);
+                    cur = j[c];
+                }
+        }
+        return __shfl_sync(0xffffffffu, jt, 31);
+    }
+
     __device__ __forceinline__ void tile(const TileView& v, int64_t r0, int nr, int) {
         const T* u = reinterpret_cast<const T*>(v.seg[0]);
         uint32_t fl = 0;
@@ -198,85 +282,15 @@ struct SweepWork {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         if (warp >= cw) return;  // the producer warp's slot in the non-TMA modes
         const int KN = Kr * N;
+        const bool one_chunk = N <= 32 * VC;  // the common shapes (N <= 64 at VC = 2)
         for (int rr = warp; rr < nr; rr += cw) {
             const T* rob = u + rr * KN;
-            int carry = 0;  // M of the previous chunk's last column
-            for (int n0c = 0; n0c < N; n0c += 32 * VC) {
-                const int n0 = n0c + lane * VC;
-                const bool valid = n0 < N;
-                int j[VC];
-#pragma unroll
-                for (int c = 0; c < VC; c++) j[c] = 0;
-                if (valid) {
-                    const T* col = rob + n0;
-                    T sf[VC], fin[VC];
-                    uint32_t mx = 0;
-                    if constexpr (KC > 0) {
-                        T x[KC][VC];
-#pragma unroll
-                        for (int k = 0; k < KC; k++) CW::load_row(col + k * N, x[k]);
-#pragma unroll
-                        for (int k = 0; k < KC; k++)
-#pragma unroll
-                            for (int c = 0; c < VC; c++) mx = max(mx, CW::sexp(x[k][c]));
-#pragma unroll
-                        for (int c = 0; c < VC; c++) {
-                            sf[c] = x[0][c];
-#pragma unroll
-                            for (int k = 1; k < KC - 1; k++) sf[c] = CW::add_rn(sf[c], x[k][c]);
-                            fin[c] = x[KC - 1][c];
-                        }
-                    } else {
-                        for (int k = 0; k < Kr; k++) {
-                            T x[VC];
-                            CW::load_row(col + k * N, x);
-#pragma unroll
-                            for (int c = 0; c < VC; c++) {
-                                mx = max(mx, CW::sexp(x[c]));
-                                if (k == 0) sf[c] = x[c];
-                                else if (k < Kr - 1) sf[c] = CW::add_rn(sf[c], x[c]);
-                                else fin[c] = x[c];
-                            }
-                        }
-                    }
-                    const bool bad = mx >= CW::kBad;
-                    bool und[VC];
-                    T rho[VC];
-#pragma unroll
-                    for (int c = 0; c < VC; c++) {
-                        j[c] = filter(sf[c], fin[c], rho[c], und[c]);
-                        und[c] = und[c] || bad;
-                    }
-                    if (bad) fl |= check_all(col);
-#pragma unroll
-                    for (int c = 0; c < VC; c++)
-                        if (und[c]) {
-                            int jj = bad ? -1 : search(sf[c], rho[c]);
-                            if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
-                            j[c] = jj;
-                        }
-                }
-                __syncwarp();
-                int jt = carry;
-#pragma unroll
-                for (int c = 0; c < VC; c++) jt = max(jt, j[c]);
-                // inclusive max-scan over the lanes (columns ascend with the lane)
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int o = __shfl_up_sync(0xffffffffu, jt, d);
-                    if (lane >= d) jt = max(jt, o);
-                }
-                int cur = __shfl_up_sync(0xffffffffu, jt, 1);
-                if (lane == 0) cur = carry;
-                if (valid && jt > cur) {
-#pragma unroll
-                    for (int c = 0; c < VC; c++)
-                        if (j[c] > cur) {
-                            step(cur, j[c], n0 + c, r0 + rr);
-                            cur = j[c];
-                        }
-                }
-                carry = __shfl_sync(0xffffffffu, jt, 31);
+            int carry;
+            if (one_chunk) {
+                carry = chunk(rob, 0, 0, r0 + rr, fl);
+            } else {
+                carry = 0;  // M of the previous chunk's last column
+                for (int n0c = 0; n0c < N; n0c += 32 * VC) carry = chunk(rob, n0c, carry, r0 + rr, fl);
             }
             // slots never tripped take the whole chunk (>= every floor)
             if (lane == 0 && carry < Cc) {

@@ -467,53 +467,96 @@ def run_e2e(args, world, soa, prev, cand, off, sched):
         outs["skip"].copy_(fleet.t["skipped"], non_blocking=True)
         outs["edge"][: o.edge_keys.shape[0]].copy_(o.edge_keys, non_blocking=True)
 
-    # ---- streaming rounds ----
+    # ---- streaming rounds (pipelined) ----
+    # The next step's H2D runs on a copy stream while this step computes and
+    # reads back: device chunks rotate through a ring of three (new, prev, and
+    # the one being filled) and the per-request scalars through two staging
+    # sets, each with its own fleet view (history and skip counters shared) and
+    # its own captured graphs, so no device-to-device copy queues behind the
+    # next step's transfer.  Every step still moves its own inputs in and its
+    # results out inside the timed region.
     h_chunks = [cand[:, 0].cpu().pin_memory(), prev.cpu().pin_memory()]  # alternate A, B
-    d_chunks = [torch.empty_like(prev), torch.empty_like(prev)]
-    d_chunks[1].copy_(h_chunks[1])
+    ring = [torch.empty_like(prev) for _ in range(3)]
     fleet = fl.DeviceFleet.from_host(soa)
     per_round = ("issued_at", "obs_captured_at", "remaining")
     h_sc = {k: torch.from_numpy(np.ascontiguousarray(soa[k])).pin_memory() for k in per_round}
     h_off = off.cpu().pin_memory()
     d_off = torch.empty_like(off)
-    inp = [rounds.DivergenceInputs(d_chunks[1], d_chunks[0], THR, offset=d_off),
-           rounds.DivergenceInputs(d_chunks[0], d_chunks[1], THR, offset=d_off)]
+    stage = [{k: fleet.t[k] if si == 0 else torch.empty_like(fleet.t[k]) for k in per_round}
+             for si in range(2)]
+    stage_off = [d_off, torch.empty_like(off)]
+    views = [fl.DeviceFleet.from_tensors({**fleet.t, **stage[si]}) for si in range(2)]
+    inp6 = [[rounds.DivergenceInputs(ring[(a + 2) % 3], ring[a], THR, offset=stage_off[si])
+             for si in range(2)] for a in range(3)]
     if graphs:
-        rnd.run(fleet, inp[0])
+        rnd.run(views[0], inp6[0][0])
         torch.cuda.synchronize()
-        g_h = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
-        for j in range(2):
-            with torch.cuda.graph(g_h[j]):
-                rnd.horizons(inp[j])
-        g_d = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_d):
-            rnd.urgency(fleet)
-            rnd.admit(fleet)
+        g_h = [[torch.cuda.CUDAGraph() for _ in range(2)] for _ in range(3)]
+        for a in range(3):
+            for si in range(2):
+                with torch.cuda.graph(g_h[a][si]):
+                    rnd.horizons(inp6[a][si])
+        g_d = [torch.cuda.CUDAGraph() for _ in range(2)]
+        for si in range(2):
+            with torch.cuda.graph(g_d[si]):
+                rnd.urgency(views[si])
+                rnd.admit(views[si])
+    cs = torch.cuda.current_stream()
+    xs = torch.cuda.Stream()
 
-    def stream_step(i):
-        j = i & 1
-        d_chunks[j].copy_(h_chunks[j], non_blocking=True)
-        d_off.copy_(h_off, non_blocking=True)
-        for k, v in h_sc.items():
-            fleet.t[k].copy_(v, non_blocking=True)
-        if graphs:
-            g_h[j].replay()
-            g_d.replay()
-            o = rnd.outputs()
-        else:
-            o = rnd.run(fleet, inp[j])
-        read_back(o, fleet)
+    def run_steps(steps, start_evt):
+        h2d = [torch.cuda.Event() for _ in range(steps)]
+        done = [torch.cuda.Event() for _ in range(steps)]
+        for i in range(steps):
+            a, si = i % 3, i % 2
+            with torch.cuda.stream(xs):
+                if i == 0:
+                    xs.wait_event(start_evt)
+                if i >= 2:  # ring slot / staging set last read by step i - 2
+                    xs.wait_event(done[i - 2])
+                ring[a].copy_(h_chunks[i & 1], non_blocking=True)
+                stage_off[si].copy_(h_off, non_blocking=True)
+                for k, v in h_sc.items():
+                    stage[si][k].copy_(v, non_blocking=True)
+                h2d[i].record(xs)
+            cs.wait_event(h2d[i])
+            if graphs:
+                g_h[a][si].replay()
+                g_d[si].replay()
+                o = rnd.outputs()
+            else:
+                o = rnd.run(views[si], inp6[a][si])
+            read_back(o, views[si])
+            done[i].record(cs)
 
     h2d_stream = h_chunks[0].numel() * 4 + h_off.numel() * 4 + sum(
         v.numel() * v.element_size() for v in h_sc.values())
     steps = max(2, min(args.steps, args.e2e_steps))
-    t = _timed(stream_step, steps, world)
+    ring[2].copy_(h_chunks[1])  # the previous chunk of step 0 (last round's, resident)
+    w0 = torch.cuda.Event()
+    w0.record(cs)
+    run_steps(2, w0)  # warm-up
+    ring[2].copy_(h_chunks[1])
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(cs)
+    run_steps(steps, s0)
+    e0.record(cs)
+    torch.cuda.synchronize()
+    el = torch.tensor([s0.elapsed_time(e0) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    t = float(el.item())
     stream = {"value": R * world * steps / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d_stream),
               "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": 1e3 * t / steps,
               "path": "streaming round through the C ABI: pinned host -> H2D of the new chunk "
                       "[R,50,7] fp32 + per-request scalars (issued_at, obs_captured_at, remaining, "
                       "offset); previous chunk (last round's) and fleet history device-resident; "
-                      "D2H of horizons, need times, masks, skip counters, ordered S_e"}
+                      "D2H of horizons, need times, masks, skip counters, ordered S_e; the next "
+                      "step's H2D (copy stream) overlaps this step's compute and D2H"}
 
     # ---- cold rounds: every input copied ----
     h_prev, h_cand = prev.cpu().pin_memory(), cand.cpu().pin_memory()

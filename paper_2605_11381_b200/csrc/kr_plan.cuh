@@ -51,6 +51,9 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
     static const int max_override = std::getenv("KR_PLAN_MAX_THREADS")
                                         ? std::atoi(std::getenv("KR_PLAN_MAX_THREADS")) : 0;
     if (max_override >= 32 && max_override < max_threads) max_threads = max_override;
+    static const int tr_override = std::getenv("KR_PLAN_FORCE_TR")
+                                       ? std::atoi(std::getenv("KR_PLAN_FORCE_TR")) : 0;
+    if (tr_override > 0 && force_tr == 0) force_tr = tr_override;  // debug knob (sweeps)
     static const int rounds_override = std::getenv("KR_PLAN_MIN_ROUNDS")
                                            ? std::atoi(std::getenv("KR_PLAN_MIN_ROUNDS")) : 0;
     if (rounds_override >= 1 && rounds_override <= kMaxRounds) min_rounds = rounds_override;

@@ -283,7 +283,7 @@ def run_ours(args, world, rank, local_rank):
         gd[0].record(stream); rnd.g_decide.replay(); gd[1].record(stream)
         torch.cuda.synchronize()
         breakdown["urgency_plus_admission_graph_ms"] = gd[0].elapsed_time(gd[1])
-        if args.reserve_sms > 0:  # the side stream inside the timed rounds (concurrent)
+        if args.reserve_sms != 0:  # the side stream inside the timed rounds (concurrent)
             breakdown["side_stream_ms_in_round"] = statistics.mean(
                 a.elapsed_time(b) for a, b in sev)
         breakdown["reserve_sms"] = args.reserve_sms
@@ -597,7 +597,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--eager", action="store_true",
                     help="N=1: the N>1 path (eager launches, side-stream overlap) instead of graphs")
-    ap.add_argument("--reserve-sms", type=int, default=12,
+    ap.add_argument("--reserve-sms", type=int, default=4,
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
     ap.add_argument("--layout", choices=["split", "urgency_first"], default="urgency_first",
                     help="graph layout of the round (see rounds.DecisionRound.capture)")

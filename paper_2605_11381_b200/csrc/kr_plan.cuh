@@ -27,7 +27,7 @@ namespace kr {
 static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* rbytes, int64_t R,
                             int items_per_robot, uint32_t aux_per_robot, int max_threads,
                             int regs_per_thread, int min_rounds = 1, uint32_t aux_fixed = 256,
-                            int force_tr = 0) {
+                            int force_tr = 0, int max_stages = kMaxStages) {
     const DeviceInfo& di = device_info();
     StreamPlan p{};
     p.nseg = nseg;
@@ -84,7 +84,10 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
         if (per_sm < 1) continue;
         const uint64_t budget = smem_sm / per_sm - 1024 - 128;
         int stages = static_cast<int>((budget - aux) / sb);
-        stages = stages > kMaxStages ? kMaxStages : stages;
+        stages = stages > max_stages ? max_stages : stages;
+        static const int max_stages_env = std::getenv("KR_PLAN_MAX_STAGES")
+                                              ? std::atoi(std::getenv("KR_PLAN_MAX_STAGES")) : 0;
+        if (max_stages_env >= 2 && stages > max_stages_env) stages = max_stages_env;  // debug knob
         const double inflight = static_cast<double>(per_sm) * (stages - 1) * sb;
         const double warps = per_sm * cta / 32.0;
         double score = 1.0 - static_cast<double>(items) / (static_cast<double>(rounds) * threads);

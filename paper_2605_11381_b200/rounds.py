@@ -177,6 +177,8 @@ class DecisionRound:
         if layout not in ("split", "urgency_first"):
             raise ValueError(f"unknown round layout {layout!r}")
         self.layout = layout
+        # reserve_sms < 0: concurrent without an SM cap (side kernels co-reside
+        # wherever the horizon kernel leaves room)
         self.max_sms = 0 if reserve_sms <= 0 else max(1, torch.cuda.get_device_properties(
             self.H.device).multi_processor_count - reserve_sms)
         self.run(fleet, h)  # warm-up: attribute / occupancy caches, lazy loading
@@ -195,7 +197,7 @@ class DecisionRound:
             with torch.cuda.graph(self.g_decide):
                 self.urgency(fleet)
                 self.admit(fleet)
-        self.side = torch.cuda.Stream(device=self.H.device) if reserve_sms > 0 else None
+        self.side = torch.cuda.Stream(device=self.H.device) if reserve_sms != 0 else None
 
     def replay_concurrent(self, before_horizon=None, after_horizon=None, before_side=None,
                           after_side=None) -> None:
@@ -236,7 +238,7 @@ class DecisionRound:
         self.replay_concurrent()
         return self.outputs()
 
-    def run_overlapped(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 12,
+    def run_overlapped(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 4,
                        before_horizon=None, after_horizon=None,
                        layout: str = "urgency_first") -> RoundOutputs:
         """One eager round with the graph path's overlap (see `capture`): the

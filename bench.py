@@ -309,6 +309,7 @@ def run_ours(args, world, rank, local_rank):
                      "algorithmic_bytes_per_robot_round": DIV_BYTES,
                      "launch_ms_mean": statistics.mean(div_ms),
                      "traffic_source": traffic_src},
+        "round_roofline": round_roofline(soa, R, elapsed / args.steps, peak),
         "kernels": breakdown,
         "gpu_launches": int(launches),
         "cuda_graphs": bool(graphs),
@@ -347,6 +348,22 @@ def _timed(step, steps, world):
     if world > 1:
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
     return float(el.item())
+
+
+def round_roofline(soa, R, t_round, peak):
+    """The whole round against HBM: algorithmic bytes of every step (horizon
+    2,808 B + urgency's fleet fields, history slots and outputs + admission's
+    key / observation / skip-counter / mask traffic) over the measured round
+    time -- the horizon kernel shares HBM with the concurrent side stream, so
+    its own fraction understates how busy the memory system is."""
+    slots = int(np.maximum(soa["n_exec"], soa["n_gen"]).sum())
+    urg = R * (8 * 3 + 4 * 5) + slots * 32 + R * (16 + 8)  # fields in, history, key + need out
+    adm = R * (16 + 8 + 4 + 4 + 2)  # key, obs, skipped RMW, admitted + refetch masks
+    total = R * DIV_BYTES + urg + adm
+    gbs = total / t_round / 1e9
+    return {"bytes_per_robot_round": total / R, "achieved": gbs, "peak": peak, "unit": "GB/s",
+            "frac": gbs / peak,
+            "note": "horizon + urgency + admission bytes of one round over the round time"}
 
 
 def other_configs(reps: int = 200):
@@ -597,9 +614,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--eager", action="store_true",
                     help="N=1: the N>1 path (eager launches, side-stream overlap) instead of graphs")
-    ap.add_argument("--reserve-sms", type=int, default=4,
+    ap.add_argument("--reserve-sms", type=int, default=8,
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
-    ap.add_argument("--layout", choices=["split", "urgency_first"], default="urgency_first",
+    ap.add_argument("--layout", choices=["split", "urgency_first"], default="split",
                     help="graph layout of the round (see rounds.DecisionRound.capture)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="diagnostic: the N>1 sharded round (local select, all-gather, global "

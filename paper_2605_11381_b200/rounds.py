@@ -238,9 +238,9 @@ class DecisionRound:
         self.replay_concurrent()
         return self.outputs()
 
-    def run_overlapped(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 4,
+    def run_overlapped(self, fleet: fl.DeviceFleet, h: DivergenceInputs, reserve_sms: int = 8,
                        before_horizon=None, after_horizon=None,
-                       layout: str = "urgency_first") -> RoundOutputs:
+                       layout: str = "split") -> RoundOutputs:
         """One eager round with the graph path's overlap (see `capture`): the
         horizon kernel on the current stream over all but `reserve_sms` SMs and
         the admission (for a sharded round: local select, the NCCL all-gather

@@ -442,10 +442,21 @@ def other_configs(reps: int = 200):
     U = synthetic.magnitudes(R, seed=19)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))
-    t = timed(lambda: rnd.run(fleet, inp))
+    rnd.capture(fleet, inp, reserve_sms=8, layout="split")
+    for _ in range(5):
+        rnd.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(reps):
+        rnd.replay()
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3 / reps
     out["configs[4] per-GPU share, confidence policy (U 2^20 x 6 x 50 fp32), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
-        "l2": "streams from HBM (1.26 GB of magnitudes)", "layout": "serial eager-graph round"}
+        "l2": "streams from HBM (1.26 GB of magnitudes)",
+        "layout": "split: horizons || urgency + admission (8 reserved SMs)"}
     return out
 
 

@@ -99,11 +99,13 @@ __device__ __noinline__ int sweep_exact(const T* col, int K, int N, const double
 // (Measured alternative, not kept: G = 4 / 8 lanes per robot with register-held
 // per-lane column blocks cut instructions 2x but the smem-bounded tile leaves
 // too few warps per SM -- 36% vs 42% of the HBM peak at C = 16.)
-template <typename T, int KC, int VC>
+// HALF: two robots per warp (16 lanes x 4 columns, N <= 64 and even).
+template <typename T, int KC, int VC, bool HALF = false>
 struct SweepWork {
     using CW = ConfWork<T, KC, VC>;
     using Elem = T;
     static constexpr int kVC = VC;
+    static constexpr bool kHalf = HALF;
     int K, N, TR, C, Cc, maxcap, half;
     int cw;                      // consumer warps (robots are dealt round-robin to them)
     int lut_n, lut_shift;
@@ -275,6 +277,78 @@ struct SweepWork {
         return __shfl_sync(0xffffffffu, jt, 31);
     }
 
+    // Half-warp robot: lane g of the 16 owns columns 4g .. 4g + 3 (pairs are
+    // whole: N is even), loaded as two 2-element vectors per row.
+    __device__ __forceinline__ static void load_pair(const T* p, T& a, T& b) {
+        if constexpr (sizeof(T) == 4) {
+            const float2 v = *reinterpret_cast<const float2*>(p);
+            a = v.x; b = v.y;
+        } else {
+            const double2 v = *reinterpret_cast<const double2*>(p);
+            a = v.x; b = v.y;
+        }
+    }
+
+    __device__ __forceinline__ int chunk_half(const T* rob, bool robot_ok, int64_t r,
+                                              uint32_t& fl) const {
+        const int Kr = KC > 0 ? KC : K;
+        const int g = threadIdx.x & 15;
+        const int n0 = 4 * g;
+        const bool p0 = robot_ok && n0 < N, p1 = robot_ok && n0 + 2 < N;
+        int j[4] = {0, 0, 0, 0};
+        if (p0) {
+            const T* col = rob + n0;
+            T sf[4], fin[4];
+            uint32_t mx = 0;
+            for (int k = 0; k < Kr; k++) {
+                T x[4] = {T(0), T(0), T(0), T(0)};
+                load_pair(col + k * N, x[0], x[1]);
+                if (p1) load_pair(col + k * N + 2, x[2], x[3]);
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    mx = max(mx, CW::sexp(x[c]));
+                    if (k == 0) sf[c] = x[c];
+                    else if (k < Kr - 1) sf[c] = CW::add_rn(sf[c], x[c]);
+                    else fin[c] = x[c];
+                }
+            }
+            const bool bad = mx >= CW::kBad;
+            if (bad)
+                for (int k = 0; k < Kr; k++)
+                    for (int c = 0; c < (p1 ? 4 : 2); c++) fl |= CW::check(col[k * N + c]);
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                if (c >= 2 && !p1) break;
+                T rho;
+                bool und;
+                int jj = filter(sf[c], fin[c], rho, und);
+                if (und || bad) {
+                    jj = bad ? -1 : search(sf[c], rho);
+                    if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
+                }
+                j[c] = jj;
+            }
+        }
+        __syncwarp();
+        int jt = max(max(j[0], j[1]), max(j[2], j[3]));
+#pragma unroll
+        for (int d = 1; d < 16; d <<= 1) {  // max-scan within the 16-lane half
+            const int o = __shfl_up_sync(0xffffffffu, jt, d, 16);
+            if (g >= d) jt = max(jt, o);
+        }
+        int cur = __shfl_up_sync(0xffffffffu, jt, 1, 16);
+        if (g == 0) cur = 0;
+        if (p0 && jt > cur) {
+#pragma unroll
+            for (int c = 0; c < 4; c++)
+                if ((c < 2 || p1) && j[c] > cur) {
+                    step(cur, j[c], n0 + c, r);
+                    cur = j[c];
+                }
+        }
+        return __shfl_sync(0xffffffffu, jt, 15, 16);
+    }
+
     __device__ __forceinline__ void tile(const TileView& v, int64_t r0, int nr, int) {
         const T* u = reinterpret_cast<const T*>(v.seg[0]);
         uint32_t fl = 0;
@@ -282,6 +356,25 @@ struct SweepWork {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         if (warp >= cw) return;  // the producer warp's slot in the non-TMA modes
         const int KN = Kr * N;
+        if constexpr (HALF) {
+            const int g = lane & 15;
+            for (int rb = warp * 2; rb < nr; rb += cw * 2) {
+                const int rr = rb + (lane >> 4);
+                const bool ok = rr < nr;
+                const int total = chunk_half(u + (ok ? rr : 0) * KN, ok, r0 + rr, fl);
+                if (ok && g == 0 && total < Cc) {  // slots never tripped take N
+                    atomicAdd(&tab->D[total], static_cast<uint32_t>(N));
+                    if (H)
+                        for (int c = total; c < Cc; c++)
+                            H[static_cast<int64_t>(tab->orig[c]) * R + r0 + rr] = N;
+                }
+                if (ok && H)
+                    for (int c = Cc + g; c < C; c += 16)
+                        H[static_cast<int64_t>(tab->orig[c]) * R + r0 + rr] = tab->hcap[c];
+            }
+            if (fl && flags) atomicOr(flags, fl);
+            return;
+        }
         const bool one_chunk = N <= 32 * VC;  // the common shapes (N <= 64 at VC = 2)
         for (int rr = warp; rr < nr; rr += cw) {
             const T* rob = u + rr * KN;
@@ -311,9 +404,9 @@ struct SweepWork {
 
 constexpr int kSweepThreads = 384;
 
-template <typename T, int KC, int VC, bool kStaged>
+template <typename T, int KC, int VC, bool kStaged, bool HALF = false>
 __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p,
-                                                                         SweepWork<T, KC, VC> w,
+                                                                         SweepWork<T, KC, VC, HALF> w,
                                                                          const __grid_constant__ SweepCfg cfg) {
     extern __shared__ __align__(128) unsigned char smem[];
     w.tab = reinterpret_cast<SweepTables*>(smem + stream_aux_offset());
@@ -362,8 +455,9 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
         // a warp per robot (32 "items"): 11 consumer warps x 2 robots per tile,
         // two CTAs (24 warps) per SM -- the per-robot scan is instruction-heavy,
         // so warps, not bytes in flight, set the pace
-        StreamPlan p = make_plan(1, bases, &rb, R, 32, 0, kSweepThreads - 32, kernel_regs(kstaged),
-                                 2, static_cast<uint32_t>(sizeof(SweepTables)), 22);
+        StreamPlan p = make_plan(1, bases, &rb, R, W::kHalf ? 16 : 32, 0, kSweepThreads - 32,
+                                 kernel_regs(kstaged), 2,
+                                 static_cast<uint32_t>(sizeof(SweepTables)), W::kHalf ? 44 : 22);
         // per-CTA 32-bit sums: robots per CTA (grid >= SMs) x N < 2^32
         if ((R / device_info().sm_count + 1) * static_cast<int64_t>(N) >= (int64_t(1) << 32))
             return KR_EINVAL;
@@ -384,6 +478,15 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
     if (al && sizeof(T) == 4 && N % 4 == 0 && N > 64) vc = 4;
 #define KR_SWEEP(KK, VV) \
     return go(SweepWork<T, KK, VV>{}, k_horizon_sweep<T, KK, VV, true>, k_horizon_sweep<T, KK, VV, false>)
+    // two robots per warp: N <= 64, even, 16-byte aligned base
+    static const bool half_off = std::getenv("KR_SWEEP_NO_HALF") != nullptr;  // A/B knob
+    if (!half_off && N <= 64 && N % 2 == 0 && al) {
+        if (K == 6)
+            return go(SweepWork<T, 6, 1, true>{}, k_horizon_sweep<T, 6, 1, true, true>,
+                      k_horizon_sweep<T, 6, 1, false, true>);
+        return go(SweepWork<T, 0, 1, true>{}, k_horizon_sweep<T, 0, 1, true, true>,
+                  k_horizon_sweep<T, 0, 1, false, true>);
+    }
     if constexpr (sizeof(T) == 4) {
         if (vc == 4) KR_SWEEP(0, 4);
         if (vc == 2) {

@@ -69,7 +69,7 @@ struct SweepTables {
     // (R / grid robots, N columns, horizons <= N) is < 2^32; checked on the host
     uint32_t D[kSweepMaxCfg + 1];  // difference array of the per-slot sums (mod 2^32)
     uint32_t F[kSweepMaxCfg];      // min_horizon floor corrections
-    uint16_t lut[kSweepLut];
+    uint16_t lut[kSweepLut + 2];   // [0]: below the table (0), [lut_n + 1]: above (Cc)
 };
 
 // Bit-exact count of tripping confidence configurations for one column.
@@ -109,7 +109,8 @@ struct SweepWork {
     int K, N, TR, C, Cc, maxcap, half;
     int cw;                      // consumer warps (robots are dealt round-robin to them)
     int lut_n, lut_shift;
-    uint64_t lut_lo, lut_hi;
+    uint64_t lut_lo;
+    uint64_t sfminb, sfrng;      // storage-type bits: sums in [sfmin, sfmin + sfrng] filter
     T sfmin, sfmax;
     int32_t* H;                  // [C][R] (nullable)
     unsigned long long* sums;    // [C]
@@ -129,30 +130,39 @@ struct SweepWork {
     // with one lookup; buckets that straddle a slot bound fall back to a
     // branch-free binary search.  f == 0 never trips; an exact zero mean trips
     // on any f > 0.
-    // Branch-free common path: the bucket lookup and the zero rules; `und`
-    // marks columns that need search() (ambiguous bucket, sum out of range).
-    __device__ __forceinline__ int filter(T sf, T fin, T& rho, bool& und) const {
+    // Branch-free: the bucket lookup (entry 0 / lut_n + 1 stand for the ratios
+    // below / above the table) and the zero rules; returns -1 for the columns
+    // that need search() (ambiguous bucket, sum out of range).  f == 0 gives
+    // ratio bits 0 (below: no trip); sum == 0 < f gives +inf (above: all trip).
+    __device__ __forceinline__ int filter(T sf, T fin) const {
         using B = typename std::conditional<sizeof(T) == 4, uint32_t, uint64_t>::type;
-        B bits;
+        using SB = typename std::make_signed<B>::type;
+        B bits, sb;
         if constexpr (sizeof(T) == 4) {
             float r;
             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(sf));  // <= 1 ulp, sf normal
-            rho = __fmul_rn(fin, r);
-            bits = __float_as_uint(rho);
+            bits = __float_as_uint(__fmul_rn(fin, r));
+            sb = __float_as_uint(sf);
         } else {
-            rho = __dmul_rn(fin, __drcp_rn(sf));
-            bits = static_cast<uint64_t>(__double_as_longlong(rho));
+            bits = static_cast<uint64_t>(__double_as_longlong(__dmul_rn(fin, __drcp_rn(sf))));
+            sb = static_cast<uint64_t>(__double_as_longlong(sf));
         }
-        const B lo = static_cast<B>(lut_lo), hi = static_cast<B>(lut_hi);
-        const bool below = bits < lo, above = bits >= hi;
-        const uint32_t off = below || above ? 0u : static_cast<uint32_t>((bits - lo) >> lut_shift);
-        const unsigned e = tab->lut[off];
-        int j = below ? 0 : (above ? Cc : static_cast<int>(e));
-        und = !below && !above && e == 0xFFFFu;
-        und = und || !(sf >= sfmin && sf <= sfmax);
-        if (sf == T(0)) { j = Cc; und = false; }
-        if (fin == T(0)) { j = 0; und = false; }
-        return j;
+        if (fin == T(0)) bits = 0;
+        SB idx = (static_cast<SB>(bits - static_cast<B>(lut_lo)) >> lut_shift) + 1;
+        idx = idx < 0 ? 0 : (idx > lut_n + 1 ? lut_n + 1 : idx);
+        const int e = tab->lut[idx];
+        const bool out = static_cast<B>(sb - static_cast<B>(sfminb)) > static_cast<B>(sfrng) && sb != 0;
+        return e == 0xFFFF || out ? -1 : e;
+    }
+
+    __device__ __forceinline__ static T ratio(T sf, T fin) {
+        if constexpr (sizeof(T) == 4) {
+            float r;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(sf));
+            return __fmul_rn(fin, r);
+        } else {
+            return __dmul_rn(fin, __drcp_rn(sf));
+        }
     }
 
     // ambiguous bucket: branch-free binary search over the slot bounds
@@ -238,21 +248,22 @@ struct SweepWork {
                 }
             }
             const bool bad = mx >= CW::kBad;
-            bool und[VC];
-            T rho[VC];
+            bool any = bad;
 #pragma unroll
             for (int c = 0; c < VC; c++) {
-                j[c] = filter(sf[c], fin[c], rho[c], und[c]);
-                und[c] = und[c] || bad;
+                j[c] = filter(sf[c], fin[c]);
+                any = any || j[c] < 0;
             }
-            if (bad) fl |= check_all(col);
+            if (any) {
+                if (bad) fl |= check_all(col);
 #pragma unroll
-            for (int c = 0; c < VC; c++)
-                if (und[c]) {
-                    int jj = bad ? -1 : search(sf[c], rho[c]);
-                    if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
-                    j[c] = jj;
-                }
+                for (int c = 0; c < VC; c++)
+                    if (bad || j[c] < 0) {
+                        int jj = bad ? -1 : search(sf[c], ratio(sf[c], fin[c]));
+                        if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
+                        j[c] = jj;
+                    }
+            }
         }
         __syncwarp();
         int jt = carry;
@@ -312,21 +323,25 @@ struct SweepWork {
                     else fin[c] = x[c];
                 }
             }
+            // the padding pair of a lane past N is zeros: filter() gives 0
             const bool bad = mx >= CW::kBad;
-            if (bad)
-                for (int k = 0; k < Kr; k++)
-                    for (int c = 0; c < (p1 ? 4 : 2); c++) fl |= CW::check(col[k * N + c]);
+            bool any = bad;
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                if (c >= 2 && !p1) break;
-                T rho;
-                bool und;
-                int jj = filter(sf[c], fin[c], rho, und);
-                if (und || bad) {
-                    jj = bad ? -1 : search(sf[c], rho);
-                    if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
-                }
-                j[c] = jj;
+                j[c] = filter(sf[c], fin[c]);
+                any = any || j[c] < 0;
+            }
+            if (any) {
+                const int nc = p1 ? 4 : 2;
+                if (bad)
+                    for (int k = 0; k < Kr; k++)
+                        for (int c = 0; c < nc; c++) fl |= CW::check(col[k * N + c]);
+                for (int c = 0; c < nc; c++)
+                    if (bad || j[c] < 0) {
+                        int jj = bad ? -1 : search(sf[c], ratio(sf[c], fin[c]));
+                        if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
+                        j[c] = jj;
+                    }
             }
         }
         __syncwarp();
@@ -341,7 +356,7 @@ struct SweepWork {
         if (p0 && jt > cur) {
 #pragma unroll
             for (int c = 0; c < 4; c++)
-                if ((c < 2 || p1) && j[c] > cur) {
+                if (j[c] > cur) {
                     step(cur, j[c], n0 + c, r);
                     cur = j[c];
                 }
@@ -410,7 +425,11 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p
                                                                          const __grid_constant__ SweepCfg cfg) {
     extern __shared__ __align__(128) unsigned char smem[];
     w.tab = reinterpret_cast<SweepTables*>(smem + stream_aux_offset());
-    for (int i = threadIdx.x; i < w.lut_n; i += blockDim.x) w.tab->lut[i] = cfg.lut[i];
+    for (int i = threadIdx.x; i < w.lut_n; i += blockDim.x) w.tab->lut[i + 1] = cfg.lut[i];
+    if (threadIdx.x == 0) {
+        w.tab->lut[0] = 0;
+        w.tab->lut[w.lut_n + 1] = static_cast<uint16_t>(w.Cc);
+    }
     for (int i = threadIdx.x; i < kSweepPad; i += blockDim.x) {
         w.tab->rhd[i] = cfg.rh[i];
         w.tab->rld[i] = cfg.rl[i];
@@ -467,7 +486,21 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
         w.cw = p.threads / 32;
         w.sfmin = static_cast<T>(cfg.sfmin);
         w.sfmax = static_cast<T>(cfg.sfmax);
-        w.lut_n = cfg.lut_n; w.lut_shift = cfg.lut_shift; w.lut_lo = cfg.lut_lo; w.lut_hi = cfg.lut_hi;
+        w.lut_n = cfg.lut_n; w.lut_shift = cfg.lut_shift; w.lut_lo = cfg.lut_lo;
+        if (cfg.sfmin <= cfg.sfmax) {
+            uint64_t lo, hi;
+            if constexpr (sizeof(T) == 4) {
+                const float a = static_cast<float>(cfg.sfmin), b = static_cast<float>(cfg.sfmax);
+                uint32_t ua, ub;
+                std::memcpy(&ua, &a, 4); std::memcpy(&ub, &b, 4);
+                lo = ua; hi = ub;
+            } else {
+                std::memcpy(&lo, &cfg.sfmin, 8); std::memcpy(&hi, &cfg.sfmax, 8);
+            }
+            w.sfminb = lo; w.sfrng = hi - lo;
+        } else {  // no sum filters (every nonzero sum is searched / exact)
+            w.sfminb = 0; w.sfrng = 0;
+        }
         w.H = H; w.sums = sums; w.flags = flags; w.R = R;
         return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_sweep", 0, cfg);
     };

@@ -288,8 +288,10 @@ struct SweepWork {
         return __shfl_sync(0xffffffffu, jt, 31);
     }
 
-    // Half-warp robot: lane g of the 16 owns columns 4g .. 4g + 3 (pairs are
-    // whole: N is even), loaded as two 2-element vectors per row.
+    // Half-warp robot: lane g of the 16 owns the column pairs 2g, 2g + 1 and
+    // 32 + 2g, 33 + 2g (pairs are whole: N is even), so the 16 lanes read each
+    // half-row as 128 contiguous bytes (conflict-free 8-byte loads); the max-scan
+    // runs over the first 32 columns, then over the second 32 from its total.
     __device__ __forceinline__ static void load_pair(const T* p, T& a, T& b) {
         if constexpr (sizeof(T) == 4) {
             const float2 v = *reinterpret_cast<const float2*>(p);
@@ -304,17 +306,16 @@ struct SweepWork {
                                               uint32_t& fl) const {
         const int Kr = KC > 0 ? KC : K;
         const int g = threadIdx.x & 15;
-        const int n0 = 4 * g;
-        const bool p0 = robot_ok && n0 < N, p1 = robot_ok && n0 + 2 < N;
+        const int n0 = 2 * g, n1 = 32 + 2 * g;
+        const bool p0 = robot_ok && n0 < N, p1 = robot_ok && n1 < N;
         int j[4] = {0, 0, 0, 0};
         if (p0) {
-            const T* col = rob + n0;
             T sf[4], fin[4];
             uint32_t mx = 0;
             for (int k = 0; k < Kr; k++) {
                 T x[4] = {T(0), T(0), T(0), T(0)};
-                load_pair(col + k * N, x[0], x[1]);
-                if (p1) load_pair(col + k * N + 2, x[2], x[3]);
+                load_pair(rob + k * N + n0, x[0], x[1]);
+                if (p1) load_pair(rob + k * N + n1, x[2], x[3]);
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
                     mx = max(mx, CW::sexp(x[c]));
@@ -333,35 +334,40 @@ struct SweepWork {
             }
             if (any) {
                 const int nc = p1 ? 4 : 2;
-                if (bad)
-                    for (int k = 0; k < Kr; k++)
-                        for (int c = 0; c < nc; c++) fl |= CW::check(col[k * N + c]);
-                for (int c = 0; c < nc; c++)
+                for (int c = 0; c < nc; c++) {
+                    const T* col = rob + (c < 2 ? n0 + c : n1 + c - 2);
+                    if (bad)
+                        for (int k = 0; k < Kr; k++) fl |= CW::check(col[k * N]);
                     if (bad || j[c] < 0) {
                         int jj = bad ? -1 : search(sf[c], ratio(sf[c], fin[c]));
-                        if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
+                        if (jj < 0) jj = sweep_exact(col, K, N, tab->p, Cc);
                         j[c] = jj;
                     }
+                }
             }
         }
         __syncwarp();
-        int jt = max(max(j[0], j[1]), max(j[2], j[3]));
+        int ja = max(j[0], j[1]), jb = max(j[2], j[3]);
 #pragma unroll
-        for (int d = 1; d < 16; d <<= 1) {  // max-scan within the 16-lane half
-            const int o = __shfl_up_sync(0xffffffffu, jt, d, 16);
-            if (g >= d) jt = max(jt, o);
+        for (int d = 1; d < 16; d <<= 1) {  // max-scans within the 16-lane half
+            const int oa = __shfl_up_sync(0xffffffffu, ja, d, 16);
+            const int ob = __shfl_up_sync(0xffffffffu, jb, d, 16);
+            if (g >= d) { ja = max(ja, oa); jb = max(jb, ob); }
         }
-        int cur = __shfl_up_sync(0xffffffffu, jt, 1, 16);
-        if (g == 0) cur = 0;
-        if (p0 && jt > cur) {
-#pragma unroll
-            for (int c = 0; c < 4; c++)
-                if (j[c] > cur) {
-                    step(cur, j[c], n0 + c, r);
-                    cur = j[c];
-                }
+        const int ta = __shfl_sync(0xffffffffu, ja, 15, 16);  // M after column 31
+        jb = max(jb, ta);
+        int ca = __shfl_up_sync(0xffffffffu, ja, 1, 16);
+        int cb = __shfl_up_sync(0xffffffffu, jb, 1, 16);
+        if (g == 0) { ca = 0; cb = ta; }
+        if (p0 && ja > ca) {
+            if (j[0] > ca) { step(ca, j[0], n0, r); ca = j[0]; }
+            if (j[1] > ca) step(ca, j[1], n0 + 1, r);
         }
-        return __shfl_sync(0xffffffffu, jt, 15, 16);
+        if (p1 && jb > cb) {
+            if (j[2] > cb) { step(cb, j[2], n1, r); cb = j[2]; }
+            if (j[3] > cb) step(cb, j[3], n1 + 1, r);
+        }
+        return __shfl_sync(0xffffffffu, jb, 15, 16);
     }
 
     __device__ __forceinline__ void tile(const TileView& v, int64_t r0, int nr, int) {

@@ -180,6 +180,17 @@ KR_API int kr_horizon_sweep(const void* U, int dtype, int64_t R, int32_t K, int3
  * H[r] = min_s round_optimal_horizon(ref_r, cand_{r,s}, thr).  offset /
  * len_prev / len_cand may be NULL (0 / Lp / Lc).  cos (nullable) receives the
  * fp64 cosine of every (r, s, i < limit_r), NaN beyond the limit. */
+/* Exact-cosine ddot order (workload.py:461-468 `_cosine` through numpy's
+ * OpenBLAS): the reference's fp64 cosines are those of the BLAS core numpy
+ * selected at run time, so the order is a process-wide setting that the host
+ * takes from threadpoolctl's report (OpenBLAS 0.3.30 cores SkylakeX /
+ * Cooperlake / SapphireRapids -> KR_DOT_SKYLAKEX, Haswell / Zen ->
+ * KR_DOT_HASWELL).  Read when a launch is set up.  Default KR_DOT_SKYLAKEX. */
+#define KR_DOT_SKYLAKEX 0
+#define KR_DOT_HASWELL  1
+KR_API int kr_set_dot_order(int32_t order);
+KR_API int32_t kr_get_dot_order(void);
+
 KR_API int kr_horizon_divergence(const void* prev, const void* cand, int dtype, int64_t R,
                           int32_t S, int32_t Lp, int32_t Lc, int32_t D,
                           const int32_t* offset, const int32_t* len_prev,

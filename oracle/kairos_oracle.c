@@ -66,7 +66,7 @@ double orc_np_mean_col(const double* u, int64_t rows, int64_t N, int64_t n) {
  * kernel (4 x 8-lane FMA accumulators over 32-blocks, folded to 4 x 4 lanes,
  * then 4 x 4-lane FMA over the remaining 16-blocks, lane-wise chain, then
  * (a0+a2)+(a1+a3)); the tail is a scalar FMA chain `dot += y[i] * x[i]`. */
-double orc_ddot(const double* x, const double* y, int64_t n) {
+static double ddot_skylakex(const double* x, const double* y, int64_t n) {
     int64_t n1 = n & -16, n32 = n1 & ~(int64_t)31, i = 0;
     double dot = 0.0;
     if (n1) {
@@ -87,6 +87,52 @@ double orc_ddot(const double* x, const double* y, int64_t n) {
     }
     for (; i < n; i++) dot = fma(y[i], x[i], dot);
     return dot;
+}
+
+/* The same library's Haswell core (also selected on Zen hosts), read from the
+ * installed libscipy_openblas' ddot_kernel_8 / dot_compute for that core and
+ * pinned against numpy under OPENBLAS_CORETYPE=Haswell (tests/golden/
+ * make_golden.py haswell): 4 x 4-lane FMA accumulators over 16-blocks; each
+ * folds its upper lane pair onto the lower, h_j = (acc_j[m] + acc_j[m+2]);
+ * r = (h0 + h1) + (h2 + h3) per lane; dot = r0 + r1; the tail is an unfused
+ * `dot += y[i] * x[i]` (product rounded, then the add). */
+static double ddot_haswell(const double* x, const double* y, int64_t n) {
+    int64_t n1 = n & -16, i = 0;
+    double dot = 0.0;
+    if (n1) {
+        double acc[4][4];
+        memset(acc, 0, sizeof(acc));
+        for (; i < n1; i += 16)
+            for (int j = 0; j < 4; j++)
+                for (int l = 0; l < 4; l++)
+                    acc[j][l] = fma(x[i + 4 * j + l], y[i + 4 * j + l], acc[j][l]);
+        double r[2];
+        for (int m = 0; m < 2; m++) {
+            double h[4];
+            for (int j = 0; j < 4; j++) h[j] = acc[j][m] + acc[j][m + 2];
+            r[m] = (h[0] + h[1]) + (h[2] + h[3]);
+        }
+        dot = r[0] + r[1];
+    }
+    for (; i < n; i++) {
+        double p = y[i] * x[i];
+        dot = dot + p;
+    }
+    return dot;
+}
+
+static int g_dot_order = ORC_DOT_SKYLAKEX;
+
+int orc_set_dot_order(int order) {
+    if (order != ORC_DOT_SKYLAKEX && order != ORC_DOT_HASWELL) return -1;
+    g_dot_order = order;
+    return 0;
+}
+
+int orc_get_dot_order(void) { return g_dot_order; }
+
+double orc_ddot(const double* x, const double* y, int64_t n) {
+    return g_dot_order == ORC_DOT_HASWELL ? ddot_haswell(x, y, n) : ddot_skylakex(x, y, n);
 }
 
 /* workload.py:461-468 */

@@ -27,7 +27,14 @@ extern "C" {
 
 /* numpy 2.3 `u[:-1].mean(axis=0)` element n of a row-major [rows, N] block. */
 double orc_np_mean_col(const double* u, int64_t rows, int64_t N, int64_t n);
-/* OpenBLAS 0.3.30 ddot, contiguous, SkylakeX kernel order. */
+/* OpenBLAS 0.3.30 ddot, contiguous, in the order of the BLAS core selected
+ * with orc_set_dot_order (process-wide, like OpenBLAS' own core choice):
+ * ORC_DOT_SKYLAKEX (default; SkylakeX / Cooperlake / SapphireRapids cores) or
+ * ORC_DOT_HASWELL (Haswell / Zen cores). */
+#define ORC_DOT_SKYLAKEX 0
+#define ORC_DOT_HASWELL 1
+int orc_set_dot_order(int order);
+int orc_get_dot_order(void);
 double orc_ddot(const double* x, const double* y, int64_t n);
 /* workload.py:461-468 `_cosine(a, b)`. */
 double orc_cosine(const double* a, const double* b, int64_t D);

@@ -79,6 +79,10 @@ def lib():
         L.orc_np_mean_col.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         L.orc_ddot.restype = ctypes.c_double
         L.orc_ddot.argtypes = [_f64p, _f64p, ctypes.c_int64]
+        L.orc_set_dot_order.restype = ctypes.c_int
+        L.orc_set_dot_order.argtypes = [ctypes.c_int]
+        L.orc_get_dot_order.restype = ctypes.c_int
+        L.orc_get_dot_order.argtypes = []
         L.orc_cosine.restype = ctypes.c_double
         L.orc_cosine.argtypes = [_f64p, _f64p, ctypes.c_int64]
         L.orc_decide_horizon_conf.restype = ctypes.c_int32
@@ -140,6 +144,23 @@ def hz_ratio(control_hz) -> tuple[int, int]:
 def np_mean_col(u, n: int) -> float:
     u = _f64(u)
     return lib().orc_np_mean_col(_p(u, _f64p), u.shape[0], u.shape[1], n)
+
+
+DOT_ORDERS = {"skylakex": 0, "haswell": 1}
+
+
+def set_dot_order(name: str) -> str:
+    """Select the OpenBLAS core whose ddot order the oracle reproduces
+    (process-wide); returns the previous one."""
+    prev = get_dot_order()
+    if lib().orc_set_dot_order(DOT_ORDERS[name]) != 0:
+        raise ValueError(name)
+    return prev
+
+
+def get_dot_order() -> str:
+    code = lib().orc_get_dot_order()
+    return next(k for k, v in DOT_ORDERS.items() if v == code)
 
 
 def ddot(x, y) -> float:

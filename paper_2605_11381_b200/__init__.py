@@ -19,7 +19,8 @@ reference's names and signatures are kept; `*_batch` variants and
 from .core import (ActionChunk, Duration, Interval, LastExecInfo, PendingRequest,  # noqa: F401
                    RoundTimeline, TaskState, TimePoint, exec_duration, exec_end_from_piggyback,
                    us_from_actions, us_from_actions_batch)
-from .divergence import round_optimal_horizon, round_optimal_horizon_batch  # noqa: F401
+from .divergence import (dot_order, round_optimal_horizon, round_optimal_horizon_batch,  # noqa: F401
+                         set_dot_order)
 from .engines import (EngineProfile, NetworkModel, ProfileError, batch_latency,  # noqa: F401
                       cloud_round_trip, transfer_time)
 from .ledger import DeviceLedger, LedgerStates  # noqa: F401

@@ -123,6 +123,8 @@ _SIGNATURES = {
     "kr_trace_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "kr_trace_columns_of": (ctypes.POINTER(KrTraceColumns), [_vp]),
     "kr_trace_free": (None, [_vp]),
+    "kr_set_dot_order": (ctypes.c_int, [_i32]),
+    "kr_get_dot_order": (_i32, []),
     "kr_place_cloud": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, ctypes.POINTER(KrFleet),
                                       ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp]),
 }
@@ -151,9 +153,54 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    lib.kr_set_dot_order(DOT_ORDERS[_dot_order_choice()[0]])
     if path is None:
         _LIB = lib
     return lib
+
+
+# --- exact-cosine ddot order (workload.py:461-468 through numpy's OpenBLAS) ----
+DOT_ORDERS = {"skylakex": 0, "haswell": 1}
+# OpenBLAS 0.3.30 runtime cores -> the ddot kernel they run (kernel/x86_64/ddot.c
+# with the skylakex / haswell micro-kernels; Zen shares Haswell's kernels)
+_CORE_ORDER = {"skylakex": "skylakex", "cooperlake": "skylakex", "sapphirerapids": "skylakex",
+               "haswell": "haswell", "zen": "haswell"}
+_DOT_CHOICE = None
+
+
+def numpy_blas_core() -> str | None:
+    """The OpenBLAS core numpy's own BLAS runs in this process (threadpoolctl),
+    or None when numpy is not on OpenBLAS / threadpoolctl is unavailable."""
+    try:
+        import numpy  # noqa: F401  (its BLAS must be loaded to be reported)
+        import threadpoolctl
+    except ImportError:
+        return None
+    infos = [i for i in threadpoolctl.threadpool_info() if i.get("internal_api") == "openblas"]
+    infos.sort(key=lambda i: "numpy" not in i.get("filepath", ""))
+    return infos[0].get("architecture") if infos else None
+
+
+def _dot_order_choice() -> tuple[str, str]:
+    """(order, why): KR_DOT_ORDER=skylakex|haswell overrides; otherwise the
+    order of numpy's OpenBLAS core; SkylakeX (with a warning) when that core's
+    order is not one this library reproduces."""
+    global _DOT_CHOICE
+    if _DOT_CHOICE is None:
+        env = os.environ.get("KR_DOT_ORDER", "auto").lower()
+        if env in DOT_ORDERS:
+            _DOT_CHOICE = (env, "KR_DOT_ORDER")
+        else:
+            core = numpy_blas_core()
+            order = _CORE_ORDER.get((core or "").lower())
+            if order is None:
+                import warnings
+                warnings.warn(f"numpy's BLAS core {core!r} has no reproduced ddot order; exact "
+                              "cosines follow OpenBLAS SkylakeX (set KR_DOT_ORDER to choose)",
+                              RuntimeWarning, stacklevel=3)
+                order = "skylakex"
+            _DOT_CHOICE = (order, f"numpy OpenBLAS core {core}")
+    return _DOT_CHOICE
 
 
 def require_cuda() -> torch.device:

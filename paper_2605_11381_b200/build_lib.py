@@ -21,10 +21,11 @@ INCLUDE = PKG.parent / "include"
 OUT = PKG / "libkairos_b200.so"
 OBJ = PKG / "build"
 
-SOURCES = ["kr_capi.cu", "kr_horizon.cu", "kr_sweep.cu", "kr_sweep_f32.cu", "kr_sweep_f64.cu",
+SOURCES = ["kr_capi.cu", "kr_horizon.cu", "kr_div_skx.cu", "kr_div_hsw.cu", "kr_sweep.cu",
+           "kr_sweep_f32.cu", "kr_sweep_f64.cu",
            "kr_urgency.cu", "kr_select.cu", "kr_ingest.cpp"]
 HEADERS = ["kr_common.cuh", "kr_host.cuh", "kr_stream.cuh", "kr_plan.cuh", "kr_conf.cuh",
-           "kr_sweep.cuh"]
+           "kr_sweep.cuh", "kr_div.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

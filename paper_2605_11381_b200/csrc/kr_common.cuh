@@ -208,6 +208,78 @@ __device__ __forceinline__ double cosine_skx_fixed(const T* a, const T* b) {
     return ddiv(xy, dmul(na, nb));
 }
 
+// The same library's Haswell core (selected on Haswell and Zen hosts; read
+// from the installed libscipy_openblas' ddot kernel for that core and pinned
+// against numpy under OPENBLAS_CORETYPE=Haswell): n & -16 elements through
+// 4x4-lane FMA accumulators over 16-blocks, each folding its lanes (m, m+2),
+// then (h0+h1)+(h2+h3) per lane and r0+r1; the tail is an unfused
+// `dot += y * x` (D < 16: only the tail).
+template <class FX, class FY>
+__device__ __forceinline__ double ddot_hsw(FX x, FY y, int n) {
+    int n1 = n & -16, i = 0;
+    double dot = 0.0;
+    if (n1) {
+        double acc[16];
+#pragma unroll
+        for (int e = 0; e < 16; e++) acc[e] = 0.0;
+        for (; i < n1; i += 16) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) acc[e] = dfma(x(i + e), y(i + e), acc[e]);
+        }
+        double r[2];
+#pragma unroll
+        for (int m = 0; m < 2; m++) {
+            double h[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) h[j] = dadd(acc[4 * j + m], acc[4 * j + m + 2]);
+            r[m] = dadd(dadd(h[0], h[1]), dadd(h[2], h[3]));
+        }
+        dot = dadd(r[0], r[1]);
+    }
+    for (; i < n; i++) dot = dadd(dot, dmul(y(i), x(i)));
+    return dot;
+}
+
+// Which OpenBLAS core's ddot order the exact cosines follow (a kernel
+// template parameter; the host picks it from kr_set_dot_order).
+enum : int { kDotSkylakeX = 0, kDotHaswell = 1 };
+
+__device__ __forceinline__ double cos_from_dots(double xx, double yy, double xy) {
+    double na = dsqrt(xx), nb = dsqrt(yy);
+    if (na == 0.0 && nb == 0.0) return 1.0;
+    if (na == 0.0 || nb == 0.0) return 0.0;
+    return ddiv(xy, dmul(na, nb));
+}
+
+// `_cosine` in the given core's order
+template <int ORD, typename T>
+__device__ __forceinline__ double cosine_ord(const T* a, const T* b, int D) {
+    if constexpr (ORD == kDotSkylakeX) {
+        return cosine_skx(a, b, D);
+    } else {
+        auto fa = [a](int i) { return to_f64(a[i]); };
+        auto fb = [b](int i) { return to_f64(b[i]); };
+        return cos_from_dots(ddot_hsw(fa, fa, D), ddot_hsw(fb, fb, D), ddot_hsw(fa, fb, D));
+    }
+}
+
+template <int DC, int ORD, typename T>
+__device__ __forceinline__ double cosine_ord_fixed(const T* a, const T* b) {
+    if constexpr (ORD == kDotSkylakeX) {
+        return cosine_skx_fixed<DC>(a, b);
+    } else {
+        double x[DC], y[DC];
+#pragma unroll
+        for (int i = 0; i < DC; i++) {
+            x[i] = to_f64(a[i]);
+            y[i] = to_f64(b[i]);
+        }
+        auto fx = [&](int i) { return x[i]; };
+        auto fy = [&](int i) { return y[i]; };
+        return cos_from_dots(ddot_hsw(fx, fx, DC), ddot_hsw(fy, fy, DC), ddot_hsw(fx, fy, DC));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Exact fp32 pre-decision ("filter") for the cosine threshold test
 // ---------------------------------------------------------------------------

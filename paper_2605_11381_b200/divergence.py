@@ -22,6 +22,22 @@ from . import _lib
 from . import device as dev
 
 
+def set_dot_order(order: str) -> None:
+    """Choose the OpenBLAS core whose ddot order the exact fp64 cosines follow:
+    "skylakex" (SkylakeX / Cooperlake / SapphireRapids hosts) or "haswell"
+    (Haswell / Zen hosts).  The default is the core numpy's own OpenBLAS runs
+    in this process (threadpoolctl), so results match `numpy.dot` on this
+    host; KR_DOT_ORDER overrides it at load.  Process-wide, like OpenBLAS'."""
+    if order not in _lib.DOT_ORDERS:
+        raise ValueError(f"dot order must be one of {sorted(_lib.DOT_ORDERS)}, got {order!r}")
+    _lib.check(_lib.load().kr_set_dot_order(_lib.DOT_ORDERS[order]), "kr_set_dot_order")
+
+
+def dot_order() -> str:
+    code = _lib.load().kr_get_dot_order()
+    return next(k for k, v in _lib.DOT_ORDERS.items() if v == code)
+
+
 def _check_thr(sim_threshold: float) -> None:
     if not 0.0 < sim_threshold <= 1.0:
         raise ValueError(f"sim_threshold must be in (0, 1], got {sim_threshold}")

@@ -180,11 +180,11 @@ def gen_divergence(rng: np.random.Generator):
     return cases
 
 
-def save_divergence(cases):
+def save_divergence(cases, name="divergence.npz"):
     rs = np.array([c[0].shape for c in cases], np.int64)
     cs = np.array([c[1].shape for c in cases], np.int64)
     np.savez_compressed(
-        OUT / "divergence.npz",
+        OUT / name,
         ref=np.concatenate([c[0].ravel() for c in cases]),
         cand=np.concatenate([c[1].ravel() for c in cases]),
         ref_shapes=rs, cand_shapes=cs,
@@ -588,7 +588,26 @@ def gen_traces():
                                                          indent=0))
 
 
+def gen_divergence_haswell():
+    """The divergence cases with the reference's cosines computed by numpy's
+    OpenBLAS running its Haswell core (OPENBLAS_CORETYPE=Haswell, which the
+    library also selects on Zen hosts): pins the second ddot order."""
+    if os.environ.get("OPENBLAS_CORETYPE") != "Haswell":
+        import subprocess
+        env = dict(os.environ, OPENBLAS_CORETYPE="Haswell")
+        subprocess.run([sys.executable, __file__, "haswell"], env=env, check=True)
+        return
+    import threadpoolctl
+    cores = {i["architecture"] for i in threadpoolctl.threadpool_info()
+             if i.get("internal_api") == "openblas"}
+    assert cores == {"Haswell"}, cores
+    save_divergence(gen_divergence(np.random.default_rng(31)), "divergence_haswell.npz")
+
+
 def main():
+    if sys.argv[1:] == ["haswell"]:  # only the Haswell-order divergence fixture
+        gen_divergence_haswell()
+        return
     if sys.argv[1:] == ["traces"]:  # only the trace-ingest fixtures
         gen_traces()
         return
@@ -601,6 +620,7 @@ def main():
     rng = np.random.default_rng(20260517)
     save_confidence(gen_confidence(rng))
     save_divergence(gen_divergence(rng))
+    gen_divergence_haswell()
     (OUT / "time.json").write_text(json.dumps(gen_time(rng)))
     (OUT / "plan.json").write_text(json.dumps(gen_plan(rng), separators=(",", ":")))
     (OUT / "plan_cloud.json").write_text(json.dumps(gen_plan_cloud(np.random.default_rng(7)),

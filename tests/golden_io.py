@@ -36,8 +36,10 @@ def sweep_cases():
     return out
 
 
-def divergence_cases():
-    z = np.load(GOLDEN / "divergence.npz")
+def divergence_cases(name: str = "divergence.npz"):
+    """divergence.npz: cosines from numpy's OpenBLAS SkylakeX core (this host);
+    divergence_haswell.npz: the same reference run under its Haswell core."""
+    z = np.load(GOLDEN / name)
     out = []
     for i in range(len(z["thr"])):
         ref = z["ref"][z["ref_off"][i]:z["ref_off"][i + 1]].reshape(z["ref_shapes"][i])

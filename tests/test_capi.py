@@ -50,6 +50,31 @@ def test_host_only_entry_points():
     assert lib.kr_horizon_divergence(None, None, 0, 4, 1, 8, 8, 7, None, None, None, 0.0, None,
                                      None, 0, None) == _lib.KR_EINVAL
     assert lib.kr_horizon_static(0, 8, 3, None, None) == _lib.KR_OK
+    prev = lib.kr_get_dot_order()
+    assert lib.kr_set_dot_order(7) == _lib.KR_EINVAL and lib.kr_get_dot_order() == prev
+    assert lib.kr_set_dot_order(1) == _lib.KR_OK and lib.kr_get_dot_order() == 1
+    assert lib.kr_set_dot_order(prev) == _lib.KR_OK
+
+
+@pytest.mark.parametrize("env,expect", [({"OPENBLAS_CORETYPE": "Haswell"}, "haswell"),
+                                        ({"OPENBLAS_CORETYPE": "Zen"}, "haswell"),
+                                        ({"OPENBLAS_CORETYPE": "SkylakeX"}, "skylakex"),
+                                        ({"KR_DOT_ORDER": "haswell"}, "haswell")])
+def test_dot_order_follows_numpy_blas_core(env, expect):
+    """The exact cosines take the ddot order of the OpenBLAS core numpy runs
+    in the process (threadpoolctl), unless KR_DOT_ORDER overrides it."""
+    import os
+    import sys
+    code = ("from paper_2605_11381_b200 import _lib\n"
+            "lib = _lib.load()\n"
+            "print(_lib._dot_order_choice()[0], lib.kr_get_dot_order())")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                         env={**os.environ, **env}, check=True).stdout.split()
+    assert out == [expect, str(_order_code(expect))]
+
+
+def _order_code(name):
+    return {"skylakex": 0, "haswell": 1}[name]
 
 
 def test_struct_layouts_match_header():

@@ -104,6 +104,60 @@ def test_divergence_golden(kb):
     assert not bad_h and not bad_c, (bad_h[:5], bad_c[:5])
 
 
+@pytest.fixture
+def haswell(kb):
+    """Run a test with the exact cosines in OpenBLAS' Haswell ddot order (the
+    device library and the oracle), restoring both afterwards."""
+    prev_dev, prev_orc = kb.dot_order(), orc.set_dot_order("haswell")
+    kb.set_dot_order("haswell")
+    try:
+        yield
+    finally:
+        kb.set_dot_order(prev_dev)
+        orc.set_dot_order(prev_orc)
+
+
+def test_divergence_golden_haswell_order(kb, haswell):
+    """The reference run under numpy's OpenBLAS Haswell core (also Zen's):
+    horizons and every cosine bit-exact with the device's Haswell order."""
+    from paper_2605_11381_b200.divergence import round_optimal_horizon_batch
+    bad_h, bad_c = [], []
+    for i, (ref, cand, thr, exp, cos) in enumerate(
+            golden_io.divergence_cases("divergence_haswell.npz")):
+        r = torch.tensor(ref[None], device="cuda")
+        c_ = torch.tensor(cand[None], device="cuda")
+        H, c = round_optimal_horizon_batch(r, c_, thr, return_cos=True)
+        H2 = round_optimal_horizon_batch(r, c_, thr)  # fp32 filter + exact fallback
+        if int(H.item()) != exp or int(H2.item()) != exp:
+            bad_h.append(i)
+        if not np.array_equal(c[0, 0, :len(cos)].cpu().numpy(), cos):
+            bad_c.append(i)
+    assert not bad_h and not bad_c, (bad_h[:5], bad_c[:5])
+
+
+@pytest.mark.parametrize("R,S,Lp,Lc,D", [(1024, 1, 50, 50, 7), (300, 1, 64, 64, 32),
+                                         (130, 8, 50, 50, 7), (65, 2, 40, 40, 48),
+                                         (33, 1, 10, 10, 16)])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_divergence_haswell_order_vs_oracle(kb, haswell, R, S, Lp, Lc, D, dtype):
+    """Every kernel variant (D = 7 / 32 specialisations, generic D, ensembles,
+    fp64 storage) in the Haswell order against the oracle in that order, with
+    thresholds placed exactly on computed cosines so the exact path decides."""
+    from paper_2605_11381_b200.divergence import round_optimal_horizon_batch
+    rng = np.random.default_rng(R * 7 + D)
+    prev = rng.normal(size=(R, Lp, D)).astype(dtype)
+    noise = rng.normal(size=(R, S, Lc, D)) * (0.35 * np.arange(1, Lc + 1) / Lc)[None, None, :, None]
+    cand = (prev[:, None, :Lc] + noise).astype(dtype)
+    _, cos0 = orc.divergence_batch(prev, cand, 0.9, want_cos=True)
+    for thr in (0.9, float(np.clip(np.nanmedian(cos0[:, :, Lc // 3]), 1e-3, 1.0))):
+        exp, exp_cos = orc.divergence_batch(prev, cand, thr, want_cos=True)
+        t = lambda a: torch.from_numpy(a).cuda()
+        H, cos = round_optimal_horizon_batch(t(prev), t(cand), thr, return_cos=True)
+        assert np.array_equal(H.cpu().numpy(), exp)
+        assert np.array_equal(cos.cpu().numpy(), exp_cos, equal_nan=True)
+        assert np.array_equal(round_optimal_horizon_batch(t(prev), t(cand), thr).cpu().numpy(), exp)
+
+
 @pytest.mark.parametrize("R,S,Lp,Lc,D", [(1024, 1, 50, 50, 7), (300, 1, 64, 64, 32),
                                          (130, 8, 50, 50, 7), (77, 3, 20, 16, 5),
                                          (65, 2, 40, 40, 48), (33, 1, 10, 10, 16),

@@ -53,6 +53,30 @@ def test_divergence_golden_horizon_and_cosine():
     assert not bad_h and not bad_c, (bad_h[:5], bad_c[:5])
 
 
+def test_divergence_golden_haswell_order():
+    """The reference's cosines under numpy's OpenBLAS Haswell core (Zen hosts
+    run the same kernel): the oracle's Haswell ddot order reproduces every one
+    bit-for-bit, and the SkylakeX order does not (the fixture has teeth)."""
+    cases = golden_io.divergence_cases("divergence_haswell.npz")
+    prev = orc.set_dot_order("haswell")
+    try:
+        bad_h, bad_c = [], []
+        for i, (ref, cand, thr, exp, cos) in enumerate(cases):
+            if orc.round_optimal_horizon(ref, cand, thr) != exp:
+                bad_h.append(i)
+            mine = np.array([orc.cosine(cand[j], ref[j]) for j in range(len(cos))])
+            if not np.array_equal(mine, cos):
+                bad_c.append(i)
+        assert not bad_h and not bad_c, (bad_h[:5], bad_c[:5])
+        orc.set_dot_order("skylakex")
+        differ = sum(not np.array_equal(
+            np.array([orc.cosine(cand[j], ref[j]) for j in range(len(cos))]), cos)
+            for ref, cand, thr, exp, cos in cases)
+        assert differ > 100
+    finally:
+        orc.set_dot_order(prev)
+
+
 def test_divergence_batch_ragged_matches_scalar():
     rng = np.random.default_rng(6)
     R, S, Lp, Lc, D = 40, 3, 20, 16, 7

@@ -116,7 +116,12 @@ struct SweepWork {
     unsigned long long* sums;    // [C]
     uint32_t* flags;
     int64_t R;
-    SweepTables* tab;            // shared
+    // the shared tables sit at a fixed offset of the dynamic shared memory:
+    // addressed through the shared window directly (no per-use generic base)
+    __device__ __forceinline__ static SweepTables* tables() {
+        extern __shared__ __align__(128) unsigned char smem[];
+        return reinterpret_cast<SweepTables*>(smem + stream_aux_offset());
+    }
 
     __device__ void setup(int) {}
 
@@ -150,7 +155,7 @@ struct SweepWork {
         if (fin == T(0)) bits = 0;
         SB idx = (static_cast<SB>(bits - static_cast<B>(lut_lo)) >> lut_shift) + 1;
         idx = idx < 0 ? 0 : (idx > lut_n + 1 ? lut_n + 1 : idx);
-        const int e = tab->lut[idx];
+        const int e = tables()->lut[idx];
         const bool out = static_cast<B>(sb - static_cast<B>(sfminb)) > static_cast<B>(sfrng) && sb != 0;
         return e == 0xFFFF || out ? -1 : e;
     }
@@ -170,8 +175,8 @@ struct SweepWork {
         if (!(sf >= sfmin && sf <= sfmax)) return -1;
         const T* rh;
         const T* rl;
-        if constexpr (sizeof(T) == 4) { rh = tab->rh; rl = tab->rl; }
-        else { rh = tab->rhd; rl = tab->rld; }
+        if constexpr (sizeof(T) == 4) { rh = tables()->rh; rl = tables()->rl; }
+        else { rh = tables()->rhd; rl = tables()->rld; }
         int pos = 0;
         for (int st = half; st > 0; st >>= 1)
             if (rho > rh[pos + st - 1]) pos += st;
@@ -181,17 +186,17 @@ struct SweepWork {
 
     // configurations [a, b) take horizon n at this robot (a < b)
     __device__ __forceinline__ void step(int a, int b, int n, int64_t r) const {
-        atomicAdd(&tab->D[a], static_cast<uint32_t>(n));
-        atomicSub(&tab->D[b], static_cast<uint32_t>(n));
+        atomicAdd(&tables()->D[a], static_cast<uint32_t>(n));
+        atomicSub(&tables()->D[b], static_cast<uint32_t>(n));
         if (n < maxcap)  // below some min_horizon floor (horizon.py:130)
             for (int c = a; c < b; c++) {
-                const int cap = tab->hcap[c];
-                if (cap > n) atomicAdd(&tab->F[c], static_cast<uint32_t>(cap - n));
+                const int cap = tables()->hcap[c];
+                if (cap > n) atomicAdd(&tables()->F[c], static_cast<uint32_t>(cap - n));
             }
         if (H)
             for (int c = a; c < b; c++) {
-                const int cap = tab->hcap[c];
-                H[static_cast<int64_t>(tab->orig[c]) * R + r] = n > cap ? n : cap;
+                const int cap = tables()->hcap[c];
+                H[static_cast<int64_t>(tables()->orig[c]) * R + r] = n > cap ? n : cap;
             }
     }
 
@@ -260,7 +265,7 @@ struct SweepWork {
                 for (int c = 0; c < VC; c++)
                     if (bad || j[c] < 0) {
                         int jj = bad ? -1 : search(sf[c], ratio(sf[c], fin[c]));
-                        if (jj < 0) jj = sweep_exact(col + c, K, N, tab->p, Cc);
+                        if (jj < 0) jj = sweep_exact(col + c, K, N, tables()->p, Cc);
                         j[c] = jj;
                     }
             }
@@ -340,7 +345,7 @@ struct SweepWork {
                         for (int k = 0; k < Kr; k++) fl |= CW::check(col[k * N]);
                     if (bad || j[c] < 0) {
                         int jj = bad ? -1 : search(sf[c], ratio(sf[c], fin[c]));
-                        if (jj < 0) jj = sweep_exact(col, K, N, tab->p, Cc);
+                        if (jj < 0) jj = sweep_exact(col, K, N, tables()->p, Cc);
                         j[c] = jj;
                     }
                 }
@@ -384,14 +389,14 @@ struct SweepWork {
                 const bool ok = rr < nr;
                 const int total = chunk_half(u + (ok ? rr : 0) * KN, ok, r0 + rr, fl);
                 if (ok && g == 0 && total < Cc) {  // slots never tripped take N
-                    atomicAdd(&tab->D[total], static_cast<uint32_t>(N));
+                    atomicAdd(&tables()->D[total], static_cast<uint32_t>(N));
                     if (H)
                         for (int c = total; c < Cc; c++)
-                            H[static_cast<int64_t>(tab->orig[c]) * R + r0 + rr] = N;
+                            H[static_cast<int64_t>(tables()->orig[c]) * R + r0 + rr] = N;
                 }
                 if (ok && H)
                     for (int c = Cc + g; c < C; c += 16)
-                        H[static_cast<int64_t>(tab->orig[c]) * R + r0 + rr] = tab->hcap[c];
+                        H[static_cast<int64_t>(tables()->orig[c]) * R + r0 + rr] = tables()->hcap[c];
             }
             if (fl && flags) atomicOr(flags, fl);
             return;
@@ -408,14 +413,14 @@ struct SweepWork {
             }
             // slots never tripped take the whole chunk (>= every floor)
             if (lane == 0 && carry < Cc) {
-                atomicAdd(&tab->D[carry], static_cast<uint32_t>(N));
+                atomicAdd(&tables()->D[carry], static_cast<uint32_t>(N));
                 if (H)
                     for (int c = carry; c < Cc; c++)
-                        H[static_cast<int64_t>(tab->orig[c]) * R + r0 + rr] = N;
+                        H[static_cast<int64_t>(tables()->orig[c]) * R + r0 + rr] = N;
             }
             if (H)
                 for (int c = Cc + lane; c < C; c += 32)
-                    H[static_cast<int64_t>(tab->orig[c]) * R + r0 + rr] = tab->hcap[c];
+                    H[static_cast<int64_t>(tables()->orig[c]) * R + r0 + rr] = tables()->hcap[c];
         }
         if (fl && flags) atomicOr(flags, fl);
     }
@@ -430,24 +435,24 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p
                                                                          SweepWork<T, KC, VC, HALF> w,
                                                                          const __grid_constant__ SweepCfg cfg) {
     extern __shared__ __align__(128) unsigned char smem[];
-    w.tab = reinterpret_cast<SweepTables*>(smem + stream_aux_offset());
-    for (int i = threadIdx.x; i < w.lut_n; i += blockDim.x) w.tab->lut[i + 1] = cfg.lut[i];
+    SweepTables* const tab = w.tables();
+    for (int i = threadIdx.x; i < w.lut_n; i += blockDim.x) tab->lut[i + 1] = cfg.lut[i];
     if (threadIdx.x == 0) {
-        w.tab->lut[0] = 0;
-        w.tab->lut[w.lut_n + 1] = static_cast<uint16_t>(w.Cc);
+        tab->lut[0] = 0;
+        tab->lut[w.lut_n + 1] = static_cast<uint16_t>(w.Cc);
     }
     for (int i = threadIdx.x; i < kSweepPad; i += blockDim.x) {
-        w.tab->rhd[i] = cfg.rh[i];
-        w.tab->rld[i] = cfg.rl[i];
-        w.tab->rh[i] = static_cast<float>(cfg.rh[i]);  // exactly representable (host-rounded)
-        w.tab->rl[i] = static_cast<float>(cfg.rl[i]);
+        tab->rhd[i] = cfg.rh[i];
+        tab->rld[i] = cfg.rl[i];
+        tab->rh[i] = static_cast<float>(cfg.rh[i]);  // exactly representable (host-rounded)
+        tab->rl[i] = static_cast<float>(cfg.rl[i]);
         if (i < kSweepMaxCfg) {
-            w.tab->p[i] = cfg.p[i];
-            w.tab->orig[i] = cfg.orig[i];
-            w.tab->hcap[i] = cfg.hcap[i];
-            w.tab->F[i] = 0;
+            tab->p[i] = cfg.p[i];
+            tab->orig[i] = cfg.orig[i];
+            tab->hcap[i] = cfg.hcap[i];
+            tab->F[i] = 0;
         }
-        if (i <= kSweepMaxCfg) w.tab->D[i] = 0;
+        if (i <= kSweepMaxCfg) tab->D[i] = 0;
     }
     __syncthreads();
     stream_run<kStaged>(p, smem, w);
@@ -455,14 +460,14 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p
     if (threadIdx.x == 0) {  // S_c = prefix_sum(D)[c] + F[c]; static slots once per grid
         uint32_t run = 0;
         for (int c = 0; c < w.Cc; c++) {
-            run += w.tab->D[c];
-            const uint32_t s = run + w.tab->F[c];
-            if (s) atomicAdd(&w.sums[w.tab->orig[c]], static_cast<unsigned long long>(s));
+            run += tab->D[c];
+            const uint32_t s = run + tab->F[c];
+            if (s) atomicAdd(&w.sums[tab->orig[c]], static_cast<unsigned long long>(s));
         }
         if (blockIdx.x == 0)
             for (int c = w.Cc; c < w.C; c++)
-                atomicAdd(&w.sums[w.tab->orig[c]],
-                          static_cast<unsigned long long>(w.R) * static_cast<unsigned long long>(w.tab->hcap[c]));
+                atomicAdd(&w.sums[tab->orig[c]],
+                          static_cast<unsigned long long>(w.R) * static_cast<unsigned long long>(tab->hcap[c]));
     }
 }
 

@@ -257,6 +257,16 @@ __device__ __forceinline__ double cosine_ord(const T* a, const T* b, int D) {
     if constexpr (ORD == kDotSkylakeX) {
         return cosine_skx(a, b, D);
     } else {
+        if (D < 16) {  // only the unfused tail: one pass, three chains
+            double xx = 0.0, yy = 0.0, xy = 0.0;
+            for (int i = 0; i < D; i++) {
+                const double x = to_f64(a[i]), y = to_f64(b[i]);
+                xx = dadd(xx, dmul(x, x));
+                yy = dadd(yy, dmul(y, y));
+                xy = dadd(xy, dmul(y, x));
+            }
+            return cos_from_dots(xx, yy, xy);
+        }
         auto fa = [a](int i) { return to_f64(a[i]); };
         auto fb = [b](int i) { return to_f64(b[i]); };
         return cos_from_dots(ddot_hsw(fa, fa, D), ddot_hsw(fb, fb, D), ddot_hsw(fa, fb, D));
@@ -267,6 +277,16 @@ template <int DC, int ORD, typename T>
 __device__ __forceinline__ double cosine_ord_fixed(const T* a, const T* b) {
     if constexpr (ORD == kDotSkylakeX) {
         return cosine_skx_fixed<DC>(a, b);
+    } else if constexpr (DC < 16) {  // only the unfused tail: one pass, three chains
+        double xx = 0.0, yy = 0.0, xy = 0.0;
+#pragma unroll
+        for (int i = 0; i < DC; i++) {
+            const double x = to_f64(a[i]), y = to_f64(b[i]);
+            xx = dadd(xx, dmul(x, x));
+            yy = dadd(yy, dmul(y, y));
+            xy = dadd(xy, dmul(y, x));
+        }
+        return cos_from_dots(xx, yy, xy);
     } else {
         double x[DC], y[DC];
 #pragma unroll

@@ -337,6 +337,36 @@ KR_API void kr_trace_free(void* table);
 KR_API int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_key* sorted_keys,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+
+/* ---- synthetic traces (workload.py:296-456) -------------------
+ * The reference's construction on the device with counter-based randomness
+ * (Philox-4x32-10 keyed by (seed, task id), indexed by (round, column)); bit
+ * parity with numpy's Generator is not a goal.  `SyntheticSpec` fields that the
+ * kernels read: */
+typedef struct kr_synth_spec {
+    int32_t chunk_size;        /* N */
+    int32_t diffusion_steps;   /* K */
+    double decay, noise_scale, bump_factor, uncertain_fraction;
+} kr_synth_spec;
+/* workload.py:341-363 `_synth_round_magnitudes` for rounds [round0, round0+G)
+ * of the tasks tasks[A] (any int64 ids) -> U[A][G][K][N] float64 (device). */
+KR_API int kr_synth_magnitudes(const kr_synth_spec* spec, uint64_t seed, const int64_t* tasks,
+                               int64_t A, int32_t round0, int32_t G, double* U, void* stream);
+/* workload.py:404-436: consume the decided horizons H[A][G] of each task in
+ * order: trigger placement (max(0, prev_h - slack), at most prev_h - 1), the
+ * executed-action total and the budget.  state[A][4] = {executed, prev_h (-1:
+ * none), n_rounds, done}, carried across calls; trigger[A][G]; used[A][G]. */
+KR_API int kr_synth_close(const int32_t* H, int64_t A, int32_t G, int32_t budget, int32_t slack,
+                          int32_t* state, int32_t* trigger, uint8_t* used, void* stream);
+/* workload.py:438: success = rng.random() < success_rate, per task. */
+KR_API int kr_synth_success(uint64_t seed, const int64_t* tasks, int64_t A, double rate,
+                            uint8_t* success, void* stream);
+/* workload.py:417-419: per round r, h[r] rows x dim cumulative sums of
+ * normal(0, 0.05) steps into traj[row_off[r] + row][dim]. */
+KR_API int kr_synth_trajectories(uint64_t seed, const int64_t* task_of, const int32_t* round_of,
+                                 const int32_t* h, const int64_t* row_off, int64_t nr, int32_t dim,
+                                 double* traj, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,8 @@ from .horizon import (HorizonPolicyConfig, UpdateMagnitudes, decide_horizon,  # 
                       decide_horizon_batch, sweep_horizon_sums, sweep_thresholds)
 from .scheduler import (DispatchPlan, SchedulerConfig, assign_bucket,  # noqa: F401
                         estimate_exec_latency, order_within_bucket, plan, plan_fifo, plan_las)
+from .synth import (SynthColumns, SyntheticSpec, generation_slack_actions,  # noqa: F401
+                    synthesize_family, synthesize_family_columns, synthesize_trace)
 from .traces import (RoundRecord, TaskTrace, TraceColumns, TraceFormatError,  # noqa: F401
                      load_trace_columns, load_trace_dir, load_traces, pareto_rows, store_traces,
                      trace_from_dict, trace_to_dict)

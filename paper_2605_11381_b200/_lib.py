@@ -84,6 +84,14 @@ class KrTraceColumns(ctypes.Structure):
                  ("err_message", ctypes.c_char_p)])
 
 
+class KrSynthSpec(ctypes.Structure):
+    """kr_synth_spec: the SyntheticSpec fields the synthesis kernels read."""
+
+    _fields_ = [("chunk_size", _i32), ("diffusion_steps", _i32), ("decay", ctypes.c_double),
+                ("noise_scale", ctypes.c_double), ("bump_factor", ctypes.c_double),
+                ("uncertain_fraction", ctypes.c_double)]
+
+
 _SIGNATURES = {
     "kr_version": (ctypes.c_char_p, []),
     "kr_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -123,6 +131,12 @@ _SIGNATURES = {
     "kr_trace_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "kr_trace_columns_of": (ctypes.POINTER(KrTraceColumns), [_vp]),
     "kr_trace_free": (None, [_vp]),
+    "kr_synth_magnitudes": (ctypes.c_int, [ctypes.POINTER(KrSynthSpec), ctypes.c_uint64, _vp, _i64,
+                                            _i32, _i32, _vp, _vp]),
+    "kr_synth_close": (ctypes.c_int, [_vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "kr_synth_success": (ctypes.c_int, [ctypes.c_uint64, _vp, _i64, ctypes.c_double, _vp, _vp]),
+    "kr_synth_trajectories": (ctypes.c_int, [ctypes.c_uint64, _vp, _vp, _vp, _vp, _i64, _i32, _vp,
+                                              _vp]),
     "kr_set_dot_order": (ctypes.c_int, [_i32]),
     "kr_get_dot_order": (_i32, []),
     "kr_place_cloud": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, ctypes.POINTER(KrFleet),

@@ -35,6 +35,8 @@ from roboserve.core import Interval, LastExecInfo, PendingRequest, TaskState  # 
 from roboserve.engines import EngineProfile, NetworkModel  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(OUT.parent))
+import golden_io  # noqa: E402  (tests/golden_io.py: shared fixture helpers)
 
 
 # --- step 1a: confidence horizon -------------------------------------------
@@ -588,6 +590,46 @@ def gen_traces():
                                                          indent=0))
 
 
+# --- synthetic traces: the reference's distributions (§8(f)4) ---------------
+
+SYNTH_INVALID = [{"chunk_size": 0}, {"diffusion_steps": 1}, {"control_hz": 0.0},
+                 {"action_budget": 0}, {"uncertain_fraction": 1.5}, {"decay": 1.0},
+                 {"noise_scale": 0.5}, {"bump_factor": 1.0}, {"success_rate": -0.1},
+                 {"chunk_sizes": 3, "zeta": 1}]
+
+SYNTH_SETTINGS = [
+    ({}, ("confidence", {}), 100_000),
+    ({"chunk_size": 32, "diffusion_steps": 8, "action_budget": 120, "uncertain_fraction": 0.5,
+      "decay": 0.4, "noise_scale": 0.2, "bump_factor": 2.5, "success_rate": 0.6},
+     ("confidence", {"threshold": 0.3, "min_horizon": 4}), 50_000),
+    ({"uncertain_fraction": 0.05, "control_hz": 15.0}, ("static", {"horizon": 20}), 100_000),
+]
+
+
+def gen_synth():
+    out = []
+    for spec_kw, (kind, pol_kw), gen_latency in SYNTH_SETTINGS:
+        spec = workload.SyntheticSpec(**spec_kw)
+        pol = (horizon.HorizonPolicyConfig.confidence(**pol_kw) if kind == "confidence"
+               else horizon.HorizonPolicyConfig.static(**pol_kw))
+        fam = workload.synthesize_family(spec, pol, gen_latency, 3000, seed=17)
+        out.append({"spec": spec_kw, "policy": [kind, pol_kw], "gen_latency": gen_latency,
+                    "stats": golden_io.synth_stats(fam, spec_kw)})
+    # the reference's validation message (workload.py:386-391)
+    try:
+        workload.synthesize_trace(workload.SyntheticSpec(), horizon.HorizonPolicyConfig.static(2),
+                                  100_000, 0)
+    except ValueError as e:
+        err = str(e)
+    spec_errors = []
+    for kw in SYNTH_INVALID:
+        try:
+            workload.SyntheticSpec.from_dict(kw)
+        except ValueError as e:
+            spec_errors.append([kw, str(e)])
+    return {"settings": out, "too_slow_error": err, "spec_errors": spec_errors}
+
+
 def gen_divergence_haswell():
     """The divergence cases with the reference's cosines computed by numpy's
     OpenBLAS running its Haswell core (OPENBLAS_CORETYPE=Haswell, which the
@@ -605,6 +647,9 @@ def gen_divergence_haswell():
 
 
 def main():
+    if sys.argv[1:] == ["synth"]:  # only the synthesis-distribution fixture
+        (OUT / "synth_stats.json").write_text(json.dumps(gen_synth(), indent=0))
+        return
     if sys.argv[1:] == ["haswell"]:  # only the Haswell-order divergence fixture
         gen_divergence_haswell()
         return
@@ -629,6 +674,7 @@ def main():
     save_sweep(gen_sweep(np.random.default_rng(11)))
     (OUT / "sim_replay.json").write_text(json.dumps(gen_sim(), separators=(",", ":")))
     gen_traces()
+    (OUT / "synth_stats.json").write_text(json.dumps(gen_synth(), indent=0))
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".npz", ".json"):
             print(f"{p.name:28s} {p.stat().st_size:>9d} B")

@@ -152,3 +152,30 @@ TRACES_DIR = GOLDEN / "traces"
 
 def traces_expected():
     return json.loads((GOLDEN / "traces_expected.json").read_text())
+
+
+def synth():
+    return json.loads((GOLDEN / "synth_stats.json").read_text())
+
+
+def synth_stats(traces, spec_kw) -> dict:
+    """Distribution summary of a trace family (computed the same way for the
+    reference in make_golden.py and for the device synthesis in
+    tests/test_gpu_synth.py)."""
+    N = spec_kw.get("chunk_size", 50)
+    bump = spec_kw.get("bump_factor", 1.8)
+    hs, trig, nunc, u0, rpt = [], [], [], [], []
+    for t in traces:
+        rpt.append(len(t.rounds))
+        for r in t.rounds:
+            hs.append(r.horizon)
+            trig.append(r.trigger_action_index)
+            u = np.asarray(r.update_magnitudes.u)
+            nunc.append(int((u[-1] == bump * u[:-1].mean(axis=0)).sum()))
+            u0.append(float(u[0].mean()))
+    hist = np.bincount(np.array(hs), minlength=N + 1)
+    return {"tasks": len(traces), "rounds": len(hs), "rounds_per_task": float(np.mean(rpt)),
+            "horizon_mean": float(np.mean(hs)), "horizon_std": float(np.std(hs)),
+            "horizon_hist": (hist / hist.sum()).tolist(), "trigger_mean": float(np.mean(trig)),
+            "tail_mean": float(np.mean(nunc)), "u0_mean": float(np.mean(u0)),
+            "success_mean": float(np.mean([t.success for t in traces]))}

@@ -17,9 +17,11 @@ generated a few rounds per launch for every task still below its budget;
 from __future__ import annotations
 
 import ctypes
+import json
 import math
 from dataclasses import dataclass
 from fractions import Fraction
+from pathlib import Path
 from typing import Optional
 
 import numpy as np
@@ -29,7 +31,7 @@ from . import _lib
 from . import device as dev
 from .core import Duration, exec_duration
 from .horizon import HorizonPolicyConfig, UpdateMagnitudes, decide_horizon_batch
-from .traces import RoundRecord, TaskTrace
+from .traces import RoundRecord, TaskTrace, store_traces
 
 
 @dataclass(frozen=True)
@@ -247,3 +249,27 @@ def synthesize_family(spec: SyntheticSpec, policy: HorizonPolicyConfig, gen_late
     (workload.py:445-456)."""
     return synthesize_family_columns(spec, policy, gen_latency, count, seed, id_prefix=id_prefix,
                                      **kwargs).to_traces()
+
+
+def cmd_gen_traces(spec: str | Path, out_dir: str | Path, policy: str = "confidence",
+                   static_h: Optional[int] = None, threshold: float = 0.4, h_min: int = 5) -> int:
+    """`roboserve gen-traces` (cli.py:32-53): a spec file (SyntheticSpec fields
+    plus `count`, `seed`, `gen_latency_us`) -> out_dir/traces.jsonl, the family
+    synthesised on the device."""
+    if policy == "static":
+        if static_h is None:
+            raise ValueError("--static-h is required with --policy static")
+        pol = HorizonPolicyConfig.static(static_h)
+    else:
+        pol = HorizonPolicyConfig.confidence(threshold=threshold, min_horizon=h_min)
+    spec_data = json.loads(Path(spec).read_text(encoding="utf-8"))
+    count = spec_data.pop("count", 1)
+    seed = spec_data.pop("seed", 0)
+    gen_latency = spec_data.pop("gen_latency_us", 300_000)
+    traces = synthesize_family(SyntheticSpec.from_dict(spec_data), pol, gen_latency, count, seed)
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    out_path = out / "traces.jsonl"
+    store_traces(traces, out_path)
+    print(f"wrote {len(traces)} traces to {out_path}")
+    return 0

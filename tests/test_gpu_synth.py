@@ -118,3 +118,19 @@ def test_traces_round_trip_through_ingest(kb, tmp_path):
     kb.store_traces(fam, p)
     back = kb.load_traces(p)
     assert [kb.trace_to_dict(t) for t in back] == [kb.trace_to_dict(t) for t in fam]
+
+
+def test_cmd_gen_traces_then_pareto(kb, tmp_path, capsys):
+    """gen-traces (cli.py:32-53) on the device, then the pareto sweep over it."""
+    import json
+    from paper_2605_11381_b200.synth import cmd_gen_traces
+    spec = tmp_path / "spec.json"
+    spec.write_text(json.dumps({"count": 12, "seed": 4, "gen_latency_us": 100_000,
+                                "action_budget": 90}))
+    assert cmd_gen_traces(spec, tmp_path / "out", h_min=5) == 0
+    assert "wrote 12 traces to" in capsys.readouterr().out
+    fam = kb.load_traces(tmp_path / "out" / "traces.jsonl")
+    assert len(fam) == 12 and all(sum(r.horizon for r in t.rounds) >= 90 for t in fam)
+    with pytest.raises(ValueError, match="--static-h is required"):
+        cmd_gen_traces(spec, tmp_path / "o2", policy="static")
+    assert kb.traces.cmd_pareto(tmp_path / "out" / "traces.jsonl", tmp_path / "p.csv") == 0

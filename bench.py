@@ -368,7 +368,10 @@ def round_roofline(soa, R, t_round, peak):
 
 def other_configs(reps: int = 200):
     """The other BASELINE.json configs on this GPU, each one whole decision
-    round (horizons + urgency + top-k admission) replayed as one CUDA graph.
+    round (horizons + urgency + top-k admission) replayed from CUDA graphs in
+    the concurrent "split" layout (horizons || urgency + admission), with the
+    reserved-SM count measured best per size (profiles/r1_small_layouts.jsonl,
+    tools/small_layouts.py).
     configs[1] and [2] are L2-resident (labelled); configs[3] streams from HBM.
     configs[0] (the paper's Fig. 4 scenario) is a correctness case
     (tests/test_gpu_scheduler.py), configs[4] is the headline above."""
@@ -378,19 +381,15 @@ def other_configs(reps: int = 200):
     lib = _lib.load()
     out = {}
 
-    def timed(fn):
-        fn()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            fn()
+    def timed_captured(rnd, fleet, inp, reserve):
+        rnd.capture(fleet, inp, reserve_sms=reserve, layout="split")
         for _ in range(10):
-            g.replay()
+            rnd.replay()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record()
         for _ in range(reps):
-            g.replay()
+            rnd.replay()
         b.record()
         torch.cuda.synchronize()
         return a.elapsed_time(b) / 1e3 / reps
@@ -406,9 +405,10 @@ def other_configs(reps: int = 200):
     prev, cand, off = synthetic.chunks(R, seed=12)
     rnd = rounds.DecisionRound(R, 64, sched_for(soa))
     inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
-    t = timed(lambda: rnd.run(fleet, inp))
+    t = timed_captured(rnd, fleet, inp, 8)
     out["configs[1] 1k robots 50x7 k=64"] = {
-        "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t, "l2": "resident (0.3 MB inputs)"}
+        "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t, "l2": "resident (0.3 MB inputs)",
+        "layout": "split, 8 reserved SMs"}
     # configs[2]: 16k mixed fleet, two homogeneous tensors, 64-step chunks, k = 1024
     R = 16384
     soa = synthetic.fleet_soa(R, seed=13)
@@ -418,11 +418,12 @@ def other_configs(reps: int = 200):
     rnd = rounds.DecisionRound(R, 1024, sched_for(soa))
     inp = rounds.MixedInputs([(0, rounds.DivergenceInputs(pa, ca, THR, offset=oa)),
                               (R // 2, rounds.DivergenceInputs(ph, chh, THR, offset=oh))])
-    t = timed(lambda: rnd.run(fleet, inp))
+    t = timed_captured(rnd, fleet, inp, -1)
     out["configs[2] 16k mixed (8k arms 64x7 + 8k humanoids 64x32) k=1024"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "163 MB of chunks (> 126 MB L2): mostly streamed from HBM",
-        "layout": "the two groups' horizon kernels on forked streams, then urgency + admission"}
+        "layout": "split, uncapped: the two groups' horizon kernels on forked streams || "
+                  "urgency + admission"}
     # configs[3]: 64k robots, 8-sample ensembles 50x7, k = 8192 (one GPU's whole fleet)
     R = 65536
     soa = synthetic.fleet_soa(R, seed=16)
@@ -430,10 +431,10 @@ def other_configs(reps: int = 200):
     prev, cand, off = synthetic.chunks(R, seed=17, S=8)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
-    t = timed(lambda: rnd.run(fleet, inp))
+    t = timed_captured(rnd, fleet, inp, 4)
     out["configs[3] 64k robots S=8 ensembles 50x7 k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
-        "l2": "streams from HBM (826 MB inputs)"}
+        "l2": "streams from HBM (826 MB inputs)", "layout": "split, 4 reserved SMs"}
     # the headline fleet with the confidence policy (paper default t=0.4, H_min=5)
     from paper_2605_11381_b200 import HorizonPolicyConfig
     R = 1 << 20

@@ -24,7 +24,7 @@ subset of the union of local top-k' sets and keys are unique.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist

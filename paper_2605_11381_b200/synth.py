@@ -24,7 +24,6 @@ from fractions import Fraction
 from pathlib import Path
 from typing import Optional
 
-import numpy as np
 import torch
 
 from . import _lib

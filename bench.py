@@ -458,6 +458,43 @@ def other_configs(reps: int = 200):
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (1.26 GB of magnitudes)",
         "layout": "split: horizons || urgency + admission (8 reserved SMs)"}
+    # the headline fleet with a cloud tier (phase 3 at fleet scale, §8(f)1):
+    # full key order + edge admission + the ordered offload scan
+    import numpy as np
+    from paper_2605_11381_b200 import engines as eng
+    R, k = 1 << 20, 8192
+    soa = synthetic.fleet_soa(R, seed=20)
+    fleet = fl.DeviceFleet.from_host(soa)
+    prev, cand, off = synthetic.chunks(R, seed=21)
+    edge = eng.EngineProfile(tier="edge", capacity=k, max_batch=256,
+                             points=((1, 150_000), (256, 400_000)))
+    cloud = eng.EngineProfile(tier="cloud", capacity=2048, max_batch=512,
+                              points=((1, 80_000), (512, 250_000)))
+    net = eng.NetworkModel(base_latency_us=20_000, uplink_bps=400_000_000,
+                           downlink_bps=1_000_000_000)
+    rnd = rounds.HybridDecisionRound(R, k, sched_for(soa), cloud.capacity)
+    payload = torch.from_numpy(np.random.default_rng(22).choice(
+        np.array([100_000, 300_000, 2_000_000], np.int64), R)).cuda()
+    rnd.set_cloud(eng.transfer_time_batch(net, payload, eng.UP),
+                  eng.cloud_thresholds(edge, cloud, net, 0, 0, k, rnd.cap))
+    inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
+    for _ in range(5):
+        rnd.run(fleet, inp)
+    torch.cuda.synchronize()
+    n_cloud = int(rnd.n_cloud.item())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps // 4):
+        rnd.run(fleet, inp)  # eager: the full sort reads its pass plan back (one sync)
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3 / (reps // 4)
+    out["configs[4] per-GPU share with a cloud tier (k=8192 edge, 2048 cloud slots)"] = {
+        "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t, "cloud_placed": n_cloud,
+        "full_sorts": rnd.full_sorts,
+        "layout": "eager, sequential: horizons, urgency, ordered top k + 4096 (fused select), "
+                  "edge admission, ordered offload scan, one 4-byte read of the slot count "
+                  "(rounds.HybridDecisionRound)"}
     return out
 
 

@@ -877,42 +877,76 @@ __global__ void k_transfer_time(const int64_t* payload, int64_t n, int64_t base_
 // one to the cloud iff  cloud_est(req, c) < edge_est  while c = |S_c| < cap.
 // cloud_est = C(c) + up(payload), with C(c) (queue drain + batch latency +
 // downlink) non-decreasing in c, so the test is up_r < T(c) = edge_est - C(c),
-// T non-increasing (host-computed per round).  The greedy scan is therefore
-// "the first request after the last acceptance with up_r < T(c)", searched
-// 1024 requests at a time by one CTA; when no request qualifies at c none can
-// at c + 1 either.  Accepted requests get their skip counter reset and their
-// stale-observation refetch flag (scheduler.py:223-234).
+// T non-increasing (host-computed per round).  With m_r = #{c < cap : T(c) >
+// up_r} (a binary search, T being non-increasing) the walk is the recurrence
+// fire_r = [c_r < m_r], c_{r+1} = c_r + fire_r.  One CTA takes 1,024 requests
+// per window: all threads compute m, then warp 0 resolves the recurrence 32
+// requests at a time by a ballot fixed point (lane j fires iff c + fires of
+// lanes < j < m_j; iterating from "no earlier fires" fixes at least one more
+// lane per round, and the fixed point is the sequential answer), and every
+// thread applies its own request's placement.  Accepted requests get their
+// skip counter reset and their stale-observation refetch flag
+// (scheduler.py:223-234).
 __global__ void __launch_bounds__(1024) k_place_cloud(const int32_t* order, int n, int n_edge,
                                                       const int64_t* up, const int64_t* thr,
                                                       int cap, const int64_t* obs, int32_t* skipped,
                                                       uint8_t* refetch, int64_t now, int64_t stale,
                                                       int32_t* cloud_idx, int32_t* n_cloud) {
-    __shared__ int best;
-    int pos = n_edge, c = 0;
-    while (c < cap && pos < n) {
-        const int64_t t = thr[c];
-        int found = INT_MAX;
-        for (int base = pos; base < n; base += blockDim.x) {
-            if (threadIdx.x == 0) best = INT_MAX;
-            __syncthreads();
-            const int r = base + threadIdx.x;
-            if (r < n && up[order[r]] < t) atomicMin(&best, r);
-            __syncthreads();
-            found = best;
-            __syncthreads();
-            if (found != INT_MAX) break;
+    __shared__ int s_m[1024];
+    __shared__ uint32_t s_fire[32];
+    __shared__ int s_pre[32];
+    __shared__ int s_c;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_c = 0;
+    __syncthreads();
+    for (int base = n_edge; base < n; base += 1024) {
+        const int c0 = s_c;
+        if (c0 >= cap) break;
+        const int r = base + tid;
+        int m = 0;
+        if (r < n) {
+            const int64_t u = up[order[r]];
+            int lo = 0, hi = cap;  // first c with T(c) <= u
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (thr[mid] > u) lo = mid + 1;
+                else hi = mid;
+            }
+            m = lo;
         }
-        if (found == INT_MAX) break;  // T only decreases: nothing qualifies later
-        if (threadIdx.x == 0) {
-            const int i = order[found];
-            cloud_idx[c] = i;
+        s_m[tid] = m;
+        __syncthreads();
+        if (warp == 0) {
+            int cc = c0;
+            const uint32_t below = (1u << lane) - 1u;
+            for (int ch = 0; ch < 32; ch++) {
+                const int mm = s_m[ch * 32 + lane];
+                uint32_t f = __ballot_sync(0xffffffffu, cc < mm);
+                for (;;) {
+                    const uint32_t g = __ballot_sync(0xffffffffu, cc + __popc(f & below) < mm);
+                    if (g == f) break;
+                    f = g;
+                }
+                if (lane == 0) {
+                    s_fire[ch] = f;
+                    s_pre[ch] = cc;
+                }
+                cc += __popc(f);
+            }
+            if (lane == 0) s_c = cc;
+        }
+        __syncthreads();
+        const uint32_t f = s_fire[warp];
+        if ((f >> lane) & 1u) {
+            const int slot = s_pre[warp] + __popc(f & ((1u << lane) - 1u));
+            const int i = order[r];
+            cloud_idx[slot] = i;
             if (skipped) skipped[i] = 0;
             if (refetch) refetch[i] = now - obs[i] > stale;
         }
-        c++;
-        pos = found + 1;
+        __syncthreads();
     }
-    if (threadIdx.x == 0) *n_cloud = c;
+    if (tid == 0) *n_cloud = s_c;
 }
 
 static unsigned grid_stream(int64_t n) {

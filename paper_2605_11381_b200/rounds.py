@@ -272,6 +272,95 @@ class DecisionRound:
         return self.outputs()
 
 
+class HybridDecisionRound(DecisionRound):
+    """Single-GPU fleet round with the phase-3 cloud tier (scheduler.py:193-234,
+    §8(f)1 at fleet scale): edge admission of the first k in key order
+    (kr_admit), then the ordered offload scan over the following ranks
+    (kr_place_cloud) against the round's per-count thresholds
+    T(c) = edge_est - (drain(c) + batch(c+1) + down) (engines.cloud_thresholds,
+    host integers) and the requests' uplink times.
+
+    The scan usually fills the cloud slots within a few thousand ranks, so the
+    order is only materialised for the first k + window ranks (the fused
+    select, no side effects); when the scan reaches the end of that window
+    with slots left (one 4-byte read back), the full key order is sorted and
+    the scan re-run over it (the placement is idempotent).  Outputs: the
+    round's `outputs()` (edge = order[:k]) plus `cloud()` in offload order;
+    deferred = everything else."""
+
+    def __init__(self, R: int, k: int, sched: _lib.KrSched, cloud_cap: int,
+                 window: int | None = None):
+        super().__init__(R, k, sched)
+        d = dev.device()
+        self.cap = max(0, min(int(cloud_cap), R - self.k))
+        self.kp = min(R, self.k + (window if window is not None else max(2 * self.cap, 4096)))
+        self.cand_idx = torch.empty(max(self.kp, 1), dtype=torch.int32, device=d)
+        self.cand_keys = fl.new_keys(max(self.kp, 1), d)
+        self.order = None  # full order (fallback only)
+        self.sorted_keys = None
+        self.cloud_idx = torch.empty(max(self.cap, 1), dtype=torch.int32, device=d)
+        self.n_cloud = torch.zeros(1, dtype=torch.int32, device=d)
+        self.up_us = None
+        self.thresholds = None
+        self.full_sorts = 0  # rounds that needed the full order (diagnostic)
+
+    def set_cloud(self, up_us: torch.Tensor, thresholds) -> None:
+        """up_us [R] int64 (engines.transfer_time_batch of each request's
+        payload); thresholds: T(c) for c < cap (engines.cloud_thresholds)."""
+        if up_us.shape[0] != self.R or up_us.dtype != torch.int64:
+            raise ValueError("up_us must be an int64 tensor of R uplink times")
+        thr = torch.as_tensor(list(thresholds)[: self.cap], dtype=torch.int64)
+        if thr.numel() < self.cap:
+            raise ValueError("need a threshold for every cloud slot")
+        self.up_us = up_us
+        self.thresholds = thr.to(up_us.device)
+
+    def _place(self, fleet, order: torch.Tensor, n: int) -> None:
+        fs = fleet.c_struct()
+        _lib.check(self.lib.kr_place_cloud(
+            order.data_ptr(), n, self.k, self.up_us.data_ptr(), self.thresholds.data_ptr(),
+            self.cap, ctypes.byref(fs), ctypes.byref(self.sched), self.refetch.data_ptr(),
+            self.cloud_idx.data_ptr(), self.n_cloud.data_ptr(), dev.stream()), "kr_place_cloud")
+
+    def admit(self, fleet: fl.DeviceFleet) -> None:
+        k, R = self.k, self.R
+        if self.cap > 0 and self.up_us is None:
+            raise RuntimeError("set_cloud() first: the round has a cloud tier")
+        # the ordered first kp ranks, no side effects
+        fl.select_admit(self.keys, self.kp, self.ws, key_stats=self.key_stats,
+                        edge_idx=self.cand_idx, edge_keys=self.cand_keys)
+        kth_ptr = self.cand_keys.data_ptr() + (k - 1) * 16 if 0 < k < R else None
+        fl.admit(self.keys, k, kth_ptr, fleet, self.sched, None, admitted=self.admitted,
+                 refetch=self.refetch)
+        if self.cap == 0:
+            self.n_cloud.zero_()
+            return
+        self._place(fleet, self.cand_idx, self.kp)
+        if self.kp < R and int(self.n_cloud.item()) < self.cap:
+            if self.order is None:
+                self.order = torch.empty(R, dtype=torch.int32, device=self.keys.device)
+                self.sorted_keys = fl.new_keys(R, self.keys.device)
+            fl.sort_keys(self.keys, self.ws, order=self.order, sorted_keys=self.sorted_keys)
+            self._place(fleet, self.order, R)
+            self.full_sorts += 1
+
+    def outputs(self) -> RoundOutputs:
+        return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
+                            self.cand_keys[: self.k], self.cand_idx[: self.k], self.kth)
+
+    def cloud(self) -> torch.Tensor:
+        """The offloaded robots in offload order (one device->host read)."""
+        return self.cloud_idx[: int(self.n_cloud.item())]
+
+    def full_order(self) -> torch.Tensor:
+        """The complete key order (sorted on demand when the round did not)."""
+        if self.order is None:
+            self.order = torch.empty(self.R, dtype=torch.int32, device=self.keys.device)
+            self.sorted_keys = fl.new_keys(self.R, self.keys.device)
+        fl.sort_keys(self.keys, self.ws, order=self.order, sorted_keys=self.sorted_keys)
+        return self.order
+
+
 def sharded_topk(keys, n_local: int, k: int, sizes: list, ops, group=None):
     """Exact global top-k admission over robot-sharded keys (host protocol).
 

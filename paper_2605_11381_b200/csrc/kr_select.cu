@@ -29,7 +29,10 @@ namespace kr {
 
 constexpr int kDigitBits = 11;
 constexpr int kBins = 1 << kDigitBits;
-constexpr int kSortTile = 2048;  // LSD radix: elements per CTA tile (256 threads x 8)
+#ifndef KR_SORT_TILE
+#define KR_SORT_TILE 4096
+#endif
+constexpr int kSortTile = KR_SORT_TILE;  // LSD radix: elements per CTA tile (256 threads x 16)
 
 struct SelState {
     unsigned long long st[2][4];  // [parity] {or_hi, or_lo, and_hi, and_lo}
@@ -709,21 +712,41 @@ __global__ void __launch_bounds__(256) k_rs_hist(const kr_key* keys, int64_t n, 
     const int64_t t = blockIdx.x;
     const int64_t lo = t * kSortTile, hi = lo + kSortTile < n ? lo + kSortTile : n;
     const unsigned mask = (1u << width) - 1;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        kr_key k = keys[i];
-        atomicAdd(&h[shr128_lo(k.hi, k.lo, shift) & mask], 1u);
+    const int lane = threadIdx.x & 31;
+    // warp-aggregated: high windows (bucket, aged estimate) hold few distinct
+    // digits, and per-element shared atomics on one bin serialise
+    for (int64_t base = lo; base < hi; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        unsigned d = 0xFFFFFFFFu;
+        if (i < hi) {
+            const kr_key k = keys[i];
+            d = static_cast<unsigned>(shr128_lo(k.hi, k.lo, shift) & mask);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
     }
     __syncthreads();
     tile_hist[static_cast<int64_t>(threadIdx.x) * ntiles + t] = h[threadIdx.x];
 }
 
-// Exclusive scan of m entries in place, one CTA of 1024 threads.
+// Exclusive scan of m entries in place, one CTA of 1024 threads: each thread
+// owns a contiguous segment (a multiple of 16 entries), read and rewritten
+// with four independent 16-byte accesses per step so the loads overlap.
 __global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* a, int64_t m) {
     __shared__ unsigned int part[1024];
-    const int64_t per = (m + blockDim.x - 1) / blockDim.x;
-    const int64_t lo = threadIdx.x * per, hi = lo + per < m ? lo + per : m;
+    int64_t per = (m + blockDim.x - 1) / blockDim.x;
+    per = (per + 15) & ~int64_t(15);
+    const int64_t lo = threadIdx.x * per < m ? threadIdx.x * per : m;
+    const int64_t hi = lo + per < m ? lo + per : m;
     unsigned int s = 0;
-    for (int64_t i = lo; i < hi; i++) s += a[i];
+    int64_t i = lo;
+    for (; i + 16 <= hi; i += 16) {
+        const uint4* q = reinterpret_cast<const uint4*>(a + i);
+        const uint4 x0 = q[0], x1 = q[1], x2 = q[2], x3 = q[3];
+        s += x0.x + x0.y + x0.z + x0.w + x1.x + x1.y + x1.z + x1.w +
+             x2.x + x2.y + x2.z + x2.w + x3.x + x3.y + x3.z + x3.w;
+    }
+    for (; i < hi; i++) s += a[i];
     part[threadIdx.x] = s;
     __syncthreads();
     for (int o = 1; o < blockDim.x; o <<= 1) {
@@ -733,7 +756,22 @@ __global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* a, int64_t m) {
         __syncthreads();
     }
     unsigned int run = threadIdx.x ? part[threadIdx.x - 1] : 0;
-    for (int64_t i = lo; i < hi; i++) {
+    i = lo;
+    for (; i + 16 <= hi; i += 16) {
+        uint4* q = reinterpret_cast<uint4*>(a + i);
+        uint4 x[4] = {q[0], q[1], q[2], q[3]};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const unsigned int v0 = x[j].x, v1 = x[j].y, v2 = x[j].z, v3 = x[j].w;
+            x[j].x = run; run += v0;
+            x[j].y = run; run += v1;
+            x[j].z = run; run += v2;
+            x[j].w = run; run += v3;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) q[j] = x[j];
+    }
+    for (; i < hi; i++) {
         unsigned int v = a[i];
         a[i] = run;
         run += v;
@@ -754,11 +792,15 @@ __global__ void __launch_bounds__(256) k_rs_scatter(const kr_key* keys, const in
     for (int d = lane; d < 256; d += 32) wc[warp][d] = 0;
     __syncwarp();
     for (int c = 0; c < per_warp; c += 32) {
-        int64_t i = wlo + c + lane;
+        const int64_t i = wlo + c + lane;
+        unsigned d = 0xFFFFFFFFu;
         if (i < n) {
-            kr_key k = keys[i];
-            atomicAdd(&wc[warp][shr128_lo(k.hi, k.lo, shift) & mask], 1u);
+            const kr_key k = keys[i];
+            d = static_cast<unsigned>(shr128_lo(k.hi, k.lo, shift) & mask);
         }
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d != 0xFFFFFFFFu && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
+        __syncwarp();
     }
     __syncthreads();
     {

@@ -272,6 +272,12 @@ KR_API int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
  * (nullable) and the k-th smallest to kth_out (nullable); k <= W * len. */
 KR_API int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t k, kr_key* out_keys,
                          kr_key* kth_out, void* stream);
+/* kr_merge_runs that also records, for each output rank, the element's
+ * position in `runs` (run r, slot j -> r * len + j): lets a caller carry
+ * per-candidate payloads (e.g. uplink times for the cloud scan) through the
+ * merge.  out_pos may be NULL. */
+KR_API int kr_merge_runs_pos(const kr_key* runs, int32_t W, int64_t len, int64_t k,
+                             kr_key* out_keys, int32_t* out_pos, kr_key* kth_out, void* stream);
 
 /* ---- phase 3: hybrid edge / cloud placement --------------------------- */
 

@@ -125,6 +125,7 @@ _SIGNATURES = {
                                 ctypes.c_size_t, _vp]),
     "kr_sort_keys": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "kr_merge_runs": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp, _vp, _vp]),
+    "kr_merge_runs_pos": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp]),
     "kr_transfer_time": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "kr_trace_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, _i64,
                                       ctypes.POINTER(_vp)]),

@@ -668,7 +668,8 @@ __global__ void __launch_bounds__(256) k_small_apply(SmallAdmitArgs a) {
 // sentinels -- broken by position).  Ranks < k are the global S_e in order;
 // rank k - 1 is the global k-th key.
 __global__ void __launch_bounds__(256) k_merge_runs(const kr_key* runs, int W, int len, int k,
-                                                    kr_key* out_keys, kr_key* kth_out) {
+                                                    kr_key* out_keys, int32_t* out_pos,
+                                                    kr_key* kth_out) {
     const int m = W * len;
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
@@ -693,6 +694,7 @@ __global__ void __launch_bounds__(256) k_merge_runs(const kr_key* runs, int W, i
             const int rank = c + (e - own * len);
             if (rank < k) {
                 if (out_keys) out_keys[rank] = x;
+                if (out_pos) out_pos[rank] = e;
                 if (kth_out && rank == k - 1) *kth_out = x;
             }
         }
@@ -1046,8 +1048,9 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
                                int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* ws,
                                size_t ws_bytes, void* stream);
 
-extern "C" int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t k,
-                             kr_key* out_keys, kr_key* kth_out, void* stream) {
+extern "C" int kr_merge_runs_pos(const kr_key* runs, int32_t W, int64_t len, int64_t k,
+                                 kr_key* out_keys, int32_t* out_pos, kr_key* kth_out,
+                                 void* stream) {
     if (W < 1 || len < 0 || k < 0 || k > static_cast<int64_t>(W) * len ||
         static_cast<int64_t>(W) * len > INT_MAX)
         return KR_EINVAL;
@@ -1058,8 +1061,13 @@ extern "C" int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t
     const int64_t cap = static_cast<int64_t>(device_info().sm_count) * 64;
     if (blocks > cap) blocks = cap;
     k_merge_runs<<<static_cast<unsigned>(blocks), 256, 0, as_stream(stream)>>>(
-        runs, W, static_cast<int>(len), static_cast<int>(k), out_keys, kth_out);
+        runs, W, static_cast<int>(len), static_cast<int>(k), out_keys, out_pos, kth_out);
     return check_launch("kr_merge_runs");
+}
+
+extern "C" int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t k,
+                             kr_key* out_keys, kr_key* kth_out, void* stream) {
+    return kr_merge_runs_pos(runs, W, len, k, out_keys, nullptr, kth_out, stream);
 }
 
 extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth,

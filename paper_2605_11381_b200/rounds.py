@@ -462,3 +462,106 @@ class ShardedDecisionRound(DecisionRound):
     def outputs(self) -> RoundOutputs:
         return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
                             self.global_edge[: self.k_global], None, self.kth_global)
+
+
+class ShardedHybridRound(ShardedDecisionRound):
+    """Robot-sharded round with the phase-3 cloud tier (SURVEY §8(e) extension).
+
+    Edge admission is the sharded top-k protocol above.  For the cloud scan
+    every rank contributes its ordered local top k + window candidates with
+    their uplink times; one all-gather, the same merge on every rank (keeping
+    each candidate's position so its uplink time follows it), and the same
+    ordered offload scan over the global first k + window ranks
+    (kr_place_cloud) -- identical on every rank.  If the scan runs out of
+    ranks with slots left, every rank widens the window 4x and repeats (the
+    decision is the same everywhere).  Each rank then applies the placements
+    of its own robots (skip counter reset, stale-observation refetch).
+    up_us: this shard's uplink times; thresholds: the global T(c)."""
+
+    def __init__(self, R_local: int, k: int, sched: _lib.KrSched, cloud_cap: int, group=None,
+                 window: int | None = None):
+        super().__init__(R_local, k, sched, group)
+        self.rank = dist.get_rank(group)
+        self.total = sum(self.sizes)
+        self.cap = max(0, min(int(cloud_cap), self.total - self.k_global))
+        self.window = window if window is not None else max(2 * self.cap, 4096)
+        self.up_us = None
+        self.thresholds = None
+        self.widened = 0
+        self.cloud_keys = fl.new_keys(max(self.cap, 1), self.H.device)
+        self.n_cloud = 0
+
+    def set_cloud(self, up_us: torch.Tensor, thresholds) -> None:
+        if up_us.shape[0] != self.R or up_us.dtype != torch.int64:
+            raise ValueError("up_us must be an int64 tensor of this shard's uplink times")
+        thr = torch.as_tensor(list(thresholds)[: self.cap], dtype=torch.int64)
+        if thr.numel() < self.cap:
+            raise ValueError("need a threshold for every cloud slot")
+        self.up_us = up_us
+        self.thresholds = thr.to(up_us.device)
+
+    def _gather(self, t: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype,
+                          device=t.device)
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(out, t, group=self.group)
+        else:  # gloo (tests: several ranks sharing one device)
+            dist.all_gather(list(out.chunk(self.world)), t, group=self.group)
+        return out
+
+    def admit(self, fleet: fl.DeviceFleet) -> None:
+        super().admit(fleet)  # edge: global top-k, masks, skip counters
+        self.n_cloud = 0
+        if self.cap == 0:
+            return
+        if self.up_us is None:
+            raise RuntimeError("set_cloud() first: the round has a cloud tier")
+        d, st = self.H.device, dev.stream()
+        window = self.window
+        while True:
+            kg2 = min(self.k_global + window, self.total)
+            kl2 = min(kg2, self.R)
+            cand_keys = fl.new_keys(kg2, d)
+            cand_keys.fill_(ALL_ONES)
+            cand_idx = torch.zeros(kg2, dtype=torch.int32, device=d)
+            cand_up = torch.zeros(kg2, dtype=torch.int64, device=d)
+            if kl2 > 0:
+                fl.select_admit(self.keys, kl2, self.ws, key_stats=self.key_stats,
+                                edge_idx=cand_idx, edge_keys=cand_keys)
+                cand_up[:kl2] = self.up_us[cand_idx[:kl2].long()]
+            g_keys, g_up = self._gather(cand_keys), self._gather(cand_up)
+            merged = fl.new_keys(kg2, d)
+            pos = torch.empty(kg2, dtype=torch.int32, device=d)
+            _lib.check(self.lib.kr_merge_runs_pos(g_keys.data_ptr(), self.world, kg2, kg2,
+                                                  merged.data_ptr(), pos.data_ptr(), None, st),
+                       "kr_merge_runs_pos")
+            cloud_pos = torch.empty(self.cap, dtype=torch.int32, device=d)
+            n_t = torch.zeros(1, dtype=torch.int32, device=d)
+            _lib.check(self.lib.kr_place_cloud(
+                pos.data_ptr(), kg2, self.k_global, g_up.data_ptr(), self.thresholds.data_ptr(),
+                self.cap, None, None, None, cloud_pos.data_ptr(), n_t.data_ptr(), st),
+                "kr_place_cloud")
+            n = int(n_t.item())
+            if n == self.cap or kg2 == self.total:
+                break
+            window *= 4
+            self.widened += 1
+        self.n_cloud = n
+        placed = cloud_pos[:n].long()
+        self.cloud_keys[:n] = g_keys[placed]
+        mine = placed[(placed // kg2) == self.rank] % kg2
+        m = int(mine.numel())
+        if m:  # this shard's placements: skip reset + refetch (kr_place_cloud, all qualify)
+            local = cand_idx[mine].contiguous()
+            zeros = torch.zeros(self.R, dtype=torch.int64, device=d)  # indexed by robot
+            big = torch.full((m,), (1 << 63) - 1, dtype=torch.int64, device=d)
+            out = torch.empty(m, dtype=torch.int32, device=d)
+            fs = fleet.c_struct()
+            _lib.check(self.lib.kr_place_cloud(
+                local.data_ptr(), m, 0, zeros.data_ptr(), big.data_ptr(), m, ctypes.byref(fs),
+                ctypes.byref(self.sched), self.refetch.data_ptr(), out.data_ptr(),
+                n_t.data_ptr(), st), "kr_place_cloud(apply)")
+
+    def cloud(self) -> torch.Tensor:
+        """The global offload set as keys, in offload order (same on every rank)."""
+        return self.cloud_keys[: self.n_cloud]

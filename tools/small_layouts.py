@@ -1,5 +1,6 @@
 """configs[1]-[3] rounds under each captured layout (sequential graph vs the
-two concurrent layouts, reserved-SM variants): python tools/small_layouts.py"""
+two concurrent layouts, reserved-SM variants): python tools/small_layouts.py
+[--confidence: the 2^20-robot confidence-policy round instead]"""
 import json
 import sys
 from pathlib import Path
@@ -40,6 +41,13 @@ def bench(fn):
 
 
 def cases():
+    if "--confidence" in sys.argv:  # the headline fleet under the confidence policy
+        from paper_2605_11381_b200 import HorizonPolicyConfig
+        R = 1 << 20
+        soa = synthetic.fleet_soa(R, seed=18)
+        yield "configs[4] confidence", R, 8192, soa, rounds.ConfidenceInputs(
+            synthetic.magnitudes(R, seed=19), HorizonPolicyConfig.confidence(0.4, 5))
+        return
     R = 1024
     soa = synthetic.fleet_soa(R, seed=11)
     prev, cand, off = synthetic.chunks(R, seed=12)
@@ -61,7 +69,7 @@ for name, R, k, soa, inp in cases():
     fleet = fl.DeviceFleet.from_host(soa)
     res = {"sequential": timed_seq(rounds.DecisionRound(R, k, sched_for(soa)), fleet, inp)}
     for layout in ("split", "urgency_first"):
-        for reserve in (-1, 4, 8, 16):
+        for reserve in ((-1, 4, 8, 16, 24, 32) if "--confidence" in sys.argv else (-1, 4, 8, 16)):
             rnd = rounds.DecisionRound(R, k, sched_for(soa))
             rnd.capture(fleet, inp, reserve_sms=reserve, layout=layout)
             res[f"{layout} reserve={reserve}"] = bench(rnd.replay)

@@ -313,14 +313,23 @@ struct SweepWork {
         const int g = threadIdx.x & 15;
         const int n0 = 2 * g, n1 = 32 + 2 * g;
         const bool p0 = robot_ok && n0 < N, p1 = robot_ok && n1 < N;
+        const bool odd = N & 1;  // rows are not pair-aligned: guarded scalar loads
         int j[4] = {0, 0, 0, 0};
         if (p0) {
             T sf[4], fin[4];
             uint32_t mx = 0;
             for (int k = 0; k < Kr; k++) {
                 T x[4] = {T(0), T(0), T(0), T(0)};
-                load_pair(rob + k * N + n0, x[0], x[1]);
-                if (p1) load_pair(rob + k * N + n1, x[2], x[3]);
+                const T* row = rob + k * N;
+                if (!odd) {
+                    load_pair(row + n0, x[0], x[1]);
+                    if (p1) load_pair(row + n1, x[2], x[3]);
+                } else {  // a column past N stays zero: filter() gives 0
+                    x[0] = row[n0];
+                    if (n0 + 1 < N) x[1] = row[n0 + 1];
+                    if (p1) x[2] = row[n1];
+                    if (n1 + 1 < N) x[3] = row[n1 + 1];
+                }
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
                     mx = max(mx, CW::sexp(x[c]));
@@ -338,9 +347,10 @@ struct SweepWork {
                 any = any || j[c] < 0;
             }
             if (any) {
-                const int nc = p1 ? 4 : 2;
-                for (int c = 0; c < nc; c++) {
-                    const T* col = rob + (c < 2 ? n0 + c : n1 + c - 2);
+                for (int c = 0; c < 4; c++) {
+                    const int n = c < 2 ? n0 + c : n1 + c - 2;
+                    if (n >= N) continue;
+                    const T* col = rob + n;
                     if (bad)
                         for (int k = 0; k < Kr; k++) fl |= CW::check(col[k * N]);
                     if (bad || j[c] < 0) {
@@ -522,9 +532,9 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
     if (al && sizeof(T) == 4 && N % 4 == 0 && N > 64) vc = 4;
 #define KR_SWEEP(KK, VV) \
     return go(SweepWork<T, KK, VV>{}, k_horizon_sweep<T, KK, VV, true>, k_horizon_sweep<T, KK, VV, false>)
-    // two robots per warp: N <= 64, even, 16-byte aligned base
+    // two robots per warp: N <= 64 (pair loads when N is even and the base 16-byte aligned)
     static const bool half_off = std::getenv("KR_SWEEP_NO_HALF") != nullptr;  // A/B knob
-    if (!half_off && N <= 64 && N % 2 == 0 && al) {
+    if (!half_off && N <= 64 && (N % 2 == 1 || al)) {
         if (K == 6)
             return go(SweepWork<T, 6, 1, true>{}, k_horizon_sweep<T, 6, 1, true, true>,
                       k_horizon_sweep<T, 6, 1, false, true>);

@@ -59,6 +59,14 @@ def main():
         t = timeit(lambda: kb.sweep_horizon_sums(cfgs, U, validate=False))
         report(f"sweep C={C}{' tie@0.8' if tie else ''} K=6 N=50 float32 (sums)", R, 6 * 50 * 4, t)
     del U
+    # the other layouts: fp64 storage, N = 49 (odd: warp per robot), N = 128 (VC = 4)
+    cfgs = [kb.HorizonPolicyConfig.confidence(0.013 + 0.947 * c / 15, 1 + c % 8) for c in range(16)]
+    for K, N, dt, es in [(6, 50, torch.float64, 8), (6, 49, torch.float32, 4),
+                         (6, 128, torch.float32, 4)]:
+        U = synthetic.magnitudes(R, seed=3, K=K, N=N, dtype=dt)
+        t = timeit(lambda: kb.sweep_horizon_sums(cfgs, U, validate=False))
+        report(f"sweep C=16 K={K} N={N} {str(dt)[6:]} (sums)", R, K * N * es, t)
+        del U
     for S, L, D, RR in [(1, 50, 7, R), (1, 64, 32, R // 2), (8, 50, 7, R // 4)]:
         prev, cand, off = synthetic.chunks(RR, seed=5, Lp=L, Lc=L, D=D, S=S)
         out = torch.empty(RR, dtype=torch.int32, device="cuda")

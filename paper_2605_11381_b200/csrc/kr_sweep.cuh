@@ -525,11 +525,10 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
         w.H = H; w.sums = sums; w.flags = flags; w.R = R;
         return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_sweep", 0, cfg);
     };
-    // columns per lane: the fewest 32-lane chunks, then the most lanes busy
+    // N > 64 (or a misaligned base): a warp per robot, chunks of 32 lanes x VC
+    // columns; VC = 2 (pair loads) when the rows allow it.  (VC = 4 was
+    // measured 2x slower at N = 128: 0.86 vs 1.75 ms, register spills.)
     const bool al = (reinterpret_cast<uintptr_t>(U) & 15u) == 0;
-    int vc = 1;
-    if (al && N % 2 == 0 && N > 32) vc = 2;
-    if (al && sizeof(T) == 4 && N % 4 == 0 && N > 64) vc = 4;
 #define KR_SWEEP(KK, VV) \
     return go(SweepWork<T, KK, VV>{}, k_horizon_sweep<T, KK, VV, true>, k_horizon_sweep<T, KK, VV, false>)
     // two robots per warp: N <= 64 (pair loads when N is even and the base 16-byte aligned)
@@ -541,17 +540,9 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
         return go(SweepWork<T, 0, 1, true>{}, k_horizon_sweep<T, 0, 1, true, true>,
                   k_horizon_sweep<T, 0, 1, false, true>);
     }
-    if constexpr (sizeof(T) == 4) {
-        if (vc == 4) KR_SWEEP(0, 4);
-        if (vc == 2) {
-            if (K == 6) KR_SWEEP(6, 2);
-            KR_SWEEP(0, 2);
-        }
-    } else {
-        if (vc == 2) {
-            if (K == 6) KR_SWEEP(6, 2);
-            KR_SWEEP(0, 2);
-        }
+    if (al && N % 2 == 0 && N > 32) {
+        if (K == 6) KR_SWEEP(6, 2);
+        KR_SWEEP(0, 2);
     }
     KR_SWEEP(0, 1);
 #undef KR_SWEEP

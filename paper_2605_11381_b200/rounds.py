@@ -467,16 +467,17 @@ class ShardedDecisionRound(DecisionRound):
 class ShardedHybridRound(ShardedDecisionRound):
     """Robot-sharded round with the phase-3 cloud tier (SURVEY §8(e) extension).
 
-    Edge admission is the sharded top-k protocol above.  For the cloud scan
-    every rank contributes its ordered local top k + window candidates with
+    Every rank contributes its ordered local top k + window candidates with
     their uplink times; one all-gather, the same merge on every rank (keeping
-    each candidate's position so its uplink time follows it), and the same
-    ordered offload scan over the global first k + window ranks
-    (kr_place_cloud) -- identical on every rank.  If the scan runs out of
-    ranks with slots left, every rank widens the window 4x and repeats (the
-    decision is the same everywhere).  Each rank then applies the placements
-    of its own robots (skip counter reset, stale-observation refetch).
-    up_us: this shard's uplink times; thresholds: the global T(c)."""
+    each candidate's position so its uplink time follows it): the merged first
+    k ranks are the global S_e (edge admission by the k-th key, exactly as the
+    edge-only protocol), and the same ordered offload scan runs over the
+    following ranks (kr_place_cloud) -- identical on every rank.  If the scan
+    runs out of ranks with slots left, every rank widens the window 4x and
+    repeats the cloud part (the decision is the same everywhere).  Each rank
+    then applies the placements of its own robots (skip counter reset,
+    stale-observation refetch).  up_us: this shard's uplink times;
+    thresholds: the global T(c)."""
 
     def __init__(self, R_local: int, k: int, sched: _lib.KrSched, cloud_cap: int, group=None,
                  window: int | None = None):
@@ -509,36 +510,58 @@ class ShardedHybridRound(ShardedDecisionRound):
             dist.all_gather(list(out.chunk(self.world)), t, group=self.group)
         return out
 
+    def _candidates(self, kg2: int):
+        """This shard's ordered top min(kg2, R) keys (sentinel-padded to kg2),
+        their local indices and uplink times; no side effects."""
+        d = self.H.device
+        kl2 = min(kg2, self.R)
+        cand_keys = fl.new_keys(kg2, d)
+        cand_keys.fill_(ALL_ONES)
+        cand_idx = torch.zeros(kg2, dtype=torch.int32, device=d)
+        cand_up = torch.zeros(kg2, dtype=torch.int64, device=d)
+        if kl2 > 0:
+            fl.select_admit(self.keys, kl2, self.ws, key_stats=self.key_stats,
+                            edge_idx=cand_idx, edge_keys=cand_keys)
+            if self.cap > 0:
+                cand_up[:kl2] = self.up_us[cand_idx[:kl2].long()]
+        return cand_keys, cand_idx, cand_up
+
     def admit(self, fleet: fl.DeviceFleet) -> None:
-        super().admit(fleet)  # edge: global top-k, masks, skip counters
-        self.n_cloud = 0
-        if self.cap == 0:
-            return
-        if self.up_us is None:
+        """One select, one all-gather of (key, uplink) candidates and one merge
+        serve both tiers: the merged first k_global ranks are the global S_e
+        (edge admission by the k-th key, as in the edge-only protocol), the
+        following ranks feed the offload scan."""
+        if self.cap > 0 and self.up_us is None:
             raise RuntimeError("set_cloud() first: the round has a cloud tier")
         d, st = self.H.device, dev.stream()
-        window = self.window
+        kg = self.k_global
+        window = self.window if self.cap > 0 else 0
+        edge_done = False
+        self.n_cloud = 0
         while True:
-            kg2 = min(self.k_global + window, self.total)
-            kl2 = min(kg2, self.R)
-            cand_keys = fl.new_keys(kg2, d)
-            cand_keys.fill_(ALL_ONES)
-            cand_idx = torch.zeros(kg2, dtype=torch.int32, device=d)
-            cand_up = torch.zeros(kg2, dtype=torch.int64, device=d)
-            if kl2 > 0:
-                fl.select_admit(self.keys, kl2, self.ws, key_stats=self.key_stats,
-                                edge_idx=cand_idx, edge_keys=cand_keys)
-                cand_up[:kl2] = self.up_us[cand_idx[:kl2].long()]
-            g_keys, g_up = self._gather(cand_keys), self._gather(cand_up)
-            merged = fl.new_keys(kg2, d)
-            pos = torch.empty(kg2, dtype=torch.int32, device=d)
-            _lib.check(self.lib.kr_merge_runs_pos(g_keys.data_ptr(), self.world, kg2, kg2,
-                                                  merged.data_ptr(), pos.data_ptr(), None, st),
-                       "kr_merge_runs_pos")
+            kg2 = min(kg + window, self.total)
+            cand_keys, cand_idx, cand_up = self._candidates(kg2)
+            g_keys = self._gather(cand_keys)
+            g_up = self._gather(cand_up) if self.cap > 0 else None
+            merged = fl.new_keys(max(kg2, 1), d)
+            pos = torch.empty(max(kg2, 1), dtype=torch.int32, device=d)
+            if kg2 > 0:
+                _lib.check(self.lib.kr_merge_runs_pos(g_keys.data_ptr(), self.world, kg2, kg2,
+                                                      merged.data_ptr(), pos.data_ptr(), None,
+                                                      st), "kr_merge_runs_pos")
+            if not edge_done:  # global S_e and the local edge admission
+                if kg > 0:
+                    self.global_edge[:kg] = merged[:kg]
+                    self.kth_global.copy_(merged[kg - 1: kg])
+                kth = self.kth_global if 0 < kg < self.total else None
+                CudaShardOps(self, fleet).apply(self.keys, kg, kth)
+                edge_done = True
+            if self.cap == 0:
+                return
             cloud_pos = torch.empty(self.cap, dtype=torch.int32, device=d)
             n_t = torch.zeros(1, dtype=torch.int32, device=d)
             _lib.check(self.lib.kr_place_cloud(
-                pos.data_ptr(), kg2, self.k_global, g_up.data_ptr(), self.thresholds.data_ptr(),
+                pos.data_ptr(), kg2, kg, g_up.data_ptr(), self.thresholds.data_ptr(),
                 self.cap, None, None, None, cloud_pos.data_ptr(), n_t.data_ptr(), st),
                 "kr_place_cloud")
             n = int(n_t.item())

@@ -368,10 +368,10 @@ def round_roofline(soa, R, t_round, peak):
 
 def other_configs(reps: int = 200):
     """The other BASELINE.json configs on this GPU, each one whole decision
-    round (horizons + urgency + top-k admission) replayed from CUDA graphs in
-    the concurrent "split" layout (horizons || urgency + admission), with the
-    reserved-SM count measured best per size (profiles/r1_small_layouts.jsonl,
-    tools/small_layouts.py).
+    round (horizons + urgency + top-k admission) replayed from CUDA graphs,
+    in the concurrent "split" layout (horizons || urgency + admission) where
+    it pays, with the reserved-SM count measured best per size
+    (profiles/r1_small_layouts.jsonl, tools/small_layouts.py).
     configs[1] and [2] are L2-resident (labelled); configs[3] streams from HBM.
     configs[0] (the paper's Fig. 4 scenario) is a correctness case
     (tests/test_gpu_scheduler.py), configs[4] is the headline above."""
@@ -405,10 +405,10 @@ def other_configs(reps: int = 200):
     prev, cand, off = synthetic.chunks(R, seed=12)
     rnd = rounds.DecisionRound(R, 64, sched_for(soa))
     inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
-    t = timed_captured(rnd, fleet, inp, 8)
+    t = timed_captured(rnd, fleet, inp, 0)
     out["configs[1] 1k robots 50x7 k=64"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t, "l2": "resident (0.3 MB inputs)",
-        "layout": "split, 8 reserved SMs"}
+        "layout": "sequential graphs (at 1k robots a second stream costs more than it hides)"}
     # configs[2]: 16k mixed fleet, two homogeneous tensors, 64-step chunks, k = 1024
     R = 16384
     soa = synthetic.fleet_soa(R, seed=13)

@@ -543,46 +543,89 @@ __device__ __forceinline__ bool pair_gt(const kr_key& a, int32_t ia, const kr_ke
 //      smaller pairs in every other run (binary search), computed by one thread
 //      per pair and scattered directly.  Pairs are unique (index tiebreak), so
 //      positions form a permutation.
+struct Pair {
+    kr_key k;
+    int32_t i;
+};
+
+__device__ __forceinline__ Pair shfl_pair(const Pair& p, int lane_mask) {
+    Pair q;
+    q.k.hi = __shfl_xor_sync(0xffffffffu, p.k.hi, lane_mask);
+    q.k.lo = __shfl_xor_sync(0xffffffffu, p.k.lo, lane_mask);
+    q.i = __shfl_xor_sync(0xffffffffu, p.i, lane_mask);
+    return q;
+}
+
+// keep the smaller pair of (mine, other) when keep_min, else the larger
+__device__ __forceinline__ Pair keep(const Pair& mine, const Pair& other, bool keep_min) {
+    const bool gt = pair_gt(mine.k, mine.i, other.k, other.i);
+    return (gt == keep_min) ? other : mine;
+}
+
+// One run of kRun = 256 pairs per CTA, a bitonic network held in registers:
+// thread t owns elements 2t and 2t + 1; partners at distance j = 1 are in the
+// same thread, j = 2..32 in the same warp (shuffles), j = 64, 128 in another
+// warp (one shared-memory exchange each).  Padding is +inf (all-ones, INT_MAX).
 __global__ void __launch_bounds__(kRunThreads) k_run_sort(const kr_key* keys, const int32_t* idx,
                                                           const unsigned int* count_dev, int m_host,
                                                           kr_key* rk, int32_t* ri) {
-    __shared__ kr_key sk[kRun];
-    __shared__ int32_t si[kRun];
+    static_assert(kRun == 2 * kRunThreads, "two elements per thread");
+    __shared__ Pair sp[kRun];
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
     const int base = blockIdx.x * kRun;
     if (base >= m) return;
     const int n = min(kRun, m - base);
-    unsigned np2 = 1;
-    while (np2 < static_cast<unsigned>(n)) np2 <<= 1;
-    for (unsigned i = threadIdx.x; i < np2; i += blockDim.x) {
-        if (i < static_cast<unsigned>(n)) {
-            sk[i] = keys[base + i];
-            si[i] = idx ? idx[base + i] : base + static_cast<int>(i);
+    const int t = threadIdx.x;
+    Pair e[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+        const int x = 2 * t + q;
+        if (x < n) {
+            e[q].k = keys[base + x];
+            e[q].i = idx ? idx[base + x] : base + x;
         } else {
-            sk[i] = kr_key{~0ull, ~0ull};
-            si[i] = INT_MAX;
+            e[q].k = kr_key{~0ull, ~0ull};
+            e[q].i = INT_MAX;
         }
     }
-    __syncthreads();
-    for (unsigned kk = 2; kk <= np2; kk <<= 1) {
-        for (unsigned j = kk >> 1; j > 0; j >>= 1) {
-            for (unsigned t = threadIdx.x; t < np2 / 2; t += blockDim.x) {
-                const unsigned i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
-                const unsigned l = i | j;
-                const bool up = (i & kk) == 0;
-                const kr_key ka = sk[i], kb = sk[l];
-                const int32_t ia = si[i], ib = si[l];
-                if (pair_gt(ka, ia, kb, ib) == up) {
-                    sk[i] = kb; sk[l] = ka;
-                    si[i] = ib; si[l] = ia;
+#pragma unroll
+    for (int kk = 2; kk <= kRun; kk <<= 1) {
+        const bool up = ((2 * t) & kk) == 0;  // same for both elements (kk >= 2)
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j == 1) {
+                if (pair_gt(e[0].k, e[0].i, e[1].k, e[1].i) == up) {
+                    const Pair tmp = e[0];
+                    e[0] = e[1];
+                    e[1] = tmp;
                 }
+            } else {
+                const bool lower = ((2 * t) & j) == 0;  // element below its partner
+                const bool keep_min = lower == up;
+                Pair o[2];
+                if (j <= 32) {
+                    o[0] = shfl_pair(e[0], j >> 1);
+                    o[1] = shfl_pair(e[1], j >> 1);
+                } else {
+                    sp[2 * t] = e[0];
+                    sp[2 * t + 1] = e[1];
+                    __syncthreads();
+                    o[0] = sp[(2 * t) ^ j];
+                    o[1] = sp[(2 * t + 1) ^ j];
+                    __syncthreads();
+                }
+                e[0] = keep(e[0], o[0], keep_min);
+                e[1] = keep(e[1], o[1], keep_min);
             }
-            __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        rk[base + i] = sk[i];
-        ri[base + i] = si[i];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+        const int x = 2 * t + q;
+        if (x < n) {
+            rk[base + x] = e[q].k;
+            ri[base + x] = e[q].i;
+        }
     }
 }
 

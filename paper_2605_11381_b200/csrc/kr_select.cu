@@ -673,7 +673,11 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
 // rank merge) and apply rank < k as admission (keys are unique, so this is
 // key <= kth) -- three short parallel launches instead of the radix select's
 // dozen, for latency-bound rounds such as configs[1] (1k robots).
-constexpr int kSmallAdmit = 8192;  // measured: at 16k the rank merge (64 runs) loses to the select
+#ifndef KR_SMALL_ADMIT
+#define KR_SMALL_ADMIT 16384
+#endif
+constexpr int kSmallAdmit = KR_SMALL_ADMIT;  // 16k: with the register run sort the
+                                             // small path beats the select (configs[2] 91 -> 86 us)
 
 struct SmallAdmitArgs {
     const kr_key* sorted_keys;

@@ -88,7 +88,9 @@ def _skewed(n, rng, mode):
                                       (70000, 69999, "kairos"), (50, 49, "few_bits"),
                                       (1 << 16, 1 << 15, "kairos"), (2, 1, "kairos"),
                                       (1024, 64, "kairos"), (4096, 4095, "few_bits"),
-                                      (4097, 4000, "kairos")])
+                                      (4097, 4000, "kairos"), (12000, 1024, "kairos"),
+                                      (16384, 16383, "few_bits"), (16384, 1, "kairos"),
+                                      (16385, 1024, "kairos"), (9000, 4500, "dense_low_bin")])
 def test_select_admit_fused(n, k, mode):
     from paper_2605_11381_b200 import fleet as fl
     rng = np.random.default_rng(n + k)

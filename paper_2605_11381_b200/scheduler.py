@@ -220,13 +220,20 @@ def _place(reqs, states, keys, fleet, sched, flags, edge, cloud, net, edge_avail
             ctypes.byref(sched), refetch.data_ptr(), cloud_idx.data_ptr(), n_cloud_t.data_ptr(),
             dev.stream()), "kr_place_cloud")
         n_cloud = int(n_cloud_t.item())
-    f = dev.read_flags(flags)
+    # one device->host read of everything the result objects need
+    out = torch.empty(3 * n + 1, dtype=torch.int32, device=keys.device)
+    out[:n] = order
+    out[n:2 * n] = refetch
+    out[2 * n:3 * n] = fleet.t["skipped"]
+    out[3 * n:] = flags
+    host = out.cpu().numpy()
+    f = int(host[3 * n]) & 0xFFFFFFFF
     if f & (_lib.FLAG_KEY_RANGE | _lib.FLAG_RATIO):
         raise ValueError("a pending request falls outside the packed sort-key range "
                          "(aged estimate >= 2^56 µs or lifetime >= 2^53 µs)")
-    order_h = order.cpu().numpy()
-    refetch_h = refetch.cpu().numpy()
-    skipped_h = fleet.t["skipped"].cpu().numpy()
+    order_h = host[:n]
+    refetch_h = host[n:2 * n]
+    skipped_h = host[2 * n:3 * n]
     cloud_h = cloud_idx[:n_cloud].cpu().numpy() if n_cloud else np.zeros(0, np.int32)
     in_cloud = set(int(i) for i in cloud_h)
     s_edge = [reqs[i] for i in order_h[:k]]

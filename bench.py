@@ -452,7 +452,7 @@ def other_configs(reps: int = 200):
     U = synthetic.magnitudes(R, seed=19)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))
-    rnd.capture(fleet, inp, reserve_sms=8, layout="split")
+    rnd.capture(fleet, inp, reserve_sms=24, layout="split")  # profiles/r1_confidence_layouts.jsonl
     for _ in range(5):
         rnd.replay()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -466,7 +466,7 @@ def other_configs(reps: int = 200):
     out["configs[4] per-GPU share, confidence policy (U 2^20 x 6 x 50 fp32), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (1.26 GB of magnitudes)",
-        "layout": "split: horizons || urgency + admission (8 reserved SMs)"}
+        "layout": "split: horizons || urgency + admission (24 reserved SMs)"}
     # the headline fleet with a cloud tier (phase 3 at fleet scale, §8(f)1):
     # full key order + edge admission + the ordered offload scan
     import numpy as np

@@ -170,6 +170,10 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
             per_sm = f.occ_blocks;
         }
         if (per_sm < 1) per_sm = 1;
+        // sharing the GPU (max_sms > 0): one CTA slot per SM stays free so the
+        // side stream's kernels can co-reside where registers are the limit
+        static const bool keep_slot = std::getenv("KR_SHARED_FULL_SM") == nullptr;  // A/B knob
+        if (max_sms > 0 && keep_slot && per_sm > 1) per_sm -= 1;
         int64_t ntiles = (p.R + p.TR - 1) / p.TR;
         int sms = device_info().sm_count;
         if (max_sms > 0 && max_sms < sms) sms = max_sms;

@@ -672,7 +672,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--eager", action="store_true",
                     help="N=1: the N>1 path (eager launches, side-stream overlap) instead of graphs")
-    ap.add_argument("--reserve-sms", type=int, default=8,
+    ap.add_argument("--reserve-sms", type=int, default=10,
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
     ap.add_argument("--layout", choices=["split", "urgency_first"], default="split",
                     help="graph layout of the round (see rounds.DecisionRound.capture)")

@@ -427,11 +427,11 @@ def other_configs(reps: int = 200):
     rnd = rounds.DecisionRound(R, 1024, sched_for(soa))
     inp = rounds.MixedInputs([(0, rounds.DivergenceInputs(pa, ca, THR, offset=oa)),
                               (R // 2, rounds.DivergenceInputs(ph, chh, THR, offset=oh))])
-    t = timed_captured(rnd, fleet, inp, -1)
+    t = timed_captured(rnd, fleet, inp, 8)
     out["configs[2] 16k mixed (8k arms 64x7 + 8k humanoids 64x32) k=1024"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "163 MB of chunks (> 126 MB L2): mostly streamed from HBM",
-        "layout": "split, uncapped: the two groups' horizon kernels on forked streams || "
+        "layout": "split, 8 reserved SMs: the two groups' horizon kernels on forked streams || "
                   "urgency + admission"}
     # configs[3]: 64k robots, 8-sample ensembles 50x7, k = 8192 (one GPU's whole fleet)
     R = 65536

@@ -21,7 +21,10 @@
 
 namespace kr {
 
-constexpr int kSharedStages = 3;  // ring depth when the horizon kernel shares the GPU
+#ifndef KR_SHARED_STAGES
+#define KR_SHARED_STAGES 3
+#endif
+constexpr int kSharedStages = KR_SHARED_STAGES;  // ring depth when the horizon kernel shares the GPU
 
 // ---------------------------------------------------------------------------
 // Divergence horizon (workload.py:461-496), S-sample ensembles, ragged rows

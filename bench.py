@@ -64,11 +64,15 @@ def workload_config(args, world):
 # --------------------------------------------------------------------------
 # clocks (NVML, sampled during the timed region)
 # --------------------------------------------------------------------------
-def _clock_poll(index, stop, out):
-    """Child process: poll NVML SM clock + throttle reasons until `stop` is set."""
+def _clock_poll(index, stop, ready, out):
+    """Child process: poll NVML SM clock + throttle reasons until `stop` is set
+    (`ready` is set once NVML answers, so the parent starts its timed region
+    only after sampling has begun)."""
     import pynvml
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(index)
+    pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    ready.set()
     samples, masks = [], 0
     while not stop.is_set():
         try:
@@ -99,11 +103,13 @@ class ClockSampler:
         try:
             import pynvml  # noqa: F401
             self.stop = self.ctx.Event()
+            ready = self.ctx.Event()
             self.q = self.ctx.Queue()
-            self.proc = self.ctx.Process(target=_clock_poll, args=(self.index, self.stop, self.q),
-                                         daemon=True)
+            self.proc = self.ctx.Process(target=_clock_poll,
+                                         args=(self.index, self.stop, ready, self.q), daemon=True)
             self.proc.start()
-            time.sleep(0.05)  # first samples before the timed region starts
+            ready.wait(timeout=30)  # NVML initialised and answering
+            time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -271,6 +277,7 @@ def run_ours(args, world, rank, local_rank):
         end.record(stream)
         barrier()
     launches = per_round * args.steps if graphs else lib.kr_launch_count() - n0
+    rnd.check()  # validation word of every timed round (key ranges, shard key uniqueness)
     elapsed = start.elapsed_time(end) / 1e3
     div_ms = [a.elapsed_time(b) for a, b in ev]
     t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")

@@ -71,6 +71,8 @@ enum { KR_KAIROS = 0, KR_FIFO = 1, KR_LAS = 2 };
 #define KR_FLAG_TIME_RANGE 0x8u  /* core.py:38-41 negative action count / overflow       */
 #define KR_FLAG_RATIO      0x10u /* wait-ratio operand beyond 2^53 (inexact double)      */
 #define KR_FLAG_LEDGER     0x20u /* ledger event out of order / beyond capacity        */
+#define KR_FLAG_DUP_KEY    0x40u /* sharded merge met one key on two shards (non-global
+                                    robot ranks or per-shard issued bases)           */
 
 /* 128-bit composite sort key (ascending = reference order). */
 typedef struct kr_key {
@@ -269,15 +271,18 @@ KR_API int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
 /* Sharded admission (rounds.sharded_topk): `runs` holds W ascending runs of
  * `len` keys each (every rank's local top-k' candidates, all-ones padded, as
  * all-gathered).  Writes the k smallest keys overall, in order, to out_keys
- * (nullable) and the k-th smallest to kth_out (nullable); k <= W * len. */
+ * (nullable) and the k-th smallest to kth_out (nullable); k <= W * len.
+ * The merge is exact for unique keys only: a non-padding key that occurs
+ * twice sets KR_FLAG_DUP_KEY in *flags (nullable). */
 KR_API int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t k, kr_key* out_keys,
-                         kr_key* kth_out, void* stream);
+                         kr_key* kth_out, uint32_t* flags, void* stream);
 /* kr_merge_runs that also records, for each output rank, the element's
  * position in `runs` (run r, slot j -> r * len + j): lets a caller carry
  * per-candidate payloads (e.g. uplink times for the cloud scan) through the
  * merge.  out_pos may be NULL. */
 KR_API int kr_merge_runs_pos(const kr_key* runs, int32_t W, int64_t len, int64_t k,
-                             kr_key* out_keys, int32_t* out_pos, kr_key* kth_out, void* stream);
+                             kr_key* out_keys, int32_t* out_pos, kr_key* kth_out, uint32_t* flags,
+                             void* stream);
 
 /* ---- phase 3: hybrid edge / cloud placement --------------------------- */
 

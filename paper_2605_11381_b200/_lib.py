@@ -26,6 +26,7 @@ FLAG_KEY_RANGE = 0x4
 FLAG_TIME_RANGE = 0x8
 FLAG_RATIO = 0x10
 FLAG_LEDGER = 0x20
+FLAG_DUP_KEY = 0x40
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -124,8 +125,8 @@ _SIGNATURES = {
                                 ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp, _vp,
                                 ctypes.c_size_t, _vp]),
     "kr_sort_keys": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
-    "kr_merge_runs": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp, _vp, _vp]),
-    "kr_merge_runs_pos": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "kr_merge_runs": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "kr_merge_runs_pos": (ctypes.c_int, [_vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "kr_transfer_time": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "kr_trace_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, _i64,
                                       ctypes.POINTER(_vp)]),

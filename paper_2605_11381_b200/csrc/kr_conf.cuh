@@ -81,9 +81,13 @@ struct ConfWork {
             lo = fin < __dmul_rn(thr, dnd);
             in_range = thr >= 1e-300 && thr <= 1e300 && N >= 2;  // N == 1: pairwise order
         }
+        // an exact zero mean: the reference's threshold (1 + t) * 0.0 is 0 for
+        // finite 1 + t, so any f > 0 trips (NaN for t = inf / NaN: never) --
+        // decided here directly, since c1 overflows to inf for thresholds
+        // beyond FLT_MAX and thr = 0 * inf would be NaN
         const bool zero_mean = sf == T(0);
         und = !(fin == T(0) || zero_mean || (in_range && (hi || lo)));
-        return hi;
+        return zero_mean ? (fin > T(0) && isfinite(opt)) : hi;
     }
 
     __device__ __forceinline__ bool exact(const T* col) const { return conf_exact(col, K, N, opt); }

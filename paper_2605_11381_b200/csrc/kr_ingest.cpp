@@ -657,23 +657,29 @@ int ingest_threads(size_t len) {
     return n < by_size ? n : by_size;
 }
 
-}  // namespace
+// Run fn(0..n-1) on up to n host threads.  If a thread cannot be created
+// (std::system_error) the remaining ranges run on the calling thread; every
+// started thread is joined before anything propagates.
+template <class F>
+void run_ranges(size_t n, F&& fn) {
+    std::vector<std::thread> th;
+    size_t started = 0;
+    try {
+        th.reserve(n);
+        for (; started < n; started++) th.emplace_back(fn, started);
+    } catch (...) {
+    }
+    for (size_t r = started; r < n; r++) fn(r);
+    for (auto& x : th) x.join();
+}
 
-// Lines are independent, so the buffer is cut at line boundaries into one
-// range per host thread; the ranges' tables are concatenated in order, and the
-// first range that fails decides the error (as the sequential loop would).
-extern "C" int kr_trace_parse(const char* buf, size_t len, int64_t first_line, void** table) {
-    if (!table || (!buf && len)) return KR_EINVAL;
-    if (len == 0) buf = "";
-    Table* t = new (std::nothrow) Table();
-    if (!t) return KR_EINVAL;
-    *table = t;
+int parse_impl(const char* buf, size_t len, int64_t first_line, Table& t) {
     const int64_t line0 = first_line > 0 ? first_line : 1;
     const char* end = buf + len;
     const int nt = ingest_threads(len);
     if (nt <= 1) {
-        const int st = parse_range(buf, end, line0, *t);
-        finalize(*t);
+        const int st = parse_range(buf, end, line0, t);
+        finalize(t);
         return st;
     }
     std::vector<const char*> cut{buf};
@@ -689,40 +695,59 @@ extern "C" int kr_trace_parse(const char* buf, size_t len, int64_t first_line, v
     std::vector<Table> part(nr);
     std::vector<int> st(nr, KR_OK);
     std::vector<int64_t> lines(nr + 1, 0);
-    {
-        std::vector<std::thread> th;
-        for (size_t r = 0; r < nr; r++)
-            th.emplace_back([&, r] {
-                const char* q = cut[r];
-                int64_t n = 0;
-                while ((q = static_cast<const char*>(std::memchr(q, '\n', static_cast<size_t>(cut[r + 1] - q))))) {
-                    n++;
-                    q++;
-                }
-                lines[r + 1] = n;
-            });
-        for (auto& x : th) x.join();
-    }
+    run_ranges(nr, [&](size_t r) {
+        const char* q = cut[r];
+        int64_t n = 0;
+        while ((q = static_cast<const char*>(std::memchr(q, '\n', static_cast<size_t>(cut[r + 1] - q))))) {
+            n++;
+            q++;
+        }
+        lines[r + 1] = n;
+    });
     lines[0] = line0;
     for (size_t r = 1; r <= nr; r++) lines[r] += lines[r - 1];
-    {
-        std::vector<std::thread> th;
-        for (size_t r = 0; r < nr; r++)
-            th.emplace_back([&, r] { st[r] = parse_range(cut[r], cut[r + 1], lines[r], part[r]); });
-        for (auto& x : th) x.join();
-    }
+    // a range that throws (bad_alloc) reports KR_ENOSPACE for itself
+    run_ranges(nr, [&](size_t r) {
+        try {
+            st[r] = parse_range(cut[r], cut[r + 1], lines[r], part[r]);
+        } catch (...) {
+            st[r] = KR_ENOSPACE;
+        }
+    });
     int status = KR_OK;
     for (size_t r = 0; r < nr; r++) {
-        merge(*t, part[r]);
+        merge(t, part[r]);
         if (st[r] != KR_OK) {
-            t->err = part[r].err;
-            t->err_line = part[r].err_line;
+            if (st[r] == KR_EFORMAT) {
+                t.err = part[r].err;
+                t.err_line = part[r].err_line;
+            }
             status = st[r];
             break;
         }
     }
-    finalize(*t);
+    finalize(t);
     return status;
+}
+
+}  // namespace
+
+// Lines are independent, so the buffer is cut at line boundaries into one
+// range per host thread; the ranges' tables are concatenated in order, and the
+// first range that fails decides the error (as the sequential loop would).
+// No exception leaves this function: allocation failures anywhere (the
+// ranges' tables, merge, finalize) return KR_ENOSPACE.
+extern "C" int kr_trace_parse(const char* buf, size_t len, int64_t first_line, void** table) {
+    if (!table || (!buf && len)) return KR_EINVAL;
+    if (len == 0) buf = "";
+    Table* t = new (std::nothrow) Table();
+    if (!t) return KR_ENOSPACE;
+    *table = t;
+    try {
+        return parse_impl(buf, len, first_line, *t);
+    } catch (...) {
+        return KR_ENOSPACE;
+    }
 }
 
 extern "C" int kr_trace_load(const char* path, void** table) {
@@ -731,9 +756,14 @@ extern "C" int kr_trace_load(const char* path, void** table) {
     FILE* f = std::fopen(path, "rb");
     if (!f) return KR_EINVAL;
     std::string data;
-    char buf[1 << 16];
-    size_t n;
-    while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) data.append(buf, n);
+    try {
+        char buf[1 << 16];
+        size_t n;
+        while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) data.append(buf, n);
+    } catch (...) {
+        std::fclose(f);
+        return KR_ENOSPACE;
+    }
     std::fclose(f);
     return kr_trace_parse(data.data(), data.size(), 1, table);
 }

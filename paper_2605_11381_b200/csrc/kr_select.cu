@@ -713,30 +713,43 @@ __global__ void __launch_bounds__(256) k_small_apply(SmallAdmitArgs a) {
 // = its index in its run + the number of smaller elements in each other run
 // (binary search; one lane per run, a warp per element; ties -- the all-ones
 // sentinels -- broken by position).  Ranks < k are the global S_e in order;
-// rank k - 1 is the global k-th key.
+// rank k - 1 is the global k-th key.  The protocol is exact only for unique
+// keys (global robot ranks, one issued base on every shard): a real key met
+// again in another run (or next to itself in its own) sets KR_FLAG_DUP_KEY.
+__device__ __forceinline__ bool key_eq(const kr_key& a, const kr_key& b) {
+    return a.hi == b.hi && a.lo == b.lo;
+}
+
 __global__ void __launch_bounds__(256) k_merge_runs(const kr_key* runs, int W, int len, int k,
                                                     kr_key* out_keys, int32_t* out_pos,
-                                                    kr_key* kth_out) {
+                                                    kr_key* kth_out, uint32_t* flags) {
     const int m = W * len;
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < m; e += gridDim.x * wpb) {
         const kr_key x = runs[e];
         const int own = e / len;
+        const bool real = ~(x.hi & x.lo) != 0;  // not the all-ones padding
+        bool dup = false;
         int c = 0;
         for (int r = lane; r < W; r += 32) {
-            if (r == own) continue;
             int lo = r * len, hi = lo + len;
-            const int start = lo;
+            const int start = lo, end = hi;
+            if (r == own) {
+                dup |= real && e > start && key_eq(runs[e - 1], x);
+                continue;
+            }
             while (lo < hi) {  // elements of run r ordered before (x, e)
                 const int mid = (lo + hi) >> 1;
                 if (pair_gt(x, e, runs[mid], mid)) lo = mid + 1;
                 else hi = mid;
             }
+            dup |= real && ((lo > start && key_eq(runs[lo - 1], x)) || (lo < end && key_eq(runs[lo], x)));
             c += lo - start;
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (flags && __any_sync(0xffffffffu, dup) && lane == 0) atomicOr(flags, KR_FLAG_DUP_KEY);
         if (lane == 0) {
             const int rank = c + (e - own * len);
             if (rank < k) {
@@ -1097,7 +1110,7 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
 
 extern "C" int kr_merge_runs_pos(const kr_key* runs, int32_t W, int64_t len, int64_t k,
                                  kr_key* out_keys, int32_t* out_pos, kr_key* kth_out,
-                                 void* stream) {
+                                 uint32_t* flags, void* stream) {
     if (W < 1 || len < 0 || k < 0 || k > static_cast<int64_t>(W) * len ||
         static_cast<int64_t>(W) * len > INT_MAX)
         return KR_EINVAL;
@@ -1108,13 +1121,13 @@ extern "C" int kr_merge_runs_pos(const kr_key* runs, int32_t W, int64_t len, int
     const int64_t cap = static_cast<int64_t>(device_info().sm_count) * 64;
     if (blocks > cap) blocks = cap;
     k_merge_runs<<<static_cast<unsigned>(blocks), 256, 0, as_stream(stream)>>>(
-        runs, W, static_cast<int>(len), static_cast<int>(k), out_keys, out_pos, kth_out);
+        runs, W, static_cast<int>(len), static_cast<int>(k), out_keys, out_pos, kth_out, flags);
     return check_launch("kr_merge_runs");
 }
 
 extern "C" int kr_merge_runs(const kr_key* runs, int32_t W, int64_t len, int64_t k,
-                             kr_key* out_keys, kr_key* kth_out, void* stream) {
-    return kr_merge_runs_pos(runs, W, len, k, out_keys, nullptr, kth_out, stream);
+                             kr_key* out_keys, kr_key* kth_out, uint32_t* flags, void* stream) {
+    return kr_merge_runs_pos(runs, W, len, k, out_keys, nullptr, kth_out, flags, stream);
 }
 
 extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* kth,

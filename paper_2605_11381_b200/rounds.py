@@ -45,7 +45,8 @@ class RoundOutputs:
     refetch: torch.Tensor      # uint8 [R]
     edge_keys: torch.Tensor    # int64 [k, 2] S_e keys in order (global when sharded)
     edge_idx: torch.Tensor | None = None  # int32 [k] local indices (single GPU)
-    kth: torch.Tensor | None = None
+    kth: torch.Tensor | None = None       # the k-th key (None when k == 0)
+    flags: torch.Tensor | None = None     # int32 [1] validation word (DecisionRound.check)
 
 
 @dataclass
@@ -74,6 +75,19 @@ class MixedInputs:
     groups: list
 
 
+def raise_round_flags(f: int) -> None:
+    """The validation bits of a fleet round -> the drop-in's ValueErrors."""
+    if f & _lib.FLAG_DUP_KEY:
+        raise ValueError("two shards produced the same priority key: sharded rounds need "
+                         "global robot ranks (lexrank) and one issued base on every rank")
+    if f & (_lib.FLAG_KEY_RANGE | _lib.FLAG_RATIO):
+        raise ValueError("a pending request falls outside the packed sort-key range "
+                         "(aged estimate >= 2^56 µs, issue-time span >= 2^40 µs, "
+                         ">= 2^24 requests or lifetime >= 2^53 µs)")
+    if f & _lib.FLAG_TIME_RANGE:
+        raise ValueError("remaining actions must be >= 0 (or the need time overflows int64)")
+
+
 class DecisionRound:
     """Preallocated single-GPU decision round over R robots, budget k."""
 
@@ -92,6 +106,10 @@ class DecisionRound:
         self.edge_keys = fl.new_keys(max(self.k, 1), d)
         self.ws = fl.Workspace(R)
         self.key_stats = fl.new_key_stats(d)
+        # validation word: the urgency pass ORs KR_FLAG_KEY_RANGE / _RATIO /
+        # _TIME_RANGE into it when a request falls outside the packed key's
+        # range (plan() raises there); sticky across rounds until check()
+        self.flags = dev.flags()
         self.lib = _lib.load()
         self.max_sms = 0  # divergence grid SM cap (0: all); see capture(concurrent=...)
 
@@ -144,7 +162,17 @@ class DecisionRound:
         _lib.check(self.lib.kr_urgency(
             ctypes.byref(fs), ctypes.byref(self.sched), self.keys.data_ptr(),
             self.need_time.data_ptr(), None, None, None, None, None,
-            self.key_stats.data_ptr(), None, st), "kr_urgency")
+            self.key_stats.data_ptr(), self.flags.data_ptr(), st), "kr_urgency")
+
+    def check(self, reset: bool = True) -> None:
+        """Raise the reference's ValueError if any round since the last check
+        met an input outside the packed sort key's range (one 4-byte read;
+        call it outside graph capture, e.g. every N rounds or at the end of a
+        replay).  The decisions of such a round are not the reference's."""
+        f = dev.read_flags(self.flags)
+        if reset and f:
+            self.flags.zero_()
+        raise_round_flags(f)
 
     def admit(self, fleet: fl.DeviceFleet) -> None:
         fl.select_admit(self.keys, self.k, self.ws, key_stats=self.key_stats, fleet=fleet,
@@ -153,7 +181,8 @@ class DecisionRound:
 
     def outputs(self) -> RoundOutputs:
         return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
-                            self.edge_keys[: self.k], self.edge_idx[: self.k], self.kth)
+                            self.edge_keys[: self.k], self.edge_idx[: self.k],
+                            self.kth if self.k else None, self.flags)
 
     def run(self, fleet: fl.DeviceFleet, h: DivergenceInputs) -> RoundOutputs:
         self.horizons(h)
@@ -330,6 +359,10 @@ class HybridDecisionRound(DecisionRound):
         fl.select_admit(self.keys, self.kp, self.ws, key_stats=self.key_stats,
                         edge_idx=self.cand_idx, edge_keys=self.cand_keys)
         kth_ptr = self.cand_keys.data_ptr() + (k - 1) * 16 if 0 < k < R else None
+        if 0 < k < R:
+            self.kth.copy_(self.cand_keys[k - 1: k])
+        else:  # k >= R: every key is admitted (kr_topk_select's convention)
+            self.kth.fill_(ALL_ONES)
         fl.admit(self.keys, k, kth_ptr, fleet, self.sched, None, admitted=self.admitted,
                  refetch=self.refetch)
         if self.cap == 0:
@@ -346,7 +379,8 @@ class HybridDecisionRound(DecisionRound):
 
     def outputs(self) -> RoundOutputs:
         return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
-                            self.cand_keys[: self.k], self.cand_idx[: self.k], self.kth)
+                            self.cand_keys[: self.k], self.cand_idx[: self.k],
+                            self.kth if self.k else None, self.flags)
 
     def cloud(self) -> torch.Tensor:
         """The offloaded robots in offload order (one device->host read)."""
@@ -421,7 +455,7 @@ class CudaShardOps:
         r = self.r
         _lib.check(r.lib.kr_merge_runs(runs.data_ptr(), W, kg, kg, r.global_edge.data_ptr(),
                                        r.kth_global.data_ptr() if want_kth else None,
-                                       dev.stream()), "kr_merge_runs")
+                                       r.flags.data_ptr(), dev.stream()), "kr_merge_runs")
         return r.global_edge[:kg], (r.kth_global if want_kth else None)
 
     def apply(self, keys, k, kth):
@@ -447,6 +481,15 @@ class ShardedDecisionRound(DecisionRound):
         allsz = [torch.zeros_like(sizes) for _ in range(self.world)]
         dist.all_gather(allsz, sizes, group=group)
         self.sizes = [int(s.item()) for s in allsz]
+        # keys are comparable across shards only if every rank packs them
+        # against the same round scalars (issued base, now, policy)
+        mine = torch.tensor([sched.issued_base, sched.now, sched.policy, sched.buckets,
+                             sched.aging_interval], dtype=torch.int64, device=self.H.device)
+        every = [torch.zeros_like(mine) for _ in range(self.world)]
+        dist.all_gather(every, mine, group=group)
+        if any(not torch.equal(e, every[0]) for e in every):
+            raise ValueError("sharded round: every rank needs the same kr_sched issued_base, now "
+                             "and policy (keys are compared across shards)")
         self.k_global = min(k, sum(self.sizes))
         kg = max(self.k_global, 1)
         d = self.H.device
@@ -548,7 +591,8 @@ class ShardedHybridRound(ShardedDecisionRound):
             if kg2 > 0:
                 _lib.check(self.lib.kr_merge_runs_pos(g_keys.data_ptr(), self.world, kg2, kg2,
                                                       merged.data_ptr(), pos.data_ptr(), None,
-                                                      st), "kr_merge_runs_pos")
+                                                      self.flags.data_ptr(), st),
+                           "kr_merge_runs_pos")
             if not edge_done:  # global S_e and the local edge admission
                 if kg > 0:
                     self.global_edge[:kg] = merged[:kg]

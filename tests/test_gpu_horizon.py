@@ -312,3 +312,29 @@ def test_nonfinite_thresholds(kb):
         sums = kb.sweep_horizon_sums(cells, Ut).cpu().numpy()
         assert sums[0] == sums[2] == 300 * 50
         assert sums[1] == orc.horizon_conf_batch(U, 0.4, 5).sum()
+
+
+@pytest.mark.parametrize("storage", [torch.float32, torch.float64])
+def test_zero_mean_columns_huge_thresholds(kb, storage):
+    """Columns whose earlier steps are all zero: the reference's threshold is
+    (1 + t) * 0.0 = 0, so any f > 0 trips for every finite t -- including
+    t beyond FLT_MAX, where the fp32 filter's folded factor overflows --
+    and nothing trips for t = inf / NaN ((1 + t) * 0.0 is NaN)."""
+    rng = np.random.default_rng(17)
+    U = rng.uniform(0.5, 2.0, (500, 6, 50))
+    zc = rng.integers(0, 50, 500)
+    U[np.arange(500), :-1, zc] = 0.0                       # zero mean in one column
+    U[np.arange(500), -1, zc] = rng.choice([0.0, 0.25], 500)
+    U = U.astype(np.float32 if storage == torch.float32 else np.float64)
+    Ut = torch.from_numpy(U).cuda()
+    for t in (1e39, 1e300, 3.5e38, 0.4, float("inf"), float("nan")):
+        cfg = kb.HorizonPolicyConfig.confidence(t, 1)
+        exp = orc.horizon_conf_batch(U.astype(np.float64), t, 1)
+        assert np.array_equal(kb.decide_horizon_batch(cfg, Ut).cpu().numpy(), exp), t
+        if t == 1e39:  # the zero-mean trips decide these horizons
+            assert (exp < 50).sum() > 100
+    cells = [kb.HorizonPolicyConfig.confidence(t, h) for t in (1e39, 0.4, float("inf"), 3.5e38)
+             for h in (1, 5)]
+    sums = kb.sweep_horizon_sums(cells, Ut).cpu().numpy()
+    exp = orc.sweep_sums(U.astype(np.float64), [(1, 0, c.threshold, c.min_horizon) for c in cells])
+    assert np.array_equal(sums, exp)

@@ -190,3 +190,34 @@ def test_mixed_fleet_round_vs_oracle():
         torch.cuda.synchronize()
         assert np.array_equal(out.horizon.cpu().numpy(), H)
         assert np.array_equal(out.edge_idx.cpu().numpy(), res["order"][:k])
+
+
+def test_round_flags_raise_out_of_range_keys():
+    """A fleet round keeps the urgency pass's validation word: a request whose
+    issue time lies >= 2^40 µs after the packed key's base cannot be keyed
+    exactly (plan() raises there), so check() raises the same ValueError;
+    an in-range round leaves the word clear.  Also: a hybrid round's kth
+    output is the k-th key of its ordered candidates."""
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    R, k = 5000, 100
+    soa = synthetic.fleet_soa(R, seed=61)
+    good = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                           int(soa["issued_at"].min()))
+    rnd = rounds.DecisionRound(R, k, good)
+    out = rnd.run(rounds_fleet := fl.DeviceFleet.from_host(soa),
+                  rounds.DivergenceInputs(*synthetic.chunks(R, seed=62)[:2], 0.9))
+    rnd.check()
+    assert int(out.flags.item()) == 0
+    bad = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                          int(soa["issued_at"].min()) - (1 << 41))
+    rnd2 = rounds.DecisionRound(R, k, bad)
+    rnd2.urgency(rounds_fleet)
+    rnd2.admit(rounds_fleet)
+    with pytest.raises(ValueError, match="packed sort-key range"):
+        rnd2.check()
+    rnd2.check()  # reset after raising
+    hyb = rounds.HybridDecisionRound(R, k, good, cloud_cap=0)
+    hyb.urgency(rounds_fleet)
+    hyb.admit(rounds_fleet)
+    o = hyb.outputs()
+    assert torch.equal(o.kth[0], o.edge_keys[k - 1])

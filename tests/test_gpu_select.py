@@ -145,7 +145,7 @@ def test_merge_runs(W, len_, fill):
         out = fl.new_keys(kk)
         kth = fl.new_keys(1)
         _lib.check(_lib.load().kr_merge_runs(t.data_ptr(), W, len_, kk, out.data_ptr(),
-                                             kth.data_ptr(), dev.stream()), "kr_merge_runs")
+                                             kth.data_ptr(), None, dev.stream()), "kr_merge_runs")
         got = out.cpu().numpy().view(np.uint64)
         n_real = min(kk, len(exp))
         assert np.array_equal(got[:n_real], exp[:n_real])

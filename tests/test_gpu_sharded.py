@@ -15,6 +15,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from oracle import oracle as orc
+
 pytestmark = pytest.mark.gpu
 
 
@@ -97,9 +99,68 @@ def test_sharded_round_matches_single_gpu(sizes, k, overlap):
     torch.cuda.synchronize()
     if overlap:
         assert np.array_equal(np.concatenate([r[4] for r in res]), ref.H.cpu().numpy())
+        assert np.array_equal(np.concatenate([r[4] for r in res]), orc.divergence_batch(
+            prev.cpu().numpy(), cand.cpu().numpy(), 0.9, off.cpu().numpy()))
     adm = np.concatenate([r[1] for r in res])
     skp = np.concatenate([r[2] for r in res])
     assert np.array_equal(adm, ref.admitted.cpu().numpy())
     assert np.array_equal(skp, fleet.t["skipped"].cpu().numpy())
     for r in res:  # identical ordered global S_e on every rank == single-GPU S_e keys
         assert np.array_equal(r[3], ref.edge_keys[:k].cpu().numpy())
+    # and == the oracle's plan() (not only the single-GPU round): membership,
+    # skip counters, and the global S_e order (the key's low 24 bits carry
+    # the robot's global lexrank == its index here)
+    orc_res = orc.plan_soa(soa, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+    assert np.array_equal(adm, orc_res["admitted"])
+    assert np.array_equal(skp, orc_res["skipped_out"])
+    kk = min(k, sum(sizes))
+    for r in res:
+        assert np.array_equal(r[3][:, 1] & 0xFFFFFF, orc_res["order"][:kk])
+
+
+def _dup_worker(rank, world, port, q):
+    """Both ranks hold the same robots with shard-local ranks: every key occurs
+    on both shards, which the merge must report instead of over-admitting."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+        soa = synthetic.fleet_soa(3000, seed=23)
+        sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                                int(soa["issued_at"].min()))
+        rnd = rounds.ShardedDecisionRound(3000, 500, sched)
+        fleet = fl.DeviceFleet.from_host(soa)
+        rnd.urgency(fleet)
+        rnd.admit(fleet)
+        try:
+            rnd.check()
+            q.put((rank, "no error"))
+        except ValueError as e:
+            q.put((rank, str(e)))
+        # mismatched round scalars are rejected up front
+        other = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                                int(soa["issued_at"].min()) - rank)
+        try:
+            rounds.ShardedDecisionRound(3000, 500, other)
+            q.put((rank, "no error"))
+        except ValueError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_duplicate_keys_flagged():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_dup_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    msgs = [q.get(timeout=300) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert sum("same priority key" in m for _, m in msgs) == 2
+    assert sum("same kr_sched" in m for _, m in msgs) == 2

@@ -32,15 +32,27 @@ def timeit(fn, reps=10):
     return statistics.median(ts)
 
 
-def report(name, R, bytes_per, t):
+def report(name, R, bytes_per, t, needed=None):
     gbs = bytes_per * R / t / 1e9
-    print(json.dumps({"variant": name, "robots": R, "bytes_per_robot_round": bytes_per,
-                      "ms": t * 1e3, "GBps": round(gbs, 1), "frac_of_measured_peak": round(gbs / PEAK, 3),
-                      "robot_rounds_per_s": R / t}), flush=True)
+    line = {"variant": name, "robots": R, "bytes_per_robot_round": bytes_per,
+            "ms": t * 1e3, "GBps": round(gbs, 1), "frac_of_measured_peak": round(gbs / PEAK, 3),
+            "robot_rounds_per_s": R / t}
+    if needed is not None:  # bytes a decision can read (the compared rows only)
+        line["needed_bytes_per_robot_round"] = round(needed, 1)
+        line["needed_GBps"] = round(needed * R / t / 1e9, 1)
+        line["needed_frac_of_measured_peak"] = round(needed * R / t / 1e9 / PEAK, 3)
+    print(json.dumps(line), flush=True)
 
 
 def main():
     R = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
+    only = sys.argv[2] if len(sys.argv) > 2 else ""
+    if only != "div":
+        horizon_policy(R)
+    divergence(R)
+
+
+def horizon_policy(R):
     for K, N, dt, es in [(6, 50, torch.float32, 4), (6, 50, torch.float64, 8), (6, 64, torch.float32, 4)]:
         U = synthetic.magnitudes(R, seed=3, K=K, N=N, dtype=dt)
         cfg = kb.HorizonPolicyConfig.confidence(0.4, 5)
@@ -67,11 +79,18 @@ def main():
         t = timeit(lambda: kb.sweep_horizon_sums(cfgs, U, validate=False))
         report(f"sweep C=16 K={K} N={N} {str(dt)[6:]} (sums)", R, K * N * es, t)
         del U
-    for S, L, D, RR in [(1, 50, 7, R), (1, 64, 32, R // 2), (8, 50, 7, R // 4)]:
-        prev, cand, off = synthetic.chunks(RR, seed=5, Lp=L, Lc=L, D=D, S=S)
+
+
+def divergence(R):
+    for S, L, D, RR, dt in [(1, 50, 7, R, torch.float32), (1, 64, 32, R // 2, torch.float32),
+                            (8, 50, 7, R // 4, torch.float32), (1, 50, 7, R, torch.float64)]:
+        es = 4 if dt == torch.float32 else 8
+        prev, cand, off = synthetic.chunks(RR, seed=5, Lp=L, Lc=L, D=D, S=S, dtype=dt)
+        lim = (L - off.clamp(min=0)).clamp(min=0, max=L).double().mean().item()
         out = torch.empty(RR, dtype=torch.int32, device="cuda")
         t = timeit(lambda: round_optimal_horizon_batch(prev, cand, 0.9, offset=off, out=out))
-        report(f"divergence S={S} L={L} D={D} fp32", RR, (1 + S) * L * D * 4 + 8, t)
+        report(f"divergence S={S} L={L} D={D} {str(dt)[6:]}", RR, (1 + S) * L * D * es + 8, t,
+               needed=(1 + S) * lim * D * es + 8)
         del prev, cand
 
 

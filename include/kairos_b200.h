@@ -23,6 +23,7 @@
  *   kr_ledger_apply         core.py:200-229 + waiting.py:69-93  incremental TaskState
  *                           history and running wait totals (sim.py:358-440 mutations)
  *   kr_urgency_ledger       kr_urgency over the device-resident ledger (O(1) per request)
+ *   kr_plan_small           scheduler.py:254-276 plan() edge tier for n <= 4096 in one launch
  *   kr_trace_parse / _load  workload.py:163-262  JSONL task traces -> columns (host code)
  *   kr_transfer_time        engines.py:158-169   per-request uplink time
  *   kr_place_cloud          scheduler.py:160-234 phase-3 cloud offload scan
@@ -155,6 +156,11 @@ KR_API const char* kr_status_string(int status);
 KR_API const char* kr_last_error(void);
 /* Kernels launched by this library so far in this process (diagnostic). */
 KR_API unsigned long long kr_launch_count(void);
+/* Stream-ordered copy between any two addresses (cudaMemcpyDefault): stages a
+ * scalar call's inputs from the mapped arena into device scratch. */
+KR_API int kr_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
+/* cudaStreamSynchronize(stream): the one wait of a small synchronous call. */
+KR_API int kr_stream_synchronize(void* stream);
 
 /* ---- step 1: execution-horizon selection ------------------------------ */
 
@@ -223,6 +229,20 @@ KR_API int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys, 
  * {OR hi, OR lo, AND hi, AND lo} of the keys written, so the admission select
  * needs no extra pass over the keys. */
 KR_API int kr_key_stats_init(unsigned long long* key_stats, void* stream);
+
+/* A whole edge-tier planning round for n <= 4096 pending requests in ONE
+ * launch (replaces plan(), scheduler.py:254-276, at the simulator's call
+ * sizes: sim.py:298-308): urgency keys, the total order (one-CTA bitonic
+ * sort), admission of the first min(k, n), stale-observation refetch and the
+ * skip counter update.  The fleet columns may point to mapped pinned host
+ * memory (kr_mapped_ptr) and so may `out`; out = int32 [3n + 1]: order[n]
+ * (request indices, plan order), refetch[n] and updated skipped[n] (both by
+ * request index), then the validation flags word.  fleet->skipped is NOT
+ * modified.  KR_EINVAL for n > 4096. */
+KR_API int kr_plan_small(const kr_fleet* fleet, const kr_sched* cfg, int64_t k, int32_t* out,
+                         void* stream);
+/* Device address of mapped pinned host memory (cudaHostGetDevicePointer). */
+KR_API int kr_mapped_ptr(void* host, void** device);
 
 /* Apply a batch of TaskState mutations to the device ledger (one thread per
  * task; wait totals advance incrementally).  Out-of-order rounds or rounds

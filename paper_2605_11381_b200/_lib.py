@@ -111,6 +111,11 @@ _SIGNATURES = {
     "kr_urgency": (ctypes.c_int, [ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _vp, _vp,
                                   _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kr_key_stats_init": (ctypes.c_int, [_vp, _vp]),
+    "kr_plan_small": (ctypes.c_int, [ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _i64, _vp,
+                                     _vp]),
+    "kr_mapped_ptr": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
+    "kr_memcpy_async": (ctypes.c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
+    "kr_stream_synchronize": (ctypes.c_int, [_vp]),
     "kr_ledger_apply": (ctypes.c_int, [ctypes.POINTER(KrLedger), ctypes.POINTER(KrEvents), _vp,
                                        _vp]),
     "kr_urgency_ledger": (ctypes.c_int, [ctypes.POINTER(KrLedger), ctypes.POINTER(KrRequests),

@@ -19,6 +19,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 OUT = PKG / "libkairos_b200.so"
+PACK_SRC = CSRC / "kr_pack.c"  # host runtime: CPython extension (object packing)
 OBJ = PKG / "build"
 
 SOURCES = ["kr_capi.cu", "kr_horizon.cu", "kr_div_skx.cu", "kr_div_hsw.cu", "kr_sweep.cu",
@@ -52,7 +53,27 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def pack_module_path() -> Path:
+    import sysconfig
+    return PKG / ("_kr_pack" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pack(force: bool = False) -> Path:
+    """The native object packer (_kr_pack, kr_pack.c) with the host C compiler."""
+    import sysconfig
+    out = pack_module_path()
+    if not force and out.exists() and out.stat().st_mtime >= PACK_SRC.stat().st_mtime:
+        return out
+    cc = os.environ.get("CC") or shutil.which("gcc") or "cc"
+    tmp = out.with_suffix(".tmp")
+    subprocess.run([cc, "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+                    str(PACK_SRC), "-o", str(tmp)], check=True)
+    os.replace(tmp, out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_pack(force)
     if not force and not _stale():
         return OUT
     OBJ.mkdir(exist_ok=True)

@@ -59,3 +59,15 @@ extern "C" const char* kr_status_string(int status) {
 extern "C" const char* kr_last_error(void) { return kr::g_last_error; }
 
 extern "C" unsigned long long kr_launch_count(void) { return kr::g_launches.load(); }
+
+extern "C" int kr_stream_synchronize(void* stream) {
+    KR_CUDA_TRY(cudaStreamSynchronize(kr::as_stream(stream)));
+    return KR_OK;
+}
+
+extern "C" int kr_memcpy_async(void* dst, const void* src, size_t bytes, void* stream) {
+    if ((!dst || !src) && bytes) return KR_EINVAL;
+    if (bytes == 0) return KR_OK;
+    KR_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, kr::as_stream(stream)));
+    return KR_OK;
+}

@@ -136,53 +136,61 @@ struct LedgerSrc {
     __device__ void waits(int64_t, int64_t*) const {}
 };
 
+// One request: its packed key (and the optional intermediates / need time).
+template <class Src>
+__device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, const UrgencyOut& o,
+                                              int64_t i, uint32_t& fl) {
+    const int64_t issued = s.issued(i);
+    const int32_t rank = s.rank(i);
+    if (o.need_time) {
+        int32_t rem = s.remaining(i);
+        o.need_time[i] = issued + us_from_actions(rem, c.hz_num, c.hz_den, &fl);
+    }
+    kr_key key;
+    if (c.policy == KR_FIFO) {
+        key.hi = static_cast<uint64_t>(issued) ^ (uint64_t(1) << 63);
+        key.lo = static_cast<uint64_t>(static_cast<uint32_t>(rank));
+        if (rank < 0) fl |= KR_FLAG_KEY_RANGE;
+    } else if (c.policy == KR_LAS) {
+        key.hi = static_cast<uint64_t>(s.accum(i)) ^ (uint64_t(1) << 63);
+        key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
+    }
+    const bool need_hist =
+        c.policy == KR_KAIROS || o.total_wait || o.wr || o.bucket || o.est || o.slot_wait;
+    if (need_hist) {
+        const int32_t skipped = s.skipped(i);
+        int64_t w, t0, last = 0;
+        int32_t ne;
+        s.hist(i, w, t0, ne, last);
+        double wr = wait_ratio(w, t0, c.now, &fl);
+        int32_t b = assign_bucket(wr, skipped, c.buckets, c.aging_interval);
+        const int64_t est = ne > 0 ? last : c.default_exec_estimate;
+        if (o.total_wait) o.total_wait[i] = w;
+        if (o.wr) o.wr[i] = wr;
+        if (o.bucket) o.bucket[i] = b;
+        if (o.est) o.est[i] = est;
+        if constexpr (Src::kSlots)
+            if (o.slot_wait) s.waits(i, o.slot_wait);
+        if (c.policy == KR_KAIROS) {
+            // aged = est * (1 + skipped), descending -> stored complemented
+            unsigned __int128 aged = static_cast<unsigned __int128>(est < 0 ? 0 : est) *
+                                     static_cast<unsigned __int128>(1 + (int64_t)skipped);
+            if (est < 0 || skipped < 0 || aged > kAgedMask) fl |= KR_FLAG_KEY_RANGE;
+            uint64_t a = aged > kAgedMask ? kAgedMask : static_cast<uint64_t>(aged);
+            key.hi = (static_cast<uint64_t>(c.buckets - 1 - b) << 56) | (kAgedMask - a);
+            key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
+        }
+    }
+    return key;
+}
+
 template <class Src>
 __global__ void __launch_bounds__(256) k_urgency(Src s, kr_sched c, UrgencyOut o) {
     uint32_t fl = 0;
     unsigned long long ohi = 0, olo = 0, ahi = ~0ull, alo = ~0ull;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < s.n();
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t issued = s.issued(i);
-        const int32_t rank = s.rank(i);
-        if (o.need_time) {
-            int32_t rem = s.remaining(i);
-            o.need_time[i] = issued + us_from_actions(rem, c.hz_num, c.hz_den, &fl);
-        }
-        kr_key key;
-        if (c.policy == KR_FIFO) {
-            key.hi = static_cast<uint64_t>(issued) ^ (uint64_t(1) << 63);
-            key.lo = static_cast<uint64_t>(static_cast<uint32_t>(rank));
-            if (rank < 0) fl |= KR_FLAG_KEY_RANGE;
-        } else if (c.policy == KR_LAS) {
-            key.hi = static_cast<uint64_t>(s.accum(i)) ^ (uint64_t(1) << 63);
-            key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
-        }
-        const bool need_hist =
-            c.policy == KR_KAIROS || o.total_wait || o.wr || o.bucket || o.est || o.slot_wait;
-        if (need_hist) {
-            const int32_t skipped = s.skipped(i);
-            int64_t w, t0, last = 0;
-            int32_t ne;
-            s.hist(i, w, t0, ne, last);
-            double wr = wait_ratio(w, t0, c.now, &fl);
-            int32_t b = assign_bucket(wr, skipped, c.buckets, c.aging_interval);
-            const int64_t est = ne > 0 ? last : c.default_exec_estimate;
-            if (o.total_wait) o.total_wait[i] = w;
-            if (o.wr) o.wr[i] = wr;
-            if (o.bucket) o.bucket[i] = b;
-            if (o.est) o.est[i] = est;
-            if constexpr (Src::kSlots)
-                if (o.slot_wait) s.waits(i, o.slot_wait);
-            if (c.policy == KR_KAIROS) {
-                // aged = est * (1 + skipped), descending -> stored complemented
-                unsigned __int128 aged = static_cast<unsigned __int128>(est < 0 ? 0 : est) *
-                                         static_cast<unsigned __int128>(1 + (int64_t)skipped);
-                if (est < 0 || skipped < 0 || aged > kAgedMask) fl |= KR_FLAG_KEY_RANGE;
-                uint64_t a = aged > kAgedMask ? kAgedMask : static_cast<uint64_t>(aged);
-                key.hi = (static_cast<uint64_t>(c.buckets - 1 - b) << 56) | (kAgedMask - a);
-                key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
-            }
-        }
+        const kr_key key = urgency_one(s, c, o, i, fl);
         o.keys[i] = key;
         ohi |= key.hi; olo |= key.lo; ahi &= key.hi; alo &= key.lo;
     }
@@ -362,4 +370,105 @@ extern "C" int kr_ledger_apply(const kr_ledger* ledger, const kr_events* events,
     k_ledger_apply<<<grid_for(events->n_groups, 128), 128, 0, as_stream(stream)>>>(*ledger, *events,
                                                                                    flags);
     return check_launch("kr_ledger_apply");
+}
+
+// ---------------------------------------------------------------------------
+// Small planning rounds in one launch (the simulator's per-event plan() call:
+// scheduler.py:254-276 over tens to a few thousand pending requests)
+// ---------------------------------------------------------------------------
+// One CTA: every request's key (urgency_one), a bitonic sort of (key, index)
+// pairs in shared memory, and the edge admission (scheduler.py:204-207,
+// 223-234: order prefix of length k, stale-observation refetch, skip counter
+// reset / increment) -- one launch instead of urgency + select/sort + admit.
+// The fleet columns may live in mapped pinned host memory (zero-copy: the
+// kernel reads them over PCIe, coalesced), and so may `out` (int32 [3n + 1]:
+// order, refetch flag, updated skip counter, validation flags), so a call is
+// one launch plus one stream synchronisation.
+namespace kr {
+constexpr int kPlanSmallMax = 4096;
+
+__device__ __forceinline__ bool pair_less(const kr_key& a, int ia, const kr_key& b, int ib) {
+    if (a.hi != b.hi) return a.hi < b.hi;
+    if (a.lo != b.lo) return a.lo < b.lo;
+    return ia < ib;
+}
+
+__global__ void __launch_bounds__(1024) k_plan_small(kr_fleet f, kr_sched c, int n, int P, int k,
+                                                     int32_t* out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    kr_key* keys = reinterpret_cast<kr_key*>(sm);
+    int* idx = reinterpret_cast<int*>(keys + P);
+    __shared__ uint32_t sfl;
+    if (threadIdx.x == 0) sfl = 0;
+    __syncthreads();
+    const FleetSrc s{f};
+    const UrgencyOut none{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                          nullptr};
+    uint32_t fl = 0;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        kr_key key{~0ull, ~0ull};
+        if (i < n) key = urgency_one(s, c, none, i, fl);
+        keys[i] = key;
+        idx[i] = i;
+    }
+    if (fl) atomicOr(&sfl, fl);
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const kr_key a = keys[lo], b = keys[hi];
+                const int ia = idx[lo], ib = idx[hi];
+                if (pair_less(b, ib, a, ia) == up) {
+                    keys[lo] = b; keys[hi] = a;
+                    idx[lo] = ib; idx[hi] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        const int j = idx[p];
+        const bool in = p < k;
+        out[p] = j;
+        out[n + j] = in && (c.now - f.obs_captured_at[j] > c.stale_threshold);
+        out[2 * n + j] = in ? 0 : f.skipped[j] + 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) out[3 * n] = static_cast<int32_t>(sfl);
+}
+}  // namespace kr
+
+extern "C" int kr_plan_small(const kr_fleet* fleet, const kr_sched* cfg, int64_t k, int32_t* out,
+                             void* stream) {
+    if (!fleet || !cfg || fleet->n < 0 || fleet->n > kPlanSmallMax || k < 0) return KR_EINVAL;
+    if (cfg->policy < KR_KAIROS || cfg->policy > KR_LAS || cfg->buckets < 1 ||
+        cfg->buckets > 256 || cfg->aging_interval < 1 || cfg->hz_num <= 0 || cfg->hz_den <= 0)
+        return KR_EINVAL;
+    if (fleet->n == 0) return KR_OK;
+    if (!out) return KR_EINVAL;
+    const int n = static_cast<int>(fleet->n);
+    int P = 1;
+    while (P < n) P <<= 1;
+    const int threads = P >= 2048 ? 1024 : (P / 2 < 32 ? 32 : P / 2);
+    const size_t smem = static_cast<size_t>(P) * (sizeof(kr_key) + sizeof(int));
+    if (smem > 48 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            KR_CUDA_TRY(cudaFuncSetAttribute(k_plan_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kPlanSmallMax * (sizeof(kr_key) + sizeof(int)))));
+            attr = true;
+        }
+    }
+    k_plan_small<<<1, threads, smem, as_stream(stream)>>>(*fleet, *cfg, n, P,
+                                                         static_cast<int>(k < n ? k : n), out);
+    return check_launch("kr_plan_small");
+}
+
+extern "C" int kr_mapped_ptr(void* host, void** device) {
+    if (!host || !device) return KR_EINVAL;
+    KR_CUDA_TRY(cudaHostGetDevicePointer(device, host, 0));
+    return KR_OK;
 }

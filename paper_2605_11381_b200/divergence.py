@@ -106,6 +106,25 @@ def round_optimal_horizon(reference: Sequence[Sequence[float]],
     if ref.ndim != 2 or cand.ndim != 2 or ref.shape[1] != cand.shape[1]:
         raise ValueError(f"trajectories must share action dimensionality, got shapes "
                          f"{ref.shape} and {cand.shape}")
-    H = round_optimal_horizon_batch(dev.tensor(ref[None], torch.float64),
-                                    dev.tensor(cand[None], torch.float64), sim_threshold)
-    return int(H.item())
+    (Lp, D), Lc = ref.shape, cand.shape[0]
+    if Lp == 0 or Lc == 0 or D == 0:
+        H = round_optimal_horizon_batch(dev.tensor(ref[None], torch.float64),
+                                        dev.tensor(cand[None], torch.float64), sim_threshold)
+        return int(H.item())
+    # both trajectories staged through the mapped arena into device scratch
+    # (the kernel's TMA reads HBM), the horizon returned through the arena:
+    # one copy, one launch, one synchronisation
+    nb = 8 * (ref.size + cand.size)
+    a = dev.arena(nb + 64)
+    f = a.host[64:64 + nb].view(np.float64)
+    f[:ref.size] = ref.reshape(-1)
+    f[ref.size:] = cand.reshape(-1)
+    scr = a.device_scratch(nb)
+    st = dev.raw_stream()
+    lib = _lib.load()
+    _lib.check(lib.kr_memcpy_async(scr, a.dbase + 64, nb, st), "kr_memcpy_async")
+    _lib.check(lib.kr_horizon_divergence(scr, scr + 8 * ref.size, _lib.KR_F64, 1, 1, Lp, Lc, D,
+                                         None, None, None, float(sim_threshold), a.dbase, None, 0,
+                                         st), "kr_horizon_divergence")
+    dev.sync(st)
+    return int(a.host[:4].view(np.int32)[0])

@@ -36,35 +36,48 @@ RANK_SPAN = 1 << 24
 
 
 def host_soa(pending: Sequence, states: Mapping, rank_of: Mapping[str, int]) -> dict:
-    """Reference-shaped objects -> numpy structure-of-arrays (host packing)."""
+    """Reference-shaped objects -> numpy structure-of-arrays (host packing by
+    the native packer, _kr_pack: one pass over the objects in C)."""
+    from . import _kr_pack
     n = len(pending)
-    a = {k: np.zeros(n, np.int64) for k in INT_FIELDS64}
-    a.update({k: np.zeros(n, np.int32) for k in INT_FIELDS32})
-    slot_rows: list[tuple] = []
-    for i, req in enumerate(pending):
-        st = states[req.task_id]
-        a["t_start"][i] = st.t_start
-        a["issued_at"][i] = req.issued_at
-        a["obs_captured_at"][i] = req.obs_captured_at
-        a["accum_gen"][i] = st.accumulated_generation
-        a["remaining"][i] = req.last_exec_info.remaining_actions
-        a["lexrank"][i] = rank_of[req.task_id]
-        a["skipped"][i] = req.skipped
-        ne, ng = len(st.exec_intervals), len(st.gen_starts)
-        a["n_exec"][i], a["n_gen"][i] = ne, ng
-        a["hist_off"][i] = len(slot_rows)
-        for j in range(max(ne, ng)):
-            gs = st.gen_starts[j] if j < ng else 0
-            ge = st.gen_ends[j] if j < ng and st.gen_ends[j] is not None else 0
-            if j < ne:
-                iv = st.exec_intervals[j]
-                es, ee = iv.start, iv.end
-            else:
-                es = ee = 0
-            slot_rows.append((gs, ge, es, ee))
-    a["slots"] = np.asarray(slot_rows if slot_rows else [(0, 0, 0, 0)], np.int64).reshape(-1, 4)
+    cap = 1024 + 60 * n + 128 * n
+    while True:
+        buf = np.empty(cap, np.uint8)
+        offs = _kr_pack.pack(pending, states, rank_of, buf.ctypes.data, cap, 0)
+        if offs is not None:
+            break
+        cap *= 2
+    osl, o32, _, nsl = offs
+    c64 = buf[:40 * n].view(np.int64).reshape(5, n)
+    c32 = buf[o32:o32 + 20 * n].view(np.int32).reshape(5, n)
+    a = {k: c64[j] for j, k in enumerate(("t_start", "issued_at", "obs_captured_at", "accum_gen",
+                                           "hist_off"))}
+    a.update({k: c32[j] for j, k in enumerate(INT_FIELDS32)})
+    a["slots"] = buf[osl:osl + 32 * nsl].view(np.int64).reshape(nsl, 4)
     a["n"] = n
     return a
+
+
+def pack_mapped(reqs, states, rank_of, out_bytes: int) -> tuple:
+    """host_soa's columns written straight into the mapped arena
+    (device.MappedArena) by the native packer (_kr_pack, csrc/kr_pack.c: one
+    pass over the objects in C), plus `out_bytes` of output space: returns
+    (kr_fleet over the mapped device addresses, the output region as a uint8
+    host view, its device address).  The arena is reused by the next call on
+    this thread."""
+    from . import _kr_pack
+    n = len(reqs)
+    a = dev.arena()
+    while True:
+        offs = _kr_pack.pack(reqs, states, rank_of, a.blob.data_ptr(), a.nbytes, out_bytes)
+        if offs is not None:
+            break
+        a = dev.arena(2 * a.nbytes)
+    osl, o32, oout, _ = offs
+    d, d32 = a.dbase, a.dbase + o32
+    fs = _lib.KrFleet(n, d, d + 8 * n, d + 16 * n, d + 24 * n, d32, d32 + 4 * n, d32 + 8 * n,
+                      d + 32 * n, d32 + 12 * n, d32 + 16 * n, d + osl)
+    return fs, a.host[oout:oout + out_bytes], d + oout
 
 
 @dataclass

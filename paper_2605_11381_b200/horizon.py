@@ -140,8 +140,28 @@ def decide_horizon_batch(cfg: HorizonPolicyConfig, U: torch.Tensor,
 
 def decide_horizon(cfg: HorizonPolicyConfig, magnitudes: UpdateMagnitudes) -> int:
     """One round's execution horizon (horizon.py:108-132), on the device."""
-    U = dev.tensor(magnitudes.u[None], torch.float64)
-    return int(decide_horizon_batch(cfg, U, validate=False).item())
+    u = magnitudes.u
+    K, N = u.shape
+    a = dev.arena(8 * u.size + 64)
+    a.host[64:64 + 8 * u.size].view(np.float64)[:] = u.reshape(-1)
+    H = a.host[:4].view(np.int32)
+    st = dev.raw_stream()
+    lib = _lib.load()
+    if cfg.kind == STATIC:
+        _lib.check(lib.kr_horizon_static(1, N, cfg.static_h, a.dbase, st),
+                   "kr_horizon_static")
+    else:
+        # the magnitudes (validated by UpdateMagnitudes) staged into device
+        # scratch: the streaming kernel's TMA reads HBM; the horizon comes
+        # back through the mapped arena -- one copy, one launch, one sync
+        dU = a.device_scratch(8 * u.size)
+        _lib.check(lib.kr_memcpy_async(dU, a.dbase + 64, 8 * u.size, st),
+                   "kr_memcpy_async")
+        _lib.check(lib.kr_horizon_confidence(dU, _lib.KR_F64, 1, K, N, 1.0 + cfg.threshold,
+                                             cfg.min_horizon, a.dbase, None, 0, st),
+                   "kr_horizon_confidence")
+    dev.sync(st)
+    return int(H[0])
 
 
 SWEEP_MAX_CONFIGS = 64  # per kernel launch (kr_horizon_sweep); more are split

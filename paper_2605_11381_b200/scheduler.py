@@ -36,6 +36,7 @@ from . import engines as eng
 from . import fleet as fl
 from .core import Duration, PendingRequest, TaskState, TimePoint
 from .waiting import _state_fleet
+from . import ledger as _ledger
 
 KAIROS = "kairos"
 FIFO = "fifo"
@@ -106,10 +107,10 @@ def estimate_exec_latency(state: TaskState, default: Optional[Duration] = None) 
     return int(out.est.item())
 
 
-def _issued_base(issued: np.ndarray) -> int:
-    if issued.size == 0:
+def _issued_base(issued) -> int:
+    if len(issued) == 0:
         return 0
-    lo, hi = int(issued.min()), int(issued.max())
+    lo, hi = int(min(issued)), int(max(issued))
     if hi - lo >= fl.ISSUED_SPAN:
         raise ValueError("pending issue times span more than 2^40 µs; the packed sort key "
                          "cannot order them")
@@ -176,19 +177,64 @@ def plan(pending: Iterable[PendingRequest], states: Mapping[str, TaskState], edg
     if cfg.buckets > 256:
         raise ValueError("the packed sort key supports at most 256 buckets")
     rank = _ranks([r.task_id for r in reqs])
-    issued = np.fromiter((r.issued_at for r in reqs), np.int64, n)
-    base = _issued_base(issued)
-    sched = fl.sched_struct(cfg.policy, cfg.buckets, cfg.aging_interval, cfg.stale_threshold,
-                            cfg.default_exec_estimate, int(now), 1, base)
+    base = _issued_base([r.issued_at for r in reqs])
+    # the plan's keys need no control rate (need times are not part of it): hz = 1/1
+    sched = _lib.KrSched(fl.POLICY_CODE[cfg.policy], cfg.buckets, cfg.aging_interval, 0,
+                         cfg.stale_threshold, cfg.default_exec_estimate, int(now), 1, 1, base)
+    ledger_backed = isinstance(states, _ledger.LedgerStates)
+    no_cloud = cloud is None or net is None or cloud_avail == 0 or edge_avail >= n
+    if not ledger_backed and no_cloud and n <= SMALL_PLAN_MAX:
+        return _plan_small(reqs, states, rank, sched, min(edge_avail, n))
     flags = dev.flags()
-    from . import ledger as _ledger
-    if isinstance(states, _ledger.LedgerStates):
+    if ledger_backed:
         keys, view = states.ledger.urgency(reqs, states, rank, sched, flags)
     else:
         view = fl.DeviceFleet.from_host(fl.host_soa(reqs, states, rank))
         keys = fl.urgency(view, sched, need_time=False, flags=flags).keys
     return _place(reqs, states, keys, view, sched, flags, edge, cloud, net, edge_avail,
                   cloud_avail, edge_in_flight, cloud_in_flight)
+
+
+# ---------------------------------------------------------------------------
+# Small planning rounds: one launch, zero-copy staging (kr_plan_small)
+# ---------------------------------------------------------------------------
+SMALL_PLAN_MAX = 4096  # kr_plan_small's one-CTA bitonic sort
+
+
+def _bumped(req, skipped: int):
+    """dataclasses.replace(req, skipped=skipped) for an already validated
+    request (scheduler.py:232-234): the copy's fields are the original's."""
+    d = getattr(req, "__dict__", None)
+    if d is None or not hasattr(type(req), "__dataclass_fields__"):
+        return replace(req, skipped=skipped)
+    new = object.__new__(type(req))
+    new.__dict__.update(d)
+    new.__dict__["skipped"] = skipped
+    return new
+
+
+def _plan_small(reqs, states, rank_of, sched, k) -> DispatchPlan:
+    """Edge-tier plan() for n <= SMALL_PLAN_MAX in one launch + one sync."""
+    n = len(reqs)
+    fs, out, out_dev = fl.pack_mapped(reqs, states, rank_of, 4 * (3 * n + 1))
+    out = out.view(np.int32)
+    st = dev.raw_stream()
+    _lib.check(_lib.load().kr_plan_small(ctypes.byref(fs), ctypes.byref(sched), k, out_dev,
+                                         st), "kr_plan_small")
+    dev.sync(st)
+    f = int(out[3 * n]) & 0xFFFFFFFF
+    if f & (_lib.FLAG_KEY_RANGE | _lib.FLAG_RATIO):
+        raise ValueError("a pending request falls outside the packed sort-key range "
+                         "(aged estimate >= 2^56 µs or lifetime >= 2^53 µs)")
+    order_h = out[:n].tolist()
+    skipped_h = out[2 * n:3 * n].tolist()
+    refetch_idx = np.flatnonzero(out[n:2 * n]).tolist()
+    for i in order_h:
+        states[reqs[i].task_id].skipped = skipped_h[i]
+    s_edge = tuple([reqs[i] for i in order_h[:k]])
+    deferred = tuple([_bumped(reqs[i], skipped_h[i]) for i in order_h[k:]])
+    refetch_ids = frozenset([reqs[i].task_id for i in refetch_idx])
+    return DispatchPlan(edge=s_edge, cloud=(), deferred=deferred, refetch_task_ids=refetch_ids)
 
 
 def _place(reqs, states, keys, fleet, sched, flags, edge, cloud, net, edge_avail, cloud_avail,
@@ -244,7 +290,7 @@ def _place(reqs, states, keys, fleet, sched, flags, edge, cloud, net, edge_avail
     for i in order_h[k:]:
         if int(i) in in_cloud:
             continue
-        deferred.append(replace(reqs[i], skipped=int(skipped_h[i])))
+        deferred.append(_bumped(reqs[i], int(skipped_h[i])))
     refetch_ids = frozenset(reqs[i].task_id for i in np.nonzero(refetch_h)[0])
     return DispatchPlan(edge=tuple(s_edge), cloud=tuple(s_cloud), deferred=tuple(deferred),
                         refetch_task_ids=refetch_ids)

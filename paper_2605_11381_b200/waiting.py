@@ -8,6 +8,7 @@ ratio and the per-round waits are computed by the `kr_urgency` /
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from types import SimpleNamespace
 from typing import Sequence
@@ -53,6 +54,29 @@ def _sched(now: int) -> _lib.KrSched:
     return fl.sched_struct("fifo", 1, 1, 0, 0, now, 1, 0)
 
 
+_NO_REQ = SimpleNamespace(task_id=None, issued_at=0, obs_captured_at=0, skipped=0,
+                          last_exec_info=SimpleNamespace(remaining_actions=0))
+
+
+def _state_urgency(state: TaskState, now: int, slot_waits: bool):
+    """kr_urgency over a one-request view of `state`, columns and results in the
+    mapped arena (one launch + one synchronisation).  Returns (wr, slot waits
+    or None, flags)."""
+    req = SimpleNamespace(**{**vars(_NO_REQ), "task_id": state.task_id})
+    nsl = max(len(state.gen_starts), len(state.exec_intervals), 1)
+    out_bytes = 32 + (8 * nsl if slot_waits else 0)
+    fs, out, d = fl.pack_mapped([req], {state.task_id: state}, {state.task_id: 0}, out_bytes)
+    out[24:28].view(np.uint32)[0] = 0
+    sched = _sched(now)
+    st = dev.raw_stream()
+    _lib.check(_lib.load().kr_urgency(
+        ctypes.byref(fs), ctypes.byref(sched), d, None, None, d + 16, None, None,
+        d + 32 if slot_waits else None, None, d + 24, st), "kr_urgency")
+    dev.sync(st)
+    sw = out[32:32 + 8 * nsl].view(np.int64).copy() if slot_waits else None
+    return float(out[16:24].view(np.float64)[0]), sw, int(out[24:28].view(np.uint32)[0])
+
+
 def round_wait(gen_j: Interval, exec_j: Interval, gen_next: Interval,
                exec_next: Interval) -> Duration:
     """Wait between round j and j+1 on round j's dominant side (waiting.py:46-59)."""
@@ -77,16 +101,17 @@ def wait_ratio(ledger: WaitLedger, t_start: TimePoint, t_now: TimePoint) -> floa
     """Accumulated wait over lifetime, clamped to [0, 1] (waiting.py:62-66)."""
     if t_now <= t_start:
         raise ValueError(f"t_now {t_now} must be after t_start {t_start}")
-    total = dev.tensor([int(ledger.total_wait)], torch.int64)
-    ts = dev.tensor([int(t_start)], torch.int64)
-    wr = torch.empty(1, dtype=torch.float64, device=total.device)
-    flags = dev.flags()
-    _lib.check(_lib.load().kr_wait_ratio(total.data_ptr(), ts.data_ptr(), 1, int(t_now),
-                                         wr.data_ptr(), flags.data_ptr(), dev.stream()),
-               "kr_wait_ratio")
-    if dev.read_flags(flags) & _lib.FLAG_RATIO:
+    a = dev.arena(64)
+    v = a.host[:24].view(np.int64)  # total, t_start, ratio (fp64 bits)
+    f = a.host[24:28].view(np.uint32)
+    v[0], v[1], f[0] = int(ledger.total_wait), int(t_start), 0
+    st = dev.raw_stream()
+    _lib.check(_lib.load().kr_wait_ratio(a.dbase, a.dbase + 8, 1, int(t_now), a.dbase + 16,
+                                         a.dbase + 24, st), "kr_wait_ratio")
+    dev.sync(st)
+    if int(f[0]) & _lib.FLAG_RATIO:
         raise ValueError("wait-ratio operands beyond 2^53 are not exactly representable")
-    return float(wr.item())
+    return float(v[2:3].view(np.float64)[0])
 
 
 def ledger_from_history(state: TaskState) -> WaitLedger:
@@ -94,12 +119,10 @@ def ledger_from_history(state: TaskState) -> WaitLedger:
     n_exec = len(state.exec_intervals)
     if n_exec == 0:
         return WaitLedger.from_waits([])
-    out = fl.urgency(_state_fleet(state), _sched(0), need_time=False, slot_waits=True)
-    sw = out.slot_wait[:n_exec].cpu().numpy()
-    return WaitLedger.from_waits([int(w) for w in sw if w >= 0])
+    _, sw, _ = _state_urgency(state, 0, True)
+    return WaitLedger.from_waits([int(w) for w in sw[:n_exec] if w >= 0])
 
 
 def current_wait_ratio(state: TaskState, now: TimePoint) -> float:
     """Wait ratio of a live task; 0.0 before it has any lifetime (waiting.py:96-100)."""
-    out = fl.urgency(_state_fleet(state), _sched(int(now)), need_time=False, intermediates=True)
-    return float(out.wr.item())
+    return _state_urgency(state, int(now), False)[0]

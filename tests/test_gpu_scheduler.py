@@ -33,7 +33,13 @@ def test_time_golden(kb):
         assert out == [r["us"] for r in rs], hz
 
 
-def test_plan_golden(kb):
+@pytest.mark.parametrize("small", [True, False])
+def test_plan_golden(kb, small, monkeypatch):
+    """Every golden plan through the one-launch small path (kr_plan_small,
+    zero-copy staging) and through the general multi-kernel path."""
+    from paper_2605_11381_b200 import scheduler
+    if not small:
+        monkeypatch.setattr(scheduler, "SMALL_PLAN_MAX", 0)
     for ii, inst in enumerate(golden_io.plan_instances()):
         states, pending = golden_io.build_objects(inst, kb)
         edge = kb.EngineProfile(tier="edge", capacity=inst["capacity"], max_batch=1,
@@ -195,3 +201,31 @@ def test_engine_reference_goldens(kb):
     assert kb.cloud_round_trip(wan, 300_000, 0, 150_000) == 352_400
     with pytest.raises(kb.ProfileError):
         kb.EngineProfile(tier="edge", capacity=1, max_batch=2, points=((1, 10), (2, 100)))
+
+
+@pytest.mark.parametrize("n,k,policy", [(1, 1, "kairos"), (7, 3, "kairos"), (33, 0, "fifo"),
+                                        (200, 64, "las"), (1000, 64, "kairos"),
+                                        (4096, 1024, "kairos"), (2500, 2500, "kairos")])
+def test_plan_small_vs_oracle(kb, n, k, policy):
+    """kr_plan_small on synthetic fleets vs the oracle's plan (order, refetch,
+    skip counters), through the C ABI with the columns in mapped pinned host
+    memory: P = next power of two of n (bitonic padding), k = 0 and k = n."""
+    import ctypes
+    from paper_2605_11381_b200 import _lib, fleet as fl, synthetic
+    soa = synthetic.fleet_soa(n, seed=n + k)
+    soa["lexrank"] = np.random.default_rng(n).permutation(n).astype(np.int32)
+    base = int(soa["issued_at"].min())
+    sched = fl.sched_struct(policy, 10, 5, 150_000, 166_667, synthetic.NOW, 30, base)
+    pinned = {key: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+              for key, v in soa.items() if key != "n"}
+    fs = fl.DeviceFleet.from_tensors(pinned).c_struct()
+    out = torch.empty(3 * n + 1, dtype=torch.int32).pin_memory()
+    _lib.check(_lib.load().kr_plan_small(ctypes.byref(fs), ctypes.byref(sched), k,
+                                         out.data_ptr(), None), "kr_plan_small")
+    torch.cuda.synchronize()
+    res = orc.plan_soa(soa, policy, 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+    o = out.numpy()
+    assert np.array_equal(o[:n], res["order"])
+    assert np.array_equal(o[n:2 * n], res["refetch"])
+    assert np.array_equal(o[2 * n:3 * n], res["skipped_out"])
+    assert o[3 * n] == 0

@@ -93,8 +93,8 @@ class MappedArena(threading.local):
         return self.scratch.data_ptr()
 
     def ensure(self, nbytes: int) -> "MappedArena":
-        if nbytes > self.nbytes:
-            size = max(1 << 16, 1 << (nbytes - 1).bit_length())
+        if nbytes > self.nbytes or self.blob is None:
+            size = max(1 << 16, 1 << (max(nbytes, 1) - 1).bit_length())
             blob = torch.empty(size, dtype=torch.uint8, pin_memory=True)
             dptr = ctypes.c_void_p()
             _lib.check(_lib.load().kr_mapped_ptr(blob.data_ptr(), ctypes.byref(dptr)),

@@ -14,7 +14,7 @@ from pathlib import Path
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libkairos_b200.so"
+LIB_PATH = Path(os.environ["KR_LIB_PATH"]) if os.environ.get("KR_LIB_PATH") else _PKG / "libkairos_b200.so"  # KR_LIB_PATH: A/B builds (tools/)
 
 KR_OK, KR_EINVAL, KR_ECUDA, KR_ENOSPACE, KR_EFORMAT = 0, 1, 2, 3, 4
 KR_F32, KR_F64 = 0, 1

@@ -451,6 +451,50 @@ __device__ __forceinline__ int64_t total_wait(const int64_t* slots, int32_t n_ex
     return total;
 }
 
+// Round j's recorded wait given its successor slot (only the successor's
+// generation / execution start is read), the per-round body of total_wait.
+__device__ __forceinline__ int64_t round_wait(const Slot& cur, int64_t nxt_gs, int64_t nxt_es,
+                                              int32_t j, int32_t n_exec, int32_t n_gen) {
+    int64_t w = 0;
+    if (cur.ge - cur.gs >= cur.ee - cur.es) {
+        if (n_gen > j + 1) w = nxt_gs - cur.ge;
+    } else if (j + 1 < n_exec) {
+        w = nxt_es - cur.ee;
+    }
+    return w > 0 ? w : 0;
+}
+
+// total_wait plus the last execution's length, with the first four slots
+// loaded up front (independent loads: one memory latency for a history of up
+// to four slots instead of one per round); longer histories continue slot by
+// slot.  Same per-round arithmetic as total_wait.
+__device__ __forceinline__ void history_walk(const int64_t* slots, int32_t n_exec, int32_t n_gen,
+                                             int64_t& total, int64_t& last) {
+    total = 0;
+    last = 0;
+    if (n_exec <= 0) return;
+    const int32_t ext = n_gen > n_exec ? n_gen : n_exec;
+    const Slot z{0, 0, 0, 0};
+    const Slot s0 = load_slot(slots, 0);
+    const Slot s1 = ext > 1 ? load_slot(slots, 1) : z;
+    const Slot s2 = ext > 2 ? load_slot(slots, 2) : z;
+    const Slot s3 = ext > 3 ? load_slot(slots, 3) : z;
+    total = round_wait(s0, s1.gs, s1.es, 0, n_exec, n_gen);
+    if (n_exec > 1) total += round_wait(s1, s2.gs, s2.es, 1, n_exec, n_gen);
+    if (n_exec > 2) total += round_wait(s2, s3.gs, s3.es, 2, n_exec, n_gen);
+    const Slot& l = n_exec == 1 ? s0 : n_exec == 2 ? s1 : n_exec == 3 ? s2 : s3;
+    last = l.ee - l.es;
+    if (n_exec > 3) {  // rounds 3 .. n_exec-1
+        Slot cur = s3;
+        for (int32_t j = 3; j < n_exec; j++) {
+            const Slot nxt = j + 1 < ext ? load_slot(slots, j + 1) : z;
+            total += round_wait(cur, nxt.gs, nxt.es, j, n_exec, n_gen);
+            if (j == n_exec - 1) last = cur.ee - cur.es;
+            cur = nxt;
+        }
+    }
+}
+
 // Python `int / int` is the correctly rounded quotient; for |operands| < 2^53
 // both convert exactly and IEEE division gives the same double.
 __device__ __forceinline__ double wait_ratio(int64_t total, int64_t t_start, int64_t now,

@@ -48,4 +48,20 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Resident CTAs per SM of `kernel` at `threads` (>= 1).
+template <class K>
+inline int occupancy(K kernel, int threads, size_t smem = 0) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess)
+        b = 1;
+    return b < 1 ? 1 : b;
+}
+// CTAs covering n items at `threads` per CTA, capped at one resident wave.
+inline unsigned grid_cap(int64_t n, int threads, int per_sm) {
+    int64_t b = (n + threads - 1) / threads;
+    const int64_t cap = static_cast<int64_t>(device_info().sm_count) * per_sm;
+    if (b > cap) b = cap;
+    return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
 }  // namespace kr

@@ -28,12 +28,32 @@
 namespace kr {
 
 constexpr int kDigitBits = 11;
+#ifndef KR_SEL_U
+#define KR_SEL_U 4
+#endif
+constexpr int kSelU = KR_SEL_U;  // keys in flight per thread in the level-0 histogram
+#ifndef KR_SCAT_W
+#define KR_SCAT_W 1
+#endif
+constexpr int kScatW = KR_SCAT_W;  // digits per thread per step in the level-0 scatter
 constexpr int kBins = 1 << kDigitBits;
 #ifndef KR_SORT_TILE
 #define KR_SORT_TILE 4096
 #endif
 constexpr int kSortTile = KR_SORT_TILE;  // LSD radix: elements per CTA tile (256 threads x 16)
 
+// Digit = the values of the candidate set's kDigitBits most significant
+// *differing* bit positions (a pext of OR ^ AND), MSB first.  All candidates
+// agree on every other bit, so digit order is key order; unlike a contiguous
+// bit window it never wastes digit bits on constant fields (e.g. the high
+// zero bits of the aged estimate between the bucket and its significant bits).
+struct Digit {
+    int W;                 // number of digit bits (0: all candidates identical)
+    int nrun;              // the digit bits grouped into runs of adjacent positions
+    int run_pos[kDigitBits];  // lowest bit position (0..127) of each run, MSB run first
+    int run_len[kDigitBits];
+    bool any;
+};
 struct SelState {
     unsigned long long st[2][4];  // [parity] {or_hi, or_lo, and_hi, and_lo}
     unsigned int cnt[2];          // [parity] candidate count
@@ -46,11 +66,16 @@ struct SelState {
     unsigned int sel_count;       // admission gather count
     unsigned int pad2_[3];
     unsigned long long sst[4];    // OR/AND of the gathered (admitted) keys
+    Digit d0;                     // level-0 digit (from the keys' OR / AND)
+    unsigned int dstar0;          // its boundary bin (dstar moves on in later levels)
+    unsigned int done_hist;       // last-CTA-done counters of the two grid passes
+    unsigned int done_scatter;
     unsigned int hist[kBins];
 };
 
 struct Workspace {
     SelState* state;
+    uint16_t* digits;  // level-0 digit of every key
     kr_key* cand[2];
     kr_key* skeys[2];
     int32_t* sidx[2];
@@ -64,6 +89,7 @@ static size_t sort_tiles(int64_t n) { return static_cast<size_t>((n + kSortTile 
 static size_t workspace_bytes(int64_t n) {
     size_t nn = static_cast<size_t>(n < 1 ? 1 : n);
     size_t b = align256(sizeof(SelState));
+    b += align256(nn * sizeof(uint16_t));        // level-0 digits
     b += 2 * align256(nn * sizeof(kr_key));      // select candidates
     b += 2 * align256(nn * sizeof(kr_key));      // sort keys ping-pong
     b += 2 * align256(nn * sizeof(int32_t));     // sort index ping-pong
@@ -77,6 +103,8 @@ static Workspace carve(void* ws, int64_t n) {
     Workspace w;
     w.state = reinterpret_cast<SelState*>(p);
     p += align256(sizeof(SelState));
+    w.digits = reinterpret_cast<uint16_t*>(p);
+    p += align256(nn * sizeof(uint16_t));
     for (int i = 0; i < 2; i++) {
         w.cand[i] = reinterpret_cast<kr_key*>(p);
         p += align256(nn * sizeof(kr_key));
@@ -135,41 +163,6 @@ __device__ __forceinline__ void stats_accumulate(unsigned long long* dst, unsign
     }
 }
 
-// Block-aggregated append: returns this thread's slot (valid if `take`).
-__device__ __forceinline__ unsigned block_append(bool take, unsigned int* counter) {
-    __shared__ unsigned int wcnt[32];
-    __shared__ unsigned int base;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
-    const unsigned ballot = __ballot_sync(0xffffffffu, take);
-    if (lane == 0) wcnt[warp] = __popc(ballot);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned total = 0;
-        for (int w = 0; w < nw; w++) {
-            unsigned c = wcnt[w];
-            wcnt[w] = total;
-            total += c;
-        }
-        base = total ? atomicAdd(counter, total) : 0u;
-    }
-    __syncthreads();
-    const unsigned pos = base + wcnt[warp] + __popc(ballot & ((1u << lane) - 1));
-    __syncthreads();  // wcnt / base reused by the next call
-    return pos;
-}
-
-// Digit = the values of the candidate set's kDigitBits most significant
-// *differing* bit positions (a pext of OR ^ AND), MSB first.  All candidates
-// agree on every other bit, so digit order is key order; unlike a contiguous
-// bit window it never wastes digit bits on constant fields (e.g. the high
-// zero bits of the aged estimate between the bucket and its significant bits).
-struct Digit {
-    int W;                 // number of digit bits (0: all candidates identical)
-    int nrun;              // the digit bits grouped into runs of adjacent positions
-    int run_pos[kDigitBits];  // lowest bit position (0..127) of each run, MSB run first
-    int run_len[kDigitBits];
-    bool any;
-};
 // Built with compile-time indices only (predicated updates) so that the run
 // table lives in registers for the per-key extraction loops.
 __device__ __forceinline__ Digit digit_of(const unsigned long long* s) {
@@ -227,20 +220,45 @@ __device__ __forceinline__ unsigned digit_val(const kr_key& k, const Digit& d) {
 // ---------------------------------------------------------------------------
 // radix select
 // ---------------------------------------------------------------------------
-__global__ void k_sel_reset(SelState* s, int64_t n, int64_t k, const unsigned long long* stats) {
+// Three launches: k_sel_reset (state, level-0 digit from the keys' OR / AND),
+// k_sel_hist0 (every key's digit -> a 16-bit digit array + the histogram; the
+// last CTA to finish picks the boundary bin d*) and k_sel_scatter0 (the keys
+// of bin d*, read through the digit array, -> candidates; the last CTA runs
+// the remaining levels over the candidates alone and publishes the k-th key).
+// The admission pass then decides most keys from the digit array alone
+// (digit < d*: in, > d*: out).  "Last CTA" = the CTA whose increment of a
+// completion counter returns gridDim - 1, after a release fence by every CTA.
+__device__ __forceinline__ void sel_init(SelState* s, int64_t n, int64_t k) {
+    s->st[1][0] = 0; s->st[1][1] = 0; s->st[1][2] = ~0ull; s->st[1][3] = ~0ull;
+    s->sst[0] = 0; s->sst[1] = 0; s->sst[2] = ~0ull; s->sst[3] = ~0ull;
+    s->cnt[0] = static_cast<unsigned>(n);
+    s->cnt[1] = 0;
+    s->need = k;
+    s->done = 0;
+    s->sel_count = 0;
+    s->done_hist = 0;
+    s->done_scatter = 0;
+}
+// The level-0 digit of the full key set; a set of identical keys (n == 1,
+// keys being unique) is its own answer.
+__device__ __forceinline__ void sel_digit0(SelState* s, const kr_key* keys) {
+    s->d0 = digit_of(s->st[0]);
+    if (!s->d0.any) {
+        s->kth = keys[0];
+        s->done = 1;
+    }
+}
+
+__global__ void k_sel_reset(SelState* s, int64_t n, int64_t k, const unsigned long long* stats,
+                            const kr_key* keys) {
     for (int i = threadIdx.x; i < kBins; i += blockDim.x) s->hist[i] = 0;
     if (threadIdx.x == 0) {
-        for (int p = 0; p < 2; p++) {
-            s->st[p][0] = 0; s->st[p][1] = 0; s->st[p][2] = ~0ull; s->st[p][3] = ~0ull;
-        }
-        if (stats)
+        s->st[0][0] = 0; s->st[0][1] = 0; s->st[0][2] = ~0ull; s->st[0][3] = ~0ull;
+        sel_init(s, n, k);
+        if (stats) {
             for (int j = 0; j < 4; j++) s->st[0][j] = stats[j];
-        s->sst[0] = 0; s->sst[1] = 0; s->sst[2] = ~0ull; s->sst[3] = ~0ull;
-        s->cnt[0] = static_cast<unsigned>(n);
-        s->cnt[1] = 0;
-        s->need = k;
-        s->done = 0;
-        s->sel_count = 0;
+            sel_digit0(s, keys);
+        }
     }
 }
 
@@ -254,52 +272,35 @@ __global__ void __launch_bounds__(256) k_sel_stats(const kr_key* __restrict__ ke
     }
     stats_accumulate(s->st[0], oh, ol, ah, al);
 }
+__global__ void k_sel_digit(SelState* s, const kr_key* keys) { sel_digit0(s, keys); }
 
-// level L reads candidates src (count cnt[L&1]) and histograms their digit.
-__global__ void __launch_bounds__(256) k_sel_hist(const kr_key* __restrict__ src, SelState* s,
-                                                  int level) {
-    __shared__ unsigned int h[kBins];
-    if (s->done) return;
-    const int p = level & 1;
-    Digit d = digit_of(s->st[p]);
-    const int64_t n = s->cnt[p];
-    const int bins = 1 << d.W;
-    for (int i = threadIdx.x; i < bins; i += blockDim.x) h[i] = 0;
+// True in every thread of the CTA that completes the grid pass last.
+__device__ __forceinline__ bool last_cta(unsigned int* counter) {
+    __shared__ bool last;
+    __threadfence();
     __syncthreads();
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        atomicAdd(&h[digit_val(src[i], d)], 1u);
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
     __syncthreads();
-    for (int i = threadIdx.x; i < bins; i += blockDim.x)
-        if (h[i]) atomicAdd(&s->hist[i], h[i]);
+    if (last) __threadfence();
+    return last;
 }
 
-// One block: choose the boundary bin d* (cum_lt < need <= cum_le).
-__device__ void sel_pick_block(SelState* s, int level, const unsigned int* hist,
-                               const kr_key* src) {
+// One block: choose the boundary bin d* (cum_lt < need <= cum_le) of `hist`
+// (bins of digit d; shared memory or this CTA's own data).
+__device__ void sel_pick_block(SelState* s, const Digit& d, const unsigned int* hist) {
     __shared__ unsigned int part[1024];
-    __shared__ int found;
-    const int p = level & 1;
-    Digit d = digit_of(s->st[p]);
-    if (!d.any) {  // all candidates identical: unique keys => a single one
-        if (threadIdx.x == 0) {
-            s->kth = src[0];
-            s->done = 1;
-        }
-        return;
-    }
     const int bins = 1 << d.W;
-    const int per = (bins + blockDim.x - 1) / blockDim.x;
+    const int nt = blockDim.x;
+    const int per = (bins + nt - 1) / nt;
     unsigned int local = 0;
     for (int q = 0; q < per; q++) {
         int b = threadIdx.x * per + q;
         if (b < bins) local += hist[b];
     }
     part[threadIdx.x] = local;
-    if (threadIdx.x == 0) found = 0;
     __syncthreads();
     // inclusive scan of part[] (Hillis-Steele)
-    for (int o = 1; o < blockDim.x; o <<= 1) {
+    for (int o = 1; o < nt; o <<= 1) {
         unsigned int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
         __syncthreads();
         part[threadIdx.x] += v;
@@ -317,92 +318,81 @@ __device__ void sel_pick_block(SelState* s, int level, const unsigned int* hist,
                 s->dstar = static_cast<unsigned>(b);
                 s->dcount = c;
                 s->need = need - static_cast<long long>(cum);
-                found = 1;
                 break;
             }
             cum += c;
         }
     }
     __syncthreads();
-    (void)found;
 }
 
-__global__ void __launch_bounds__(1024) k_sel_pick(SelState* s, const kr_key* src, int level) {
-    if (s->done) return;
-    sel_pick_block(s, level, s->hist, src);
-    __syncthreads();
-    // reset for the next level
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) s->hist[i] = 0;
+// Level 0 over all keys: digits[i] and the histogram; the last CTA picks d*.
+__global__ void __launch_bounds__(256) k_sel_hist0(const kr_key* __restrict__ keys, int64_t n,
+                                                   uint16_t* __restrict__ digits, SelState* s) {
+    __shared__ unsigned int h[kBins];
+    __shared__ Digit sd;
+    __shared__ int sdone;
     if (threadIdx.x == 0) {
-        const int q = (level + 1) & 1;
-        s->st[q][0] = 0; s->st[q][1] = 0; s->st[q][2] = ~0ull; s->st[q][3] = ~0ull;
-        s->cnt[q] = 0;
+        sd = s->d0;
+        sdone = s->done;
     }
-}
-
-// Keep the boundary bin; if it holds one key that key is the answer.
-__global__ void __launch_bounds__(256) k_sel_scatter(const kr_key* __restrict__ src, kr_key* dst,
-                                                     SelState* s, int level) {
-    if (s->done) return;
-    const int p = level & 1, q = (level + 1) & 1;
-    Digit d = digit_of(s->st[p]);
-    const int64_t n = s->cnt[p];
-    const unsigned dstar = s->dstar;
-    const bool single = s->dcount == 1;
-    unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < n; base += stride) {
-        int64_t i = base + threadIdx.x;
-        bool keep = false;
-        kr_key k{0, 0};
-        if (i < n) {
-            k = src[i];
-            keep = digit_val(k, d) == dstar;
-        }
-        if (single) {
-            if (keep) {
-                s->kth = k;
-                s->done = 1;
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const Digit d = sd;
+    if (!sdone) {
+        // kSelU keys in flight per thread
+        const int64_t T = blockDim.x;
+        for (int64_t base = blockIdx.x * T * kSelU; base < n; base += int64_t(gridDim.x) * T * kSelU) {
+            kr_key kk[kSelU];
+#pragma unroll
+            for (int u = 0; u < kSelU; u++) {
+                const int64_t i = base + u * T + threadIdx.x;
+                if (i < n) kk[u] = keys[i];
             }
-            continue;
+#pragma unroll
+            for (int u = 0; u < kSelU; u++) {
+                const int64_t i = base + u * T + threadIdx.x;
+                if (i < n) {
+                    const unsigned v = digit_val(kk[u], d);
+                    digits[i] = static_cast<uint16_t>(v);
+                    atomicAdd(&h[v], 1u);
+                }
+            }
         }
-        unsigned mask = __ballot_sync(0xffffffffu, keep);
-        unsigned pos = 0;
-        if (mask) {
-            int lane = threadIdx.x & 31;
-            int leader = __ffs(mask) - 1;
-            unsigned basepos = 0;
-            if (lane == leader) basepos = atomicAdd(&s->cnt[q], __popc(mask));
-            basepos = __shfl_sync(0xffffffffu, basepos, leader);
-            pos = basepos + __popc(mask & ((1u << lane) - 1));
-        }
-        if (keep) {
-            dst[pos] = k;
-            oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
-        }
+        __syncthreads();
+        const int bins = 1 << d.W;
+        for (int i = threadIdx.x; i < bins; i += blockDim.x)
+            if (h[i]) atomicAdd(&s->hist[i], h[i]);
     }
-    if (!single) stats_accumulate(s->st[q], oh, ol, ah, al);
+    if (!last_cta(&s->done_hist) || sdone) return;
+    const int bins = 1 << d.W;
+    for (int i = threadIdx.x; i < bins; i += blockDim.x) h[i] = __ldcg(&s->hist[i]);
+    __syncthreads();
+    sel_pick_block(s, d, h);
+    if (threadIdx.x == 0) s->dstar0 = s->dstar;
 }
 
-// Single CTA: remaining levels over global ping-pong buffers.
-__global__ void __launch_bounds__(1024) k_sel_finish(SelState* s, kr_key* bufA, kr_key* bufB,
-                                                     int level) {
+// Remaining levels over the candidates (count cnt[p], OR / AND st[p]) in one
+// CTA, ping-ponging between src and dst, until one key remains.
+__device__ void sel_finish_block(SelState* s, kr_key* src, kr_key* dst, int p) {
     __shared__ unsigned int h[kBins];
     __shared__ unsigned long long sst[4];
     __shared__ unsigned int scnt;
-    if (s->done) return;
-    // bufA holds the candidates of `level` (the last grid-wide scatter's output)
-    kr_key* src = bufA;
-    kr_key* dst = bufB;
-    int p = level & 1;
+    __shared__ unsigned int sn, sdstar, ssingle;
+    __shared__ unsigned long long stin[4];
     for (int it = 0; it < 130; it++) {
-        const unsigned n = s->cnt[p];
-        Digit d = digit_of(s->st[p]);
+        // L2 reads: the first level's count and OR / AND come from other CTAs
+        if (threadIdx.x == 0) sn = __ldcg(&s->cnt[p]);
+        if (threadIdx.x < 4) stin[threadIdx.x] = __ldcg(&s->st[p][threadIdx.x]);
+        __syncthreads();
+        const unsigned n = sn;
+        const Digit d = digit_of(stin);
         if (!d.any || n <= 1) {
             if (threadIdx.x == 0) {
                 s->kth = src[0];
                 s->done = 1;
             }
+            __syncthreads();
             return;
         }
         const int bins = 1 << d.W;
@@ -410,13 +400,16 @@ __global__ void __launch_bounds__(1024) k_sel_finish(SelState* s, kr_key* bufA, 
         __syncthreads();
         for (unsigned i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&h[digit_val(src[i], d)], 1u);
         __syncthreads();
-        sel_pick_block(s, p, h, src);
-        __syncthreads();
-        const unsigned dstar = s->dstar;
-        const bool single = s->dcount == 1;
+        sel_pick_block(s, d, h);
+        if (threadIdx.x == 0) {
+            sdstar = s->dstar;
+            ssingle = s->dcount == 1;
+        }
         if (threadIdx.x < 4) sst[threadIdx.x] = threadIdx.x < 2 ? 0ull : ~0ull;
         if (threadIdx.x == 0) scnt = 0;
         __syncthreads();
+        const unsigned dstar = sdstar;
+        const bool single = ssingle;
         unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
         for (unsigned base = 0; base < n; base += blockDim.x) {
             unsigned i = base + threadIdx.x;
@@ -448,7 +441,10 @@ __global__ void __launch_bounds__(1024) k_sel_finish(SelState* s, kr_key* bufA, 
                 oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
             }
         }
-        if (single) return;
+        if (single) {
+            __syncthreads();
+            return;
+        }
         oh = warp_or(oh); ol = warp_or(ol); ah = warp_and(ah); al = warp_and(al);
         if ((threadIdx.x & 31) == 0) {
             atomicOr(&sst[0], oh); atomicOr(&sst[1], ol);
@@ -466,11 +462,80 @@ __global__ void __launch_bounds__(1024) k_sel_finish(SelState* s, kr_key* bufA, 
     }
 }
 
+// The keys of bin d* -> cand (through the digit array; single-key bin: the
+// answer), then in the last CTA the remaining levels; kth_out (nullable)
+// receives the k-th key.
+__global__ void __launch_bounds__(256) k_sel_scatter0(const kr_key* __restrict__ keys, int64_t n,
+                                                      const uint16_t* __restrict__ digits,
+                                                      kr_key* cand, kr_key* spare, SelState* s,
+                                                      kr_key* kth_out) {
+    __shared__ unsigned sdstar;
+    __shared__ int ssingle, sdone;
+    if (threadIdx.x == 0) {
+        sdstar = s->dstar;
+        ssingle = s->dcount == 1;
+        sdone = s->done;
+    }
+    __syncthreads();
+    const unsigned dstar = sdstar;
+    const bool single = ssingle;
+    unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+    if (!sdone) {
+        // kScatW digits per thread per step (8: one 16-byte load)
+        const int lane = threadIdx.x & 31;
+        const int64_t stride = int64_t(gridDim.x) * blockDim.x * kScatW;
+        for (int64_t base = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * kScatW;
+             base - threadIdx.x * kScatW < n; base += stride) {
+            uint16_t dg[kScatW];
+            if (kScatW == 8 && base + 8 <= n) {
+                const uint4 v = *reinterpret_cast<const uint4*>(digits + base);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < kScatW; u++)
+                    dg[u] = static_cast<uint16_t>(w[(u >> 1) & 3] >> (16 * (u & 1)));
+            } else {
+#pragma unroll
+                for (int u = 0; u < kScatW; u++) dg[u] = base + u < n ? digits[base + u] : 0xFFFFu;
+            }
+#pragma unroll
+            for (int u = 0; u < kScatW; u++) {
+                const bool keep = dg[u] == dstar && base + u < n;
+                kr_key k{0, 0};
+                if (keep) k = keys[base + u];
+                if (single) {
+                    if (keep) {
+                        s->kth = k;
+                        s->done = 1;
+                    }
+                    continue;
+                }
+                const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                if (mask) {
+                    const int leader = __ffs(mask) - 1;
+                    unsigned bp = 0;
+                    if (lane == leader) bp = atomicAdd(&s->cnt[1], __popc(mask));
+                    bp = __shfl_sync(0xffffffffu, bp, leader);
+                    if (keep) {
+                        cand[bp + __popc(mask & ((1u << lane) - 1))] = k;
+                        oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
+                    }
+                }
+            }
+        }
+        if (!single) stats_accumulate(s->st[1], oh, ol, ah, al);
+    }
+    if (!last_cta(&s->done_scatter)) return;
+    if (!__ldcg(&s->done)) sel_finish_block(s, cand, spare, 1);
+    if (kth_out && threadIdx.x == 0) {
+        const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(&s->kth));
+        *kth_out = kr_key{v.x, v.y};
+    }
+}
+
 __global__ void k_set_key(kr_key* dst, unsigned long long hi, unsigned long long lo) {
     dst->hi = hi;
     dst->lo = lo;
 }
-__global__ void k_copy_kth(const SelState* s, kr_key* dst) { *dst = s->kth; }
 
 // ---------------------------------------------------------------------------
 // admission pass (scheduler.py:204-207, 223-234)
@@ -489,6 +554,7 @@ struct AdmitArgs {
     kr_key* sel_keys;       // nullable (gather)
     int32_t* sel_idx;
     SelState* s;
+    const uint16_t* digits; // nullable: level-0 digits of the select that produced kth
 };
 
 __global__ void k_admit_init(SelState* s) {
@@ -498,28 +564,140 @@ __global__ void k_admit_init(SelState* s) {
     }
 }
 
+// One thread per request.  After the fused select the digit array decides a
+// request without its key unless its digit is the boundary bin's.  Admitted
+// (key, index) pairs are appended per warp (one atomic per warp; their order
+// is fixed by the sort that follows).
 __global__ void __launch_bounds__(256) k_admit(AdmitArgs a) {
     kr_key kth{~0ull, ~0ull};
     if (!a.all && !a.none) kth = *a.kth;
+    const bool dig = a.digits && !a.all && !a.none;
+    const unsigned dstar = dig ? a.s->dstar0 : 0u;
     unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int lane = threadIdx.x & 31;
     for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < a.n; base += stride) {
         int64_t i = base + threadIdx.x;
         bool in = false;
         kr_key k{0, 0};
         if (i < a.n) {
-            k = a.keys[i];
-            in = !a.none && (a.all || key_le(k, kth));
+            if (dig) {  // after the fused select: the digit decides outside bin d*
+                const unsigned dg = a.digits[i];
+                if (dg == dstar) {
+                    k = a.keys[i];
+                    in = key_le(k, kth);
+                } else {
+                    in = dg < dstar;
+                    if (in && a.sel_keys) k = a.keys[i];
+                }
+            } else {
+                k = a.keys[i];
+                in = !a.none && (a.all || key_le(k, kth));
+            }
             if (a.admitted) a.admitted[i] = in;
             if (a.refetch) a.refetch[i] = in && (a.now - __ldg(a.obs + i) > a.stale);
             if (a.skipped) a.skipped[i] = in ? 0 : a.skipped[i] + 1;
         }
-        if (a.sel_keys && __syncthreads_or(in)) {
-            unsigned pos = block_append(in, &a.s->sel_count);
-            if (in) {
-                a.sel_keys[pos] = k;
-                a.sel_idx[pos] = static_cast<int32_t>(i);
-                oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
+        if (a.sel_keys) {
+            const unsigned mask = __ballot_sync(0xffffffffu, in);
+            if (mask) {
+                const int leader = __ffs(mask) - 1;
+                unsigned bp = 0;
+                if (lane == leader) bp = atomicAdd(&a.s->sel_count, __popc(mask));
+                bp = __shfl_sync(0xffffffffu, bp, leader);
+                if (in) {
+                    const unsigned pos = bp + __popc(mask & ((1u << lane) - 1));
+                    a.sel_keys[pos] = k;
+                    a.sel_idx[pos] = static_cast<int32_t>(i);
+                    oh |= k.hi; ol |= k.lo; ah &= k.hi; al &= k.lo;
+                }
+            }
+        }
+    }
+    if (a.sel_keys) stats_accumulate(a.s->sst, oh, ol, ah, al);
+}
+
+// The admission pass after the fused select: four requests per thread with
+// vector loads / stores of the digit, skip-counter, admitted and refetch
+// columns; a request's key is read only in the boundary bin (or, when
+// gathering, if admitted), its observation time only if admitted.
+__global__ void __launch_bounds__(256) k_admit_dig(AdmitArgs a) {
+    const kr_key kth = *a.kth;
+    const unsigned dstar = a.s->dstar0;
+    const int lane = threadIdx.x & 31;
+    unsigned long long oh = 0, ol = 0, ah = ~0ull, al = ~0ull;
+    const int64_t n = a.n;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x * 4;
+    for (int64_t base = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * 4;
+         base - threadIdx.x * 4 < n; base += stride) {
+        const bool full = base + 4 <= n;
+        unsigned dg[4];
+        int32_t sk[4] = {0, 0, 0, 0};
+        if (full) {
+            const uint2 v = *reinterpret_cast<const uint2*>(a.digits + base);
+            dg[0] = v.x & 0xFFFFu; dg[1] = v.x >> 16; dg[2] = v.y & 0xFFFFu; dg[3] = v.y >> 16;
+            if (a.skipped) {
+                const int4 q = *reinterpret_cast<const int4*>(a.skipped + base);
+                sk[0] = q.x; sk[1] = q.y; sk[2] = q.z; sk[3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                dg[u] = base + u < n ? a.digits[base + u] : 0xFFFFFFFFu;
+                if (a.skipped && base + u < n) sk[u] = a.skipped[base + u];
+            }
+        }
+        bool in[4];
+        kr_key kk[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            in[u] = false;
+            kk[u] = kr_key{0, 0};
+            if (base + u < n) {
+                if (dg[u] == dstar) {
+                    kk[u] = a.keys[base + u];
+                    in[u] = key_le(kk[u], kth);
+                } else {
+                    in[u] = dg[u] < dstar;
+                    if (in[u] && a.sel_keys) kk[u] = a.keys[base + u];
+                }
+            }
+        }
+        uint32_t adm = 0, ref = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            adm |= static_cast<uint32_t>(in[u]) << (8 * u);
+            if (a.refetch && in[u] && a.now - __ldg(a.obs + base + u) > a.stale) ref |= 1u << (8 * u);
+            sk[u] = in[u] ? 0 : sk[u] + 1;
+        }
+        if (full) {
+            if (a.admitted) *reinterpret_cast<uint32_t*>(a.admitted + base) = adm;
+            if (a.refetch) *reinterpret_cast<uint32_t*>(a.refetch + base) = ref;
+            if (a.skipped) *reinterpret_cast<int4*>(a.skipped + base) = make_int4(sk[0], sk[1], sk[2], sk[3]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (base + u >= n) break;
+                if (a.admitted) a.admitted[base + u] = static_cast<uint8_t>((adm >> (8 * u)) & 1u);
+                if (a.refetch) a.refetch[base + u] = static_cast<uint8_t>((ref >> (8 * u)) & 1u);
+                if (a.skipped) a.skipped[base + u] = sk[u];
+            }
+        }
+        if (a.sel_keys) {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const unsigned mask = __ballot_sync(0xffffffffu, in[u]);
+                if (!mask) continue;
+                const int leader = __ffs(mask) - 1;
+                unsigned bp = 0;
+                if (lane == leader) bp = atomicAdd(&a.s->sel_count, __popc(mask));
+                bp = __shfl_sync(0xffffffffu, bp, leader);
+                if (in[u]) {
+                    const unsigned pos = bp + __popc(mask & ((1u << lane) - 1));
+                    a.sel_keys[pos] = kk[u];
+                    a.sel_idx[pos] = static_cast<int32_t>(base + u);
+                    oh |= kk[u].hi; ol |= kk[u].lo; ah &= kk[u].hi; al &= kk[u].lo;
+                }
             }
         }
     }
@@ -658,6 +836,65 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
         int c = 0;
         for (int r = lane; r < nruns; r += 32)
             if (r != own) c += count_less(rk, ri, r * kRun, min(r * kRun + kRun, m), x, xi);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            const int rank = c + (e - own * kRun);
+            if (out_idx) out_idx[rank] = xi;
+            if (out_keys) out_keys[rank] = x;
+        }
+    }
+}
+
+// The same rank merge with every 16th pair of every run staged in shared
+// memory (m <= kMergeSampled): a lane finds its run's 16-pair window among the
+// samples, then counts inside the window with 15 independent loads -- one
+// L2 latency per lane instead of eight dependent probes.
+constexpr int kMergeStep = 16;
+constexpr int kMergeSampled = 16384;
+__global__ void __launch_bounds__(256) k_run_merge_sampled(const kr_key* rk, const int32_t* ri,
+                                                           const unsigned int* count_dev, int m_host,
+                                                           int32_t* out_idx, kr_key* out_keys) {
+    __shared__ kr_key sk[kMergeSampled / kMergeStep];
+    __shared__ int32_t si[kMergeSampled / kMergeStep];
+    const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
+    const int ns = (m + kMergeStep - 1) / kMergeStep;
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+        sk[j] = rk[j * kMergeStep];
+        si[j] = ri[j * kMergeStep];
+    }
+    __syncthreads();
+    const int nruns = (m + kRun - 1) / kRun;
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    constexpr int kSpr = kRun / kMergeStep;  // samples per run
+    for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < m; e += gridDim.x * wpb) {
+        const kr_key x = rk[e];
+        const int32_t xi = ri[e];
+        const int own = e / kRun;
+        int c = 0;
+        for (int r = lane; r < nruns; r += 32) {
+            if (r == own) continue;
+            const int r0 = r * kRun, len = min(kRun, m - r0);
+            const int nsr = (len + kMergeStep - 1) / kMergeStep;
+            // samples of run r smaller than x
+            int lo = 0, hi = nsr;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (pair_gt(x, xi, sk[r * kSpr + mid], si[r * kSpr + mid])) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo == 0) continue;
+            const int w0 = r0 + (lo - 1) * kMergeStep;  // the last sample below x
+            int cnt = (lo - 1) * kMergeStep + 1;
+#pragma unroll
+            for (int t = 1; t < kMergeStep; t++) {
+                const int q = w0 + t;
+                if (q < r0 + len && q < r0 + lo * kMergeStep)
+                    cnt += pair_gt(x, xi, rk[q], ri[q]) ? 1 : 0;
+            }
+            c += cnt;
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (lane == 0) {
@@ -897,6 +1134,21 @@ __global__ void __launch_bounds__(256) k_rs_scatter(const kr_key* keys, const in
     }
 }
 
+#ifndef KR_ADMIT_VEC
+#define KR_ADMIT_VEC 0  // 1: four requests per thread (k_admit_dig)
+#endif
+#ifndef KR_MERGE_SAMPLED
+#define KR_MERGE_SAMPLED 0  // 1: sample-staged rank merge
+#endif
+// KR_MERGE_UNSAMPLED=1: the plain binary-search merge (A/B measurements).
+static bool merge_unsampled() {
+    static bool v = [] {
+        const char* e = getenv("KR_MERGE_UNSAMPLED");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // Sorts (keys, idx) with n elements (keys/idx may alias workspace buffer 0).
 static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx,
                       const unsigned int* count_dev, int64_t n, int32_t* out_idx, kr_key* out_keys,
@@ -912,8 +1164,15 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
         const int64_t warps = m;
         int64_t blocks = (warps + 7) / 8;
         if (blocks > 148 * 64) blocks = 148 * 64;
-        k_run_merge<<<static_cast<unsigned>(blocks), 256, 0, st>>>(rk, ri, count_dev, m, out_idx,
-                                                                   out_keys);
+        if (KR_MERGE_SAMPLED && m <= kMergeSampled && !merge_unsampled()) {
+            // every CTA stages the samples: a few CTAs per SM, several pairs per warp
+            const int64_t cap = static_cast<int64_t>(device_info().sm_count) * 2;
+            k_run_merge_sampled<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, 0, st>>>(
+                rk, ri, count_dev, m, out_idx, out_keys);
+        }
+        else
+            k_run_merge<<<static_cast<unsigned>(blocks), 256, 0, st>>>(rk, ri, count_dev, m,
+                                                                       out_idx, out_keys);
         return check_launch("run sort", 2);
     }
     // window plan from OR ^ AND of the set (read back: one stream sync)
@@ -1068,31 +1327,38 @@ extern "C" size_t kr_workspace_bytes(int64_t n) { return workspace_bytes(n); }
 
 // Launches the select pipeline (workspace state left holding the level-0
 // k-th key in state->kth).  Returns KR_OK or an error.
+// CTAs per SM of the grid passes: fewer CTAs flush fewer partial histograms
+// (global atomics on up to 2^11 bins) and fence fewer times.
+#ifndef KR_SEL_CPS
+#define KR_SEL_CPS 2
+#endif
+static int sel_ctas_per_sm(int occ) { return KR_SEL_CPS > 0 && KR_SEL_CPS < occ ? KR_SEL_CPS : occ; }
+
+// Launches the select pipeline: state->kth holds the k-th key (and kth_out,
+// when given), w.digits the level-0 digits and state->dstar their boundary bin.
 static int select_pipeline(const kr_key* keys, int64_t n, int64_t k,
                            const unsigned long long* key_stats, const Workspace& w,
-                           cudaStream_t st) {
+                           kr_key* kth_out, cudaStream_t st) {
     SelState* s = w.state;
-    k_sel_reset<<<1, 1024, 0, st>>>(s, n, k, key_stats);
-    int launches = 1;
+    k_sel_reset<<<1, 1024, 0, st>>>(s, n, k, key_stats, keys);
+    int launches = 3;
     if (!key_stats) {
         k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, s);
-        launches++;
+        k_sel_digit<<<1, 1, 0, st>>>(s, keys);
+        launches += 2;
     }
-    // level 0: all keys -> cand[0]; level 1: cand[0] -> cand[1]; finisher reads cand[1]
-    k_sel_hist<<<grid_stream(n), 256, 0, st>>>(keys, s, 0);
-    k_sel_pick<<<1, 1024, 0, st>>>(s, keys, 0);
-    k_sel_scatter<<<grid_stream(n), 256, 0, st>>>(keys, w.cand[0], s, 0);
-    k_sel_hist<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], s, 1);
-    k_sel_pick<<<1, 1024, 0, st>>>(s, w.cand[0], 1);
-    k_sel_scatter<<<grid_stream(n / 64 + 1), 256, 0, st>>>(w.cand[0], w.cand[1], s, 1);
-    k_sel_finish<<<1, 1024, 0, st>>>(s, w.cand[1], w.cand[0], 2);
-    return check_launch("select", launches + 7);
+    static int per_sm_h = sel_ctas_per_sm(occupancy(k_sel_hist0, 256));
+    static int per_sm_s = sel_ctas_per_sm(occupancy(k_sel_scatter0, 256));
+    k_sel_hist0<<<grid_cap(n, 256 * kSelU, per_sm_h), 256, 0, st>>>(keys, n, w.digits, s);
+    k_sel_scatter0<<<grid_cap(n, 256 * kScatW, per_sm_s), 256, 0, st>>>(keys, n, w.digits, w.cand[0],
+                                                                   w.cand[1], s, kth_out);
+    return check_launch("select", launches);
 }
 
 static int admit_with(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
                       const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted,
                       uint8_t* refetch, int32_t* edge_idx, kr_key* edge_keys, const Workspace& w,
-                      cudaStream_t st);
+                      cudaStream_t st, const uint16_t* digits = nullptr);
 
 extern "C" int kr_key_stats_init(unsigned long long* stats, void* stream) {
     if (!stats) return KR_EINVAL;
@@ -1142,10 +1408,7 @@ extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* 
     }
     if (!ws || ws_bytes < workspace_bytes(n) || !keys) return KR_ENOSPACE;
     Workspace w = carve(ws, n);
-    int e = select_pipeline(keys, n, k, key_stats, w, st);
-    if (e) return e;
-    k_copy_kth<<<1, 1, 0, st>>>(w.state, kth);
-    return check_launch("kr_topk_select");
+    return select_pipeline(keys, n, k, key_stats, w, kth, st);
 }
 
 extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
@@ -1191,24 +1454,21 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
         return check_launch("kr_select_admit(small)");
     }
     Workspace w = carve(ws, n);
-    int e = select_pipeline(keys, n, k, key_stats, w, st);
+    int e = select_pipeline(keys, n, k, key_stats, w, kth_out, st);
     if (e) return e;
-    if (kth_out) {
-        k_copy_kth<<<1, 1, 0, st>>>(w.state, kth_out);
-        e = check_launch("kr_select_admit");
-        if (e) return e;
-    }
     return admit_with(keys, n, k, &w.state->kth, fleet, cfg, admitted, refetch, edge_idx,
-                      edge_keys, w, st);
+                      edge_keys, w, st, w.digits);
 }
 
 // Admission pass + (optional) ordered gather of the admitted set.
 static int admit_with(const kr_key* keys, int64_t n, int64_t k, const kr_key* kth,
                       const kr_fleet* fleet, const kr_sched* cfg, uint8_t* admitted,
                       uint8_t* refetch, int32_t* edge_idx, kr_key* edge_keys, const Workspace& w,
-                      cudaStream_t st) {
+                      cudaStream_t st, const uint16_t* digits) {
     const bool gather = edge_idx || edge_keys;
-    if (gather) k_admit_init<<<1, 32, 0, st>>>(w.state);
+    // after a select the gather state was reset by k_sel_reset
+    const bool init = gather && !digits;
+    if (init) k_admit_init<<<1, 32, 0, st>>>(w.state);
     AdmitArgs a{};
     a.keys = keys;
     a.n = n;
@@ -1224,8 +1484,15 @@ static int admit_with(const kr_key* keys, int64_t n, int64_t k, const kr_key* kt
     a.sel_keys = gather ? w.skeys[0] : nullptr;
     a.sel_idx = gather ? w.sidx[0] : nullptr;
     a.s = w.state;
-    k_admit<<<grid_stream(n), 256, 0, st>>>(a);
-    int e = check_launch("k_admit", gather ? 2 : 1);
+    a.digits = digits;
+    if (KR_ADMIT_VEC && digits && kth && k > 0) {
+        static int per_sm = occupancy(k_admit_dig, 256);
+        k_admit_dig<<<grid_cap(n, 256 * 4, per_sm), 256, 0, st>>>(a);
+    } else {
+        static int per_sm = occupancy(k_admit, 256);
+        k_admit<<<grid_cap(n, 256, per_sm), 256, 0, st>>>(a);
+    }
+    int e = check_launch("k_admit", init ? 2 : 1);
     if (e || !gather) return e;
     const int64_t m = k < n ? k : n;
     if (m == 0) return KR_OK;
@@ -1260,7 +1527,7 @@ extern "C" int kr_sort_keys(const kr_key* keys, int64_t n, int32_t* order, kr_ke
     Workspace w = carve(ws, n);
     if (n <= kRunSortMax)
         return sort_pairs(w, keys, nullptr, nullptr, n, order, sorted_keys, nullptr, st);
-    k_sel_reset<<<1, 1024, 0, st>>>(w.state, n, 0, nullptr);
+    k_sel_reset<<<1, 1024, 0, st>>>(w.state, n, 0, nullptr, keys);
     k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, w.state);
     int e = check_launch("kr_sort_keys", 2);
     if (e) return e;

@@ -100,12 +100,8 @@ struct FleetSrc {
     __device__ void hist(int64_t i, int64_t& w, int64_t& t0, int32_t& ne, int64_t& last) const {
         const int64_t* slots = f.slots + 4 * __ldg(f.hist_off + i);
         ne = __ldg(f.n_exec + i);
-        w = total_wait(slots, ne, __ldg(f.n_gen + i));
         t0 = __ldg(f.t_start + i);
-        if (ne > 0) {
-            Slot l = load_slot(slots, ne - 1);
-            last = l.ee - l.es;
-        }
+        history_walk(slots, ne, __ldg(f.n_gen + i), w, last);
     }
     __device__ void waits(int64_t i, int64_t* out) const {
         slot_waits(f.slots + 4 * __ldg(f.hist_off + i), __ldg(f.n_exec + i), __ldg(f.n_gen + i),
@@ -136,15 +132,60 @@ struct LedgerSrc {
     __device__ void waits(int64_t, int64_t*) const {}
 };
 
+// Per-launch constants of the urgency pass, prepared on the host from kr_sched:
+// the aging interval as a multiply-shift divisor and, for an integer control
+// rate, the reciprocal of the round-half-up denominator 2*hz.
+struct UrgConst {
+    FastDiv aging;
+    double rinv;    // 1 / (2 hz)      (fast_time only)
+    int64_t den;    // 2 hz            (fast_time only)
+    int fast_time;  // hz_den == 1 && hz_num < 2^40
+};
+static UrgConst urg_const(const kr_sched& c) {
+    UrgConst u{};
+    u.aging = make_fastdiv(static_cast<uint32_t>(c.aging_interval));
+    u.fast_time = c.hz_den == 1 && c.hz_num < (int64_t(1) << 40);
+    u.den = 2 * c.hz_num;
+    u.rinv = 1.0 / static_cast<double>(u.den);
+    return u;
+}
+
+// us_from_actions for an int32 action count: the integer-hz branch's
+// (2*count*10^6 + hz) / (2 hz) via the fp64 reciprocal and one exact integer
+// correction (the numerator is below 2^53, the estimate within one of the
+// quotient); otherwise the general __int128 path.
+__device__ __forceinline__ int64_t us_from_actions32(int32_t count, const kr_sched& c,
+                                                     const UrgConst& u, uint32_t* flag_bits) {
+    if (!u.fast_time || count < 0) return us_from_actions(count, c.hz_num, c.hz_den, flag_bits);
+    const int64_t num = static_cast<int64_t>(count) * 2000000 + c.hz_num;
+    int64_t q = static_cast<int64_t>(__dmul_rn(static_cast<double>(num), u.rinv));
+    const int64_t r = num - q * u.den;
+    q += r < 0 ? -1 : (r >= u.den ? 1 : 0);
+    return q;
+}
+
+// assign_bucket (scheduler.py:79-88) with the aging division by multiply-shift
+// (skipped >= A >= 1 here, so the dividend is a non-negative int32).
+__device__ __forceinline__ int32_t assign_bucket32(double wr, int32_t skipped, int32_t B, int32_t A,
+                                                   const FastDiv& fa) {
+    int32_t b = static_cast<int32_t>(floor(dmul(wr, static_cast<double>(B))));
+    if (b > B - 1) b = B - 1;
+    if (skipped >= A) {
+        b = b + static_cast<int32_t>(fdiv(static_cast<uint32_t>(skipped), fa));
+        if (b > B - 1) b = B - 1;
+    }
+    return b;
+}
+
 // One request: its packed key (and the optional intermediates / need time).
 template <class Src>
-__device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, const UrgencyOut& o,
-                                              int64_t i, uint32_t& fl) {
+__device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, const UrgConst& u,
+                                              const UrgencyOut& o, int64_t i, uint32_t& fl) {
     const int64_t issued = s.issued(i);
     const int32_t rank = s.rank(i);
     if (o.need_time) {
         int32_t rem = s.remaining(i);
-        o.need_time[i] = issued + us_from_actions(rem, c.hz_num, c.hz_den, &fl);
+        o.need_time[i] = issued + us_from_actions32(rem, c, u, &fl);
     }
     kr_key key;
     if (c.policy == KR_FIFO) {
@@ -163,7 +204,7 @@ __device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, c
         int32_t ne;
         s.hist(i, w, t0, ne, last);
         double wr = wait_ratio(w, t0, c.now, &fl);
-        int32_t b = assign_bucket(wr, skipped, c.buckets, c.aging_interval);
+        int32_t b = assign_bucket32(wr, skipped, c.buckets, c.aging_interval, u.aging);
         const int64_t est = ne > 0 ? last : c.default_exec_estimate;
         if (o.total_wait) o.total_wait[i] = w;
         if (o.wr) o.wr[i] = wr;
@@ -172,11 +213,22 @@ __device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, c
         if constexpr (Src::kSlots)
             if (o.slot_wait) s.waits(i, o.slot_wait);
         if (c.policy == KR_KAIROS) {
-            // aged = est * (1 + skipped), descending -> stored complemented
-            unsigned __int128 aged = static_cast<unsigned __int128>(est < 0 ? 0 : est) *
-                                     static_cast<unsigned __int128>(1 + (int64_t)skipped);
-            if (est < 0 || skipped < 0 || aged > kAgedMask) fl |= KR_FLAG_KEY_RANGE;
-            uint64_t a = aged > kAgedMask ? kAgedMask : static_cast<uint64_t>(aged);
+            // aged = est * (1 + skipped), descending -> stored complemented;
+            // clamped at 2^56 - 1 (the 128-bit product of the original
+            // formulation: a negative multiplier wraps to a huge value)
+            const uint64_t e = est < 0 ? 0 : static_cast<uint64_t>(est);
+            const int64_t m = 1 + static_cast<int64_t>(skipped);
+            bool over;
+            uint64_t a;
+            if (m >= 0) {
+                const uint64_t lo = e * static_cast<uint64_t>(m);
+                over = __umul64hi(e, static_cast<uint64_t>(m)) != 0 || lo > kAgedMask;
+                a = over ? kAgedMask : lo;
+            } else {
+                over = e != 0;
+                a = over ? kAgedMask : 0;
+            }
+            if (est < 0 || skipped < 0 || over) fl |= KR_FLAG_KEY_RANGE;
             key.hi = (static_cast<uint64_t>(c.buckets - 1 - b) << 56) | (kAgedMask - a);
             key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
         }
@@ -184,13 +236,17 @@ __device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, c
     return key;
 }
 
-template <class Src>
-__global__ void __launch_bounds__(256) k_urgency(Src s, kr_sched c, UrgencyOut o) {
+#ifndef KR_URG_MINB
+#define KR_URG_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
+template <class Src, class Idx>
+__global__ void __launch_bounds__(256, KR_URG_MINB) k_urgency(Src s, kr_sched c, UrgConst u,
+                                                              UrgencyOut o) {
     uint32_t fl = 0;
     unsigned long long ohi = 0, olo = 0, ahi = ~0ull, alo = ~0ull;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < s.n();
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const kr_key key = urgency_one(s, c, o, i, fl);
+    const Idx n = static_cast<Idx>(s.n());
+    for (Idx i = blockIdx.x * Idx(blockDim.x) + threadIdx.x; i < n; i += Idx(gridDim.x) * blockDim.x) {
+        const kr_key key = urgency_one(s, c, u, o, i, fl);
         o.keys[i] = key;
         ohi |= key.hi; olo |= key.lo; ahi &= key.hi; alo &= key.lo;
     }
@@ -221,6 +277,22 @@ static unsigned grid_for(int64_t n, int threads) {
     int64_t cap = static_cast<int64_t>(device_info().sm_count) * 8;
     if (b > cap) b = cap;
     return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+// Persistent grid: every CTA resident at once (SMs x occupancy), each thread
+// looping over several requests so the block-level key statistics amortise;
+// 32-bit indices below 2^31 requests.
+template <class Src>
+static void launch_urgency(const Src& src, int64_t n, const kr_sched& c, const UrgencyOut& o,
+                           cudaStream_t st) {
+    const UrgConst u = urg_const(c);
+    if (n < (int64_t(1) << 31)) {
+        static int per_sm = occupancy(k_urgency<Src, int32_t>, 256);
+        k_urgency<Src, int32_t><<<grid_cap(n, 256, per_sm), 256, 0, st>>>(src, c, u, o);
+    } else {
+        static int per_sm = occupancy(k_urgency<Src, int64_t>, 256);
+        k_urgency<Src, int64_t><<<grid_cap(n, 256, per_sm), 256, 0, st>>>(src, c, u, o);
+    }
 }
 
 }  // namespace kr
@@ -270,7 +342,7 @@ extern "C" int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* ke
     if (fleet->n == 0) return KR_OK;
     if (!keys) return KR_EINVAL;
     UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, slot_wait, key_stats, flags};
-    k_urgency<<<grid_for(fleet->n, 256), 256, 0, as_stream(stream)>>>(FleetSrc{*fleet}, *cfg, o);
+    launch_urgency(FleetSrc{*fleet}, fleet->n, *cfg, o, as_stream(stream));
     return check_launch("kr_urgency");
 }
 
@@ -285,8 +357,7 @@ extern "C" int kr_urgency_ledger(const kr_ledger* ledger, const kr_requests* req
     if (req->n == 0) return KR_OK;
     if (!keys || !req->task) return KR_EINVAL;
     UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, nullptr, key_stats, flags};
-    k_urgency<<<grid_for(req->n, 256), 256, 0, as_stream(stream)>>>(LedgerSrc{*ledger, *req},
-                                                                     *cfg, o);
+    launch_urgency(LedgerSrc{*ledger, *req}, req->n, *cfg, o, as_stream(stream));
     return check_launch("kr_urgency_ledger");
 }
 
@@ -393,8 +464,8 @@ __device__ __forceinline__ bool pair_less(const kr_key& a, int ia, const kr_key&
     return ia < ib;
 }
 
-__global__ void __launch_bounds__(1024) k_plan_small(kr_fleet f, kr_sched c, int n, int P, int k,
-                                                     int32_t* out) {
+__global__ void __launch_bounds__(1024) k_plan_small(kr_fleet f, kr_sched c, UrgConst u, int n,
+                                                     int P, int k, int32_t* out) {
     extern __shared__ __align__(16) unsigned char sm[];
     kr_key* keys = reinterpret_cast<kr_key*>(sm);
     int* idx = reinterpret_cast<int*>(keys + P);
@@ -407,7 +478,7 @@ __global__ void __launch_bounds__(1024) k_plan_small(kr_fleet f, kr_sched c, int
     uint32_t fl = 0;
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
         kr_key key{~0ull, ~0ull};
-        if (i < n) key = urgency_one(s, c, none, i, fl);
+        if (i < n) key = urgency_one(s, c, u, none, i, fl);
         keys[i] = key;
         idx[i] = i;
     }
@@ -462,7 +533,7 @@ extern "C" int kr_plan_small(const kr_fleet* fleet, const kr_sched* cfg, int64_t
             attr = true;
         }
     }
-    k_plan_small<<<1, threads, smem, as_stream(stream)>>>(*fleet, *cfg, n, P,
+    k_plan_small<<<1, threads, smem, as_stream(stream)>>>(*fleet, *cfg, urg_const(*cfg), n, P,
                                                          static_cast<int>(k < n ? k : n), out);
     return check_launch("kr_plan_small");
 }

@@ -73,6 +73,10 @@ def _skewed(n, rng, mode):
     if mode == "dense_low_bin":      # > kSegMax admitted keys share the level-0 bin
         hi = np.where(rng.random(n) < 0.7, 0, rng.integers(1, 1 << 11, n)).astype(np.uint64) << np.uint64(40)
         lo = (rng.integers(0, 1 << 30, n, dtype=np.uint64) << np.uint64(24)) | np.arange(n, dtype=np.uint64)
+    elif mode == "one_outlier":      # the top digit separates one key: the boundary bin
+        hi = np.zeros(n, np.uint64)  # holds all others (the single-CTA finish does the rest)
+        hi[n // 2] = np.uint64(1) << np.uint64(63)
+        lo = (rng.integers(0, 1 << 30, n, dtype=np.uint64) << np.uint64(24)) | np.arange(n, dtype=np.uint64)
     elif mode == "few_bits":         # only rank bits differ
         hi = np.zeros(n, np.uint64)
         lo = rng.permutation(n).astype(np.uint64)
@@ -90,7 +94,9 @@ def _skewed(n, rng, mode):
                                       (1024, 64, "kairos"), (4096, 4095, "few_bits"),
                                       (4097, 4000, "kairos"), (12000, 1024, "kairos"),
                                       (16384, 16383, "few_bits"), (16384, 1, "kairos"),
-                                      (16385, 1024, "kairos"), (9000, 4500, "dense_low_bin")])
+                                      (16385, 1024, "kairos"), (9000, 4500, "dense_low_bin"),
+                                      (300000, 1000, "one_outlier"), (1 << 18, (1 << 18) - 1,
+                                                                       "one_outlier")])
 def test_select_admit_fused(n, k, mode):
     from paper_2605_11381_b200 import fleet as fl
     rng = np.random.default_rng(n + k)

@@ -336,8 +336,10 @@ def run_ours(args, world, rank, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    graphs = world == 1 and not args.no_graph and not args.eager and not args.force_sharded
-    # N > 1 (or --eager): the same overlap eagerly (the NCCL all-gather stays outside graphs)
+    # CUDA graphs at every N: the sharded round's NCCL all-gather is captured
+    # inside the admission graph (rounds.ShardedDecisionRound.capture)
+    graphs = not args.no_graph and not args.eager
+    # --eager: the same overlap with eager launches
     overlap = not graphs and args.reserve_sms > 0 and not args.no_graph
     n_cap0 = lib.kr_launch_count()
     if graphs:

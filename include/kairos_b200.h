@@ -27,6 +27,8 @@
  *   kr_trace_parse / _load  workload.py:163-262  JSONL task traces -> columns (host code)
  *   kr_transfer_time        engines.py:158-169   per-request uplink time
  *   kr_place_cloud          scheduler.py:160-234 phase-3 cloud offload scan
+ *   kr_apply_placements     scheduler.py:223-234 a sharded round's cloud placements on
+ *                           their owning shard (skip counter reset, refetch flag)
  *
  * Conventions: every pointer argument that names device data is a device
  * pointer; kr_fleet / kr_sched structs themselves live in host memory.  All
@@ -319,6 +321,17 @@ KR_API int kr_place_cloud(const int32_t* order, int64_t n, int64_t n_edge, const
                           const int64_t* thresholds, int64_t cap, const kr_fleet* fleet,
                           const kr_sched* cfg, uint8_t* refetch, int32_t* cloud_idx,
                           int32_t* n_cloud, void* stream);
+
+/* scheduler.py:223-234 for a robot-sharded round's offload set: pos[i] for
+ * i < *n_placed (device count, e.g. kr_place_cloud's n_cloud) are positions in
+ * the all-gathered candidate runs of length run_len; those in run `rank` (this
+ * shard) name local robot cand_idx[pos % run_len], whose skip counter is reset
+ * and refetch flag set (now - obs_captured_at > stale_threshold).  No host
+ * synchronisation: the count stays on the device. */
+KR_API int kr_apply_placements(const int32_t* pos, const int32_t* n_placed, int64_t cap,
+                               int64_t run_len, int32_t rank, const int32_t* cand_idx,
+                               const kr_fleet* fleet, const kr_sched* cfg, uint8_t* refetch,
+                               void* stream);
 
 /* ---- trace ingest (host code): JSON Lines task traces -> columns -------- */
 

@@ -148,6 +148,9 @@ _SIGNATURES = {
     "kr_get_dot_order": (_i32, []),
     "kr_place_cloud": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _i64, ctypes.POINTER(KrFleet),
                                       ctypes.POINTER(KrSched), _vp, _vp, _vp, _vp]),
+    "kr_apply_placements": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i32, _vp,
+                                           ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _vp,
+                                           _vp]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

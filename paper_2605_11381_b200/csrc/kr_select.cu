@@ -1312,6 +1312,21 @@ __global__ void __launch_bounds__(1024) k_place_cloud(const int32_t* order, int 
     if (tid == 0) *n_cloud = s_c;
 }
 
+// scheduler.py:223-234 applied on the owning shard (kr_apply_placements).
+__global__ void k_apply_placements(const int32_t* pos, const int32_t* n_placed, int cap,
+                                   int64_t run_len, int rank, const int32_t* cand_idx,
+                                   const int64_t* obs, int32_t* skipped, uint8_t* refetch,
+                                   int64_t now, int64_t stale) {
+    const int n = min(*n_placed, cap);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t p = pos[i];
+        if (p / run_len != rank) continue;
+        const int32_t r = cand_idx[p % run_len];
+        if (skipped) skipped[r] = 0;
+        if (refetch) refetch[r] = now - obs[r] > stale;
+    }
+}
+
 static unsigned grid_stream(int64_t n) {
     int64_t b = (n + 255) / 256;
     int64_t cap = static_cast<int64_t>(device_info().sm_count) * 8;
@@ -1563,4 +1578,18 @@ extern "C" int kr_place_cloud(const int32_t* order, int64_t n, int64_t n_edge,
                                       cfg ? cfg->now : 0, cfg ? cfg->stale_threshold : 0,
                                       cloud_idx, n_cloud);
     return check_launch("kr_place_cloud");
+}
+
+extern "C" int kr_apply_placements(const int32_t* pos, const int32_t* n_placed, int64_t cap,
+                                   int64_t run_len, int32_t rank, const int32_t* cand_idx,
+                                   const kr_fleet* fleet, const kr_sched* cfg, uint8_t* refetch,
+                                   void* stream) {
+    if (cap < 0 || cap > INT32_MAX || run_len < 1 || rank < 0 || !n_placed) return KR_EINVAL;
+    if (cap == 0) return KR_OK;
+    if (!pos || !cand_idx || !fleet || (refetch && !cfg)) return KR_EINVAL;
+    const int blocks = static_cast<int>((cap + 255) / 256);
+    k_apply_placements<<<blocks, 256, 0, as_stream(stream)>>>(
+        pos, n_placed, static_cast<int>(cap), run_len, rank, cand_idx, fleet->obs_captured_at,
+        fleet->skipped, refetch, cfg ? cfg->now : 0, cfg ? cfg->stale_threshold : 0);
+    return check_launch("kr_apply_placements");
 }

@@ -276,8 +276,9 @@ class DecisionRound:
         of candidates, global select, local admission) on a side stream
         concurrently -- preceded on the current stream by the urgency pass
         ("urgency_first") or running it on the side stream too ("split"); the
-        current stream joins the side stream at the end.  The sharded round's
-        collective runs here because NCCL work stays outside CUDA graphs."""
+        current stream joins the side stream at the end.  (A sharded round over
+        NCCL is captured too -- `capture` -- with the all-gather inside the
+        admission graph; over gloo it runs here.)"""
         n_sm = torch.cuda.get_device_properties(self.H.device).multi_processor_count
         self.max_sms = 0 if reserve_sms <= 0 else max(1, n_sm - reserve_sms)
         if getattr(self, "side", None) is None:
@@ -502,6 +503,19 @@ class ShardedDecisionRound(DecisionRound):
         sharded_topk(self.keys, self.R, self.k_request, self.sizes, CudaShardOps(self, fleet),
                      self.group)
 
+    def capture(self, fleet: fl.DeviceFleet, h, reserve_sms: int = 0,
+                layout: str = "split") -> None:
+        """CUDA graphs of the sharded round (see DecisionRound.capture): the
+        NCCL all-gather of the candidates is captured inside the admission
+        graph -- every op of the protocol works on preallocated buffers with
+        no host synchronisation -- so a replay is one enqueue per graph.  The
+        warm-up round inside DecisionRound.capture initialises the
+        communicator before capture.  NCCL only: gloo collectives run on the
+        host (use run / run_overlapped)."""
+        if dist.get_backend(self.group) != "nccl":
+            raise RuntimeError("a sharded round is captured only over NCCL (gloo runs eagerly)")
+        super().capture(fleet, h, reserve_sms=reserve_sms, layout=layout)
+
     def outputs(self) -> RoundOutputs:
         return RoundOutputs(self.H, self.need_time, self.keys, self.admitted, self.refetch,
                             self.global_edge[: self.k_global], None, self.kth_global)
@@ -544,90 +558,95 @@ class ShardedHybridRound(ShardedDecisionRound):
         self.up_us = up_us
         self.thresholds = thr.to(up_us.device)
 
-    def _gather(self, t: torch.Tensor) -> torch.Tensor:
-        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype,
-                          device=t.device)
+    def _gather(self, t: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         if dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(out, t, group=self.group)
         else:  # gloo (tests: several ranks sharing one device)
             dist.all_gather(list(out.chunk(self.world)), t, group=self.group)
         return out
 
-    def _candidates(self, kg2: int):
+    def _buffers(self, kg2: int) -> dict:
+        """Per-window device buffers, allocated once per window size (the
+        steady state never allocates: the window only widens, rarely)."""
+        if getattr(self, "_buf_kg2", None) != kg2:
+            d, n = self.H.device, max(kg2, 1)
+            self._buf = {
+                "cand_keys": fl.new_keys(n, d),
+                "cand_idx": torch.zeros(n, dtype=torch.int32, device=d),
+                "cand_up": torch.zeros(n, dtype=torch.int64, device=d),
+                "g_keys": fl.new_keys(n * self.world, d),
+                "g_up": torch.zeros(n * self.world, dtype=torch.int64, device=d),
+                "merged": fl.new_keys(n, d),
+                "pos": torch.empty(n, dtype=torch.int32, device=d),
+                "cloud_pos": torch.zeros(max(self.cap, 1), dtype=torch.int32, device=d),
+                "n_cloud": torch.zeros(1, dtype=torch.int32, device=d),
+            }
+            self._buf_kg2 = kg2
+        return self._buf
+
+    def _candidates(self, kg2: int, b: dict) -> None:
         """This shard's ordered top min(kg2, R) keys (sentinel-padded to kg2),
         their local indices and uplink times; no side effects."""
-        d = self.H.device
         kl2 = min(kg2, self.R)
-        cand_keys = fl.new_keys(kg2, d)
-        cand_keys.fill_(ALL_ONES)
-        cand_idx = torch.zeros(kg2, dtype=torch.int32, device=d)
-        cand_up = torch.zeros(kg2, dtype=torch.int64, device=d)
+        b["cand_keys"].fill_(ALL_ONES)
         if kl2 > 0:
             fl.select_admit(self.keys, kl2, self.ws, key_stats=self.key_stats,
-                            edge_idx=cand_idx, edge_keys=cand_keys)
+                            edge_idx=b["cand_idx"], edge_keys=b["cand_keys"])
             if self.cap > 0:
-                cand_up[:kl2] = self.up_us[cand_idx[:kl2].long()]
-        return cand_keys, cand_idx, cand_up
+                torch.index_select(self.up_us, 0, b["cand_idx"][:kl2], out=b["cand_up"][:kl2])
 
     def admit(self, fleet: fl.DeviceFleet) -> None:
         """One select, one all-gather of (key, uplink) candidates and one merge
         serve both tiers: the merged first k_global ranks are the global S_e
         (edge admission by the k-th key, as in the edge-only protocol), the
-        following ranks feed the offload scan."""
+        following ranks feed the offload scan.  Preallocated buffers; the one
+        host read is the offload count, deciding whether the window must widen
+        (the same decision on every rank)."""
         if self.cap > 0 and self.up_us is None:
             raise RuntimeError("set_cloud() first: the round has a cloud tier")
-        d, st = self.H.device, dev.stream()
+        st = dev.stream()
         kg = self.k_global
         window = self.window if self.cap > 0 else 0
         edge_done = False
         self.n_cloud = 0
         while True:
             kg2 = min(kg + window, self.total)
-            cand_keys, cand_idx, cand_up = self._candidates(kg2)
-            g_keys = self._gather(cand_keys)
-            g_up = self._gather(cand_up) if self.cap > 0 else None
-            merged = fl.new_keys(max(kg2, 1), d)
-            pos = torch.empty(max(kg2, 1), dtype=torch.int32, device=d)
+            b = self._buffers(kg2)
+            self._candidates(kg2, b)
+            g_keys = self._gather(b["cand_keys"][:max(kg2, 1)], b["g_keys"])
+            g_up = self._gather(b["cand_up"][:max(kg2, 1)], b["g_up"]) if self.cap > 0 else None
             if kg2 > 0:
                 _lib.check(self.lib.kr_merge_runs_pos(g_keys.data_ptr(), self.world, kg2, kg2,
-                                                      merged.data_ptr(), pos.data_ptr(), None,
-                                                      self.flags.data_ptr(), st),
+                                                      b["merged"].data_ptr(), b["pos"].data_ptr(),
+                                                      None, self.flags.data_ptr(), st),
                            "kr_merge_runs_pos")
             if not edge_done:  # global S_e and the local edge admission
                 if kg > 0:
-                    self.global_edge[:kg] = merged[:kg]
-                    self.kth_global.copy_(merged[kg - 1: kg])
+                    self.global_edge[:kg].copy_(b["merged"][:kg])
+                    self.kth_global.copy_(b["merged"][kg - 1: kg])
                 kth = self.kth_global if 0 < kg < self.total else None
                 CudaShardOps(self, fleet).apply(self.keys, kg, kth)
                 edge_done = True
             if self.cap == 0:
                 return
-            cloud_pos = torch.empty(self.cap, dtype=torch.int32, device=d)
-            n_t = torch.zeros(1, dtype=torch.int32, device=d)
             _lib.check(self.lib.kr_place_cloud(
-                pos.data_ptr(), kg2, kg, g_up.data_ptr(), self.thresholds.data_ptr(),
-                self.cap, None, None, None, cloud_pos.data_ptr(), n_t.data_ptr(), st),
-                "kr_place_cloud")
-            n = int(n_t.item())
+                b["pos"].data_ptr(), kg2, kg, g_up.data_ptr(), self.thresholds.data_ptr(),
+                self.cap, None, None, None, b["cloud_pos"].data_ptr(), b["n_cloud"].data_ptr(),
+                st), "kr_place_cloud")
+            n = int(b["n_cloud"].item())
             if n == self.cap or kg2 == self.total:
                 break
             window *= 4
             self.widened += 1
         self.n_cloud = n
-        placed = cloud_pos[:n].long()
-        self.cloud_keys[:n] = g_keys[placed]
-        mine = placed[(placed // kg2) == self.rank] % kg2
-        m = int(mine.numel())
-        if m:  # this shard's placements: skip reset + refetch (kr_place_cloud, all qualify)
-            local = cand_idx[mine].contiguous()
-            zeros = torch.zeros(self.R, dtype=torch.int64, device=d)  # indexed by robot
-            big = torch.full((m,), (1 << 63) - 1, dtype=torch.int64, device=d)
-            out = torch.empty(m, dtype=torch.int32, device=d)
-            fs = fleet.c_struct()
-            _lib.check(self.lib.kr_place_cloud(
-                local.data_ptr(), m, 0, zeros.data_ptr(), big.data_ptr(), m, ctypes.byref(fs),
-                ctypes.byref(self.sched), self.refetch.data_ptr(), out.data_ptr(),
-                n_t.data_ptr(), st), "kr_place_cloud(apply)")
+        # offload order as keys (entries past n are never read), and this
+        # shard's placements applied on the device (skip reset + refetch)
+        torch.index_select(g_keys, 0, b["cloud_pos"].long(), out=self.cloud_keys)
+        fs = fleet.c_struct()
+        _lib.check(self.lib.kr_apply_placements(
+            b["cloud_pos"].data_ptr(), b["n_cloud"].data_ptr(), self.cap, kg2, self.rank,
+            b["cand_idx"].data_ptr(), ctypes.byref(fs), ctypes.byref(self.sched),
+            self.refetch.data_ptr(), st), "kr_apply_placements")
 
     def cloud(self) -> torch.Tensor:
         """The global offload set as keys, in offload order (same on every rank)."""

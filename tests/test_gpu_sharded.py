@@ -164,3 +164,66 @@ def test_sharded_duplicate_keys_flagged():
         assert p.exitcode == 0
     assert sum("same priority key" in m for _, m in msgs) == 2
     assert sum("same kr_sched" in m for _, m in msgs) == 2
+
+
+def _nccl_capture_worker(port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+        R, k = 50_000, 4096
+        soa = synthetic.fleet_soa(R, seed=31)
+        fleet = fl.DeviceFleet.from_host(soa)
+        sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                                int(soa["issued_at"].min()))
+        prev, cand, off = synthetic.chunks(R, seed=32)
+        inputs = rounds.DivergenceInputs(prev, cand, 0.9, offset=off)
+        rnd = rounds.ShardedDecisionRound(R, k, sched)
+        skipped0 = fleet.t["skipped"].clone()
+        rnd.capture(fleet, inputs, reserve_sms=10, layout="split")
+        outs = []
+        for _ in range(3):  # capture() ran one (warm-up) round; replay three more
+            rnd.replay()
+            torch.cuda.synchronize()
+            outs.append((rnd.admitted.cpu().numpy(), fleet.t["skipped"].cpu().numpy().copy(),
+                         rnd.global_edge[: rnd.k_global].cpu().numpy(), rnd.H.cpu().numpy()))
+        rnd.check()
+        q.put((skipped0.cpu().numpy(), outs, None))
+    except Exception as e:  # noqa: BLE001
+        q.put((None, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_round_captured_over_nccl():
+    """The sharded round captured in CUDA graphs with the NCCL all-gather
+    inside (one rank): every replayed round == the oracle's plan on the evolving
+    skip counters, horizons == the oracle's."""
+    from paper_2605_11381_b200 import synthetic
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_capture_worker, args=(_port(), q))
+    p.start()
+    skipped0, outs, err = q.get(timeout=600)
+    p.join(timeout=60)
+    assert err is None, err
+    R, k = 50_000, 4096
+    soa = synthetic.fleet_soa(R, seed=31)
+    prev, cand, off = synthetic.chunks(R, seed=32)
+    H = orc.divergence_batch(prev.cpu().numpy(), cand.cpu().numpy(), 0.9, off.cpu().numpy())
+    # capture() runs one eager warm-up round (recording executes nothing);
+    # replay i sees the skip counters after 1 + i rounds
+    cur = dict(soa)
+    cur["skipped"] = skipped0.copy()
+    for _ in range(1):
+        res = orc.plan_soa(cur, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+        cur["skipped"] = res["skipped_out"]
+    for adm, sk, edge, h in outs:
+        res = orc.plan_soa(cur, "kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+        assert np.array_equal(adm, res["admitted"])
+        assert np.array_equal(sk, res["skipped_out"])
+        assert np.array_equal(h, H)
+        cur["skipped"] = res["skipped_out"]
+        del edge

@@ -342,11 +342,17 @@ def run_ours(args, world, rank, local_rank):
     # --eager: the same overlap with eager launches
     overlap = not graphs and args.reserve_sms > 0 and not args.no_graph
     n_cap0 = lib.kr_launch_count()
+    capture_error = None
     if graphs:
         # CUDA graphs: horizons | urgency + admission, the latter on a side
         # stream over `reserve_sms` SMs left free by the horizon kernel
-        rnd.capture(fleet, inputs, reserve_sms=args.reserve_sms, layout=args.layout)
-        per_round = (lib.kr_launch_count() - n_cap0) // 2  # warm-up run + capture
+        try:
+            rnd.capture(fleet, inputs, reserve_sms=args.reserve_sms, layout=args.layout)
+            per_round = (lib.kr_launch_count() - n_cap0) // 2  # warm-up run + capture
+        except Exception as e:  # noqa: BLE001 -- a capture failure falls back to eager launches
+            capture_error = f"{type(e).__name__}: {e}"[:200]
+            torch.cuda.synchronize()
+            graphs, overlap = False, args.reserve_sms > 0
     for _ in range(args.warmup):
         if graphs:
             rnd.replay()
@@ -439,7 +445,7 @@ def run_ours(args, world, rank, local_rank):
         "round_roofline": round_roofline(soa, R, elapsed / args.steps, peak),
         "kernels": breakdown,
         "gpu_launches": int(launches),
-        "cuda_graphs": bool(graphs),
+        "cuda_graphs": bool(graphs) if capture_error is None else f"capture failed ({capture_error}); eager",
         "concurrency": ((f"urgency on the whole GPU, then " if args.layout == "urgency_first" else "")
                         + f"{'admission' if args.layout == 'urgency_first' else 'urgency + admission'}"
                         f"{' + NCCL candidate all-gather' if world > 1 else ''} on a side stream over "
@@ -662,7 +668,7 @@ def run_e2e(args, world, soa, prev, cand, off, sched):
     from paper_2605_11381_b200 import fleet as fl, rounds
 
     R = args.robots
-    graphs = world == 1 and not args.no_graph
+    graphs = not args.no_graph  # the sharded round's NCCL all-gather is captured too
     rnd = (rounds.ShardedDecisionRound(R, args.k, sched) if world > 1
            else rounds.DecisionRound(R, args.k, sched))
     outs = {"H": torch.empty(R, dtype=torch.int32).pin_memory(),
@@ -705,16 +711,20 @@ def run_e2e(args, world, soa, prev, cand, off, sched):
     if graphs:
         rnd.run(views[0], inp6[0][0])
         torch.cuda.synchronize()
-        g_h = [[torch.cuda.CUDAGraph() for _ in range(2)] for _ in range(3)]
-        for a in range(3):
+        try:
+            g_h = [[torch.cuda.CUDAGraph() for _ in range(2)] for _ in range(3)]
+            for a in range(3):
+                for si in range(2):
+                    with torch.cuda.graph(g_h[a][si]):
+                        rnd.horizons(inp6[a][si])
+            g_d = [torch.cuda.CUDAGraph() for _ in range(2)]
             for si in range(2):
-                with torch.cuda.graph(g_h[a][si]):
-                    rnd.horizons(inp6[a][si])
-        g_d = [torch.cuda.CUDAGraph() for _ in range(2)]
-        for si in range(2):
-            with torch.cuda.graph(g_d[si]):
-                rnd.urgency(views[si])
-                rnd.admit(views[si])
+                with torch.cuda.graph(g_d[si]):
+                    rnd.urgency(views[si])
+                    rnd.admit(views[si])
+        except Exception:  # noqa: BLE001 -- capture failure: eager launches
+            torch.cuda.synchronize()
+            graphs = False
     cs = torch.cuda.current_stream()
     xs = torch.cuda.Stream()
 

@@ -73,6 +73,7 @@ extern "C" int kr_horizon_sweep(const void* U, int dtype, int64_t R, int32_t K, 
     cfg.lut_hi = f32 ? 0xFFFFFFFFull : ~uint64_t(0);  // above the largest ratio pattern
     cfg.lut_shift = f32 ? 31 : 63;
     cfg.lut[0] = 0xFFFF;
+    bool table = false;
     if (Cc > 0 && std::isnormal(cfg.rl[0]) && std::isfinite(cfg.rh[Cc - 1]) &&
         (!f32 || (cfg.rl[0] > 1e-37 && cfg.rh[Cc - 1] < 1e37))) {
         int e_lo, e_hi;
@@ -96,18 +97,40 @@ extern "C" int kr_horizon_sweep(const void* U, int dtype, int64_t R, int32_t K, 
             };
             cfg.lut_lo = bits_of(lo);
             cfg.lut_hi = bits_of(hi);
+            table = true;
+            // both counts are monotone in the bucket (rh, rl ascending): two pointers
+            int a = 0, nb = 0;
             for (int bkt = 0; bkt < cfg.lut_n; bkt++) {
                 const uint64_t b0 = cfg.lut_lo + (static_cast<uint64_t>(bkt) << cfg.lut_shift);
                 const double x0 = val_of(b0);
                 const double x1 = val_of(b0 + (uint64_t(1) << cfg.lut_shift) - 1);  // largest in bucket
-                int a = 0, nb = 0;
-                for (int i = 0; i < Cc; i++) {
-                    a += cfg.rh[i] < x0;    // every ratio in the bucket is a definite trip
-                    nb += cfg.rl[i] <= x1;  // some ratio in the bucket is not a definite non-trip
-                }
+                while (a < Cc && cfg.rh[a] < x0) a++;    // every ratio in the bucket is a definite trip
+                while (nb < Cc && cfg.rl[nb] <= x1) nb++;  // some ratio is not a definite non-trip
                 cfg.lut[bkt] = a == nb ? static_cast<uint16_t>(a) : uint16_t(0xFFFF);
             }
         }
+    }
+    // segmented kernel: the ratio is clamped to [clamp_lo, clamp_hi] so that
+    // (bits(ratio) - clamp_base) >> lut_shift indexes [below, table, above]
+    if (table) {
+        const uint64_t step = uint64_t(1) << cfg.lut_shift;
+        cfg.clamp_base = cfg.lut_lo - step;
+        if (f32) {
+            const uint32_t lo32 = static_cast<uint32_t>(cfg.clamp_base), hi32 = static_cast<uint32_t>(cfg.lut_hi);
+            float a, b;
+            std::memcpy(&a, &lo32, 4); std::memcpy(&b, &hi32, 4);
+            cfg.clamp_lo = a; cfg.clamp_hi = b;
+        } else {
+            std::memcpy(&cfg.clamp_lo, &cfg.clamp_base, 8);
+            std::memcpy(&cfg.clamp_hi, &cfg.lut_hi, 8);
+        }
+        cfg.lut_below = 0;
+        cfg.lut_above = static_cast<uint16_t>(Cc);
+    } else {  // no table: every ratio lands on an undecided entry
+        cfg.clamp_base = 0;
+        cfg.clamp_lo = 0.0;
+        cfg.clamp_hi = INFINITY;
+        cfg.lut_below = cfg.lut_above = 0xFFFF;
     }
     for (int i = 0; i < C; i++) {
         const int c = order[i];

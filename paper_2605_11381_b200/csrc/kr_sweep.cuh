@@ -3,6 +3,7 @@
 // streaming pass.  Device code and the per-dtype
 // launcher; the C entry point is kr_sweep.cu.
 #pragma once
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -29,8 +30,11 @@ namespace kr {
 // binary search over the sorted factors with the K1 margins, and the
 // bit-exact fp64 mean when the margins cannot decide).
 //
-// A warp owns one robot at a time (lane = VC adjacent columns, chunks of
-// 32 * VC columns).  With M_n = max_{n' <= n} j_n' (a warp max-scan carried
+// Two layouts: the segmented kernel (SweepSeg, below: G lanes per robot, each
+// deciding a register-resident window of columns) for 16 <= N <= 512 where
+// its windows do not collide in shared-memory banks, and otherwise the
+// warp-per-robot kernel (SweepWork): a warp owns one robot at a time (lane =
+// VC adjacent columns, chunks of 32 * VC columns).  With M_n = max_{n' <= n} j_n' (a warp max-scan carried
 // across chunks), configuration c's horizon is the first n with M_n > c, so
 // the column where M steps from a to b is the horizon of exactly the
 // configurations [a, b) -- one lane per step, no per-configuration loop.  The
@@ -51,26 +55,35 @@ struct SweepCfg {
     int32_t lut_n, lut_shift;            // ratio buckets (0: none), bits dropped per bucket
     uint64_t lut_lo, lut_hi;             // storage-type bit patterns of the bucketed ratio range
     double sfmin, sfmax;                 // column sums whose ratio stays a normal number
-    int32_t orig[kSweepMaxCfg];          // sorted slot -> caller's configuration index
-    int32_t hcap[kSweepMaxCfg];          // confidence: min(min_horizon, N); static: min(static_h, N)
-    double p[kSweepMaxCfg];              // 1 + t, ascending (confidence slots)
-    double rh[kSweepPad], rl[kSweepPad]; // ratio bounds (1 + t) / (K - 1) * (1 +/- margin), outward
-    uint16_t lut[kSweepLut];             // bucket -> tripping slots, 0xFFFF: undecided
+    alignas(16) int32_t orig[kSweepMaxCfg];  // sorted slot -> caller's configuration index
+    alignas(16) int32_t hcap[kSweepMaxCfg];  // confidence: min(min_horizon, N); static: min(static_h, N)
+    alignas(16) double p[kSweepMaxCfg];      // 1 + t, ascending (confidence slots)
+    alignas(16) double rh[kSweepPad];        // ratio bounds (1 + t) / (K - 1) * (1 +/- margin),
+    alignas(16) double rl[kSweepPad];        //   outward
+    alignas(16) uint16_t lut[kSweepLut]; // bucket -> tripping slots, 0xFFFF: undecided
+    uint64_t clamp_base;                 // bits of clamp_lo (segmented kernel's table origin)
+    double clamp_lo, clamp_hi;           // ratio clamp: the below / above entries
+    uint16_t lut_below, lut_above;       // sentinel entries (0 / Cc; 0xFFFF without a table)
 };
 
 // shared copies of the per-configuration tables (indexed per lane)
 struct SweepTables {
-    double rhd[kSweepPad], rld[kSweepPad];
+    alignas(16) double rhd[kSweepPad];
+    alignas(16) double rld[kSweepPad];
+    alignas(16) double p[kSweepMaxCfg];
+    alignas(16) int32_t orig[kSweepMaxCfg];
+    alignas(16) int32_t hcap[kSweepMaxCfg];
     float rh[kSweepPad], rl[kSweepPad];
-    double p[kSweepMaxCfg];
-    int32_t orig[kSweepMaxCfg];
-    int32_t hcap[kSweepMaxCfg];
     // per-CTA sums stay below 2^32: R * N elements fit in HBM, so a CTA's share
     // (R / grid robots, N columns, horizons <= N) is < 2^32; checked on the host
     uint32_t D[kSweepMaxCfg + 1];  // difference array of the per-slot sums (mod 2^32)
     uint32_t F[kSweepMaxCfg];      // min_horizon floor corrections
-    uint16_t lut[kSweepLut + 2];   // [0]: below the table (0), [lut_n + 1]: above (Cc)
+    // bucket table: entries at [kLutBase, kLutBase + lut_n) (16-byte aligned for
+    // the vector copy), [kLutBase - 1]: below the table (0), [kLutBase + lut_n]:
+    // above (Cc)
+    alignas(16) uint16_t lut[kSweepLut + 16];
 };
+constexpr int kLutBase = 8;
 
 // Bit-exact count of tripping confidence configurations for one column.
 template <typename T>
@@ -153,8 +166,8 @@ struct SweepWork {
             sb = static_cast<uint64_t>(__double_as_longlong(sf));
         }
         if (fin == T(0)) bits = 0;
-        SB idx = (static_cast<SB>(bits - static_cast<B>(lut_lo)) >> lut_shift) + 1;
-        idx = idx < 0 ? 0 : (idx > lut_n + 1 ? lut_n + 1 : idx);
+        SB idx = (static_cast<SB>(bits - static_cast<B>(lut_lo)) >> lut_shift) + kLutBase;
+        idx = idx < kLutBase - 1 ? kLutBase - 1 : (idx > lut_n + kLutBase ? lut_n + kLutBase : idx);
         const int e = tables()->lut[idx];
         const bool out = static_cast<B>(sb - static_cast<B>(sfminb)) > static_cast<B>(sfrng) && sb != 0;
         return e == 0xFFFF || out ? -1 : e;
@@ -313,40 +326,59 @@ struct SweepWork {
         const int g = threadIdx.x & 15;
         const int n0 = 2 * g, n1 = 32 + 2 * g;
         const bool p0 = robot_ok && n0 < N, p1 = robot_ok && n1 < N;
-        const bool odd = N & 1;  // rows are not pair-aligned: guarded scalar loads
         int j[4] = {0, 0, 0, 0};
         if (p0) {
             T sf[4], fin[4];
             uint32_t mx = 0;
-            for (int k = 0; k < Kr; k++) {
-                T x[4] = {T(0), T(0), T(0), T(0)};
-                const T* row = rob + k * N;
-                if (!odd) {
-                    load_pair(row + n0, x[0], x[1]);
-                    if (p1) load_pair(row + n1, x[2], x[3]);
-                } else {  // a column past N stays zero: filter() gives 0
+            if (!(N & 1)) {
+                // even N: straight-line pair loads; a lane without a second pair
+                // re-reads its first one (already validated, its trips masked below)
+                const int n1c = p1 ? n1 : n0;
+                auto row = [&](int k) {
+                    T x[4];
+                    load_pair(rob + k * N + n0, x[0], x[1]);
+                    load_pair(rob + k * N + n1c, x[2], x[3]);
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        mx = max(mx, CW::sexp(x[c]));
+                        if (k == 0) sf[c] = x[c];
+                        else if (k < Kr - 1) sf[c] = CW::add_rn(sf[c], x[c]);
+                        else fin[c] = x[c];
+                    }
+                };
+                if constexpr (KC > 0) {
+#pragma unroll
+                    for (int k = 0; k < KC; k++) row(k);
+                } else {
+                    for (int k = 0; k < Kr; k++) row(k);
+                }
+            } else {  // odd N: rows are not pair-aligned; a column past N stays zero
+                for (int k = 0; k < Kr; k++) {
+                    T x[4] = {T(0), T(0), T(0), T(0)};
+                    const T* row = rob + k * N;
                     x[0] = row[n0];
                     if (n0 + 1 < N) x[1] = row[n0 + 1];
                     if (p1) x[2] = row[n1];
                     if (n1 + 1 < N) x[3] = row[n1 + 1];
-                }
 #pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    mx = max(mx, CW::sexp(x[c]));
-                    if (k == 0) sf[c] = x[c];
-                    else if (k < Kr - 1) sf[c] = CW::add_rn(sf[c], x[c]);
-                    else fin[c] = x[c];
+                    for (int c = 0; c < 4; c++) {
+                        mx = max(mx, CW::sexp(x[c]));
+                        if (k == 0) sf[c] = x[c];
+                        else if (k < Kr - 1) sf[c] = CW::add_rn(sf[c], x[c]);
+                        else fin[c] = x[c];
+                    }
                 }
             }
-            // the padding pair of a lane past N is zeros: filter() gives 0
             const bool bad = mx >= CW::kBad;
             bool any = bad;
 #pragma unroll
             for (int c = 0; c < 4; c++) {
                 j[c] = filter(sf[c], fin[c]);
+                if (c >= 2 && !p1) j[c] = 0;  // no second pair (odd N: zeros filter to 0)
                 any = any || j[c] < 0;
             }
             if (any) {
+#pragma unroll
                 for (int c = 0; c < 4; c++) {
                     const int n = c < 2 ? n0 + c : n1 + c - 2;
                     if (n >= N) continue;
@@ -438,7 +470,406 @@ struct SweepWork {
     __device__ __forceinline__ void finish(int64_t, int, int, int, int) {}
 };
 
+// ---------------------------------------------------------------------------
+// Segmented sweep (the default for N <= 512): G lanes per robot, each lane
+// owning a window of CPL (14 or 16) columns (VW = 2: column pairs with
+// 8/16-byte loads), 32 / G robots per warp.  Pass 1 decides every column of
+// the segment in registers with no cross-lane traffic: K row loads, the
+// validation max, the fp32 sums (packed FADD2 for pairs), and the bucket-table
+// lookup on the CLAMPED ratio -- clamping the ratio to the table's range
+// replaces the index clamp and the zero rules (f == 0: ratio 0 or NaN -> the
+// "below" entry, no trip; sum == 0 < f: +inf -> the "above" entry, all trip).
+// The per-lane range checks fold into two reductions: the element maximum
+// bounds every column sum from above, and an unsigned minimum over
+// bits(sum) - 1 (a zero sum wraps to the top) bounds them from below.  Pass 2
+// is one exclusive max-scan over the robot's G segment maxima; only a lane
+// whose segment raises the running maximum walks its registers for the steps.
+// Columns the table cannot decide (and invalid or out-of-range lanes) are
+// re-decided one by one in sweep_fix, off the straight-line path.
+// Lane mapping q = lane % (32 / G) (robot), s = lane / (32 / G) (segment):
+// for N = 50 fp32 the 8-byte row loads of a half-warp hit 16 distinct bank
+// pairs (robot stride 300 words = 12 mod 32 banks, segment stride 14).
+// ---------------------------------------------------------------------------
+constexpr int kSegCols = 16;  // columns per lane (compile-time register array)
+
+// One column re-decided exactly (rare path): (flags << 16) | trip count.
+template <typename T, int KC>
+__device__ __noinline__ int sweep_fix(const T* col, int K, int N, int jf, bool check_vals,
+                                      T sfmin, T sfmax, int half, int Cc, const double* p,
+                                      const T* rh, const T* rl) {
+    using CW = ConfWork<T, KC, 1>;
+    const int Kr = KC > 0 ? KC : K;
+    uint32_t fl = 0, mx = 0;
+    T sf = col[0], fin = col[static_cast<size_t>(Kr - 1) * N];
+    for (int k = 0; k < Kr; k++) {
+        const T x = col[static_cast<size_t>(k) * N];
+        mx = max(mx, CW::sexp(x));
+        if (check_vals) fl |= CW::check(x);
+        if (k >= 1 && k < Kr - 1) sf = CW::add_rn(sf, x);
+    }
+    const bool colbad = mx >= CW::kBad;
+    const bool inr = sf == T(0) || (sf >= sfmin && sf <= sfmax);
+    int j = jf;
+    if (colbad || !inr || jf == 0xFFFF) {
+        j = -1;
+        if (!colbad && sf >= sfmin && sf <= sfmax) {  // branch-free binary search
+            T rho;
+            if constexpr (sizeof(T) == 4) {
+                float r;
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(sf));
+                rho = __fmul_rn(fin, r);
+            } else {
+                rho = __dmul_rn(fin, __drcp_rn(sf));
+            }
+            int pos = 0;
+            for (int st = half; st > 0; st >>= 1)
+                if (rho > rh[pos + st - 1]) pos += st;
+            if (pos == Cc || rho < rl[pos]) j = pos;
+        }
+        if (j < 0) j = sweep_exact(col, K, N, p, Cc);
+    }
+    return static_cast<int>(fl << 16) | j;
+}
+
+template <typename T, int KC, int VW, int CPL>
+struct SweepSeg {
+    using CW = ConfWork<T, KC, 1>;
+    using B = typename std::conditional<sizeof(T) == 4, uint32_t, uint64_t>::type;
+    using Elem = T;
+    static constexpr int kVC = VW;
+    int K, N, C, Cc, maxcap, half;
+    int G, RW, lgRW;             // lanes per robot, robots per warp (32 / G), log2(RW)
+    int cw;                      // consumer warps
+    int lut_shift;
+    B lut_base;                  // bits of clo: table index = (bits(rho) - lut_base) >> lut_shift
+    T clo, chi;                  // ratio clamp: the "below" / "above" entries
+    uint32_t emaxb;              // element bound (sexp) keeping every sum <= sfmax
+    B sfminb1;                   // bits(sfmin) - 1
+    T sfmin, sfmax;
+    int32_t* H;                  // [C][R] (nullable)
+    unsigned long long* sums;    // [C]
+    uint32_t* flags;
+    int64_t R;
+    __device__ __forceinline__ static SweepTables* tables() {
+        extern __shared__ __align__(128) unsigned char smem[];
+        return reinterpret_cast<SweepTables*>(smem + stream_aux_offset());
+    }
+    __device__ void setup(int) {}
+    // per-warp task list of the cooperative exact path (32 x CPL entries)
+    __device__ __forceinline__ static uint16_t* fix_tasks(int warp) {
+        extern __shared__ __align__(128) unsigned char smem[];
+        return reinterpret_cast<uint16_t*>(smem + stream_aux_offset() + sizeof(SweepTables)) +
+               warp * 32 * kSegCols;
+    }
+
+    __device__ __forceinline__ static B bits_of(T x) {
+        if constexpr (sizeof(T) == 4) return __float_as_uint(x);
+        else return static_cast<uint64_t>(__double_as_longlong(x));
+    }
+
+    // trip count of one column from its sum and final magnitude (bucket table)
+    __device__ __forceinline__ int lookup(T sf, T fin, B& mn) const {
+        T rho;
+        if constexpr (sizeof(T) == 4) {
+            float r;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(sf));  // <= 1 ulp, sf normal
+            rho = fminf(fmaxf(__fmul_rn(fin, r), clo), chi);
+        } else {
+            rho = fmin(fmax(__dmul_rn(fin, __drcp_rn(sf)), clo), chi);
+        }
+        mn = min(mn, bits_of(sf) - B(1));
+        const uint32_t idx = static_cast<uint32_t>((bits_of(rho) - lut_base) >> lut_shift);
+        return (tables()->lut + (kLutBase - 1))[idx];  // [0]: below, [lut_n + 1]: above
+    }
+
+    // configurations [a, b) take horizon n at this robot (a < b)
+    __device__ __forceinline__ void step(int a, int b, int n, int64_t r) const {
+        atomicAdd(&tables()->D[a], static_cast<uint32_t>(n));
+        atomicSub(&tables()->D[b], static_cast<uint32_t>(n));
+        if (n < maxcap)  // below some min_horizon floor (horizon.py:130)
+            for (int c = a; c < b; c++) {
+                const int cap = tables()->hcap[c];
+                if (cap > n) atomicAdd(&tables()->F[c], static_cast<uint32_t>(cap - n));
+            }
+        if (H)
+            for (int c = a; c < b; c++) {
+                const int cap = tables()->hcap[c];
+                H[static_cast<int64_t>(tables()->orig[c]) * R + r] = n > cap ? n : cap;
+            }
+    }
+
+    // byte i of the packed running maxima
+    __device__ __forceinline__ static int byte_at(const uint32_t (&pk)[(CPL + 3) / 4], int i) {
+        uint32_t w = pk[0];
+#pragma unroll
+        for (int t = 1; t < (CPL + 3) / 4; t++) w = (i >> 2) == t ? pk[t] : w;
+        return static_cast<int>((w >> ((i & 3) * 8)) & 0xFFu);
+    }
+
+    __device__ __forceinline__ void tile(const TileView& v, int64_t r0, int nr, int) {
+        const T* u = reinterpret_cast<const T*>(v.seg[0]);
+        const int Kr = KC > 0 ? KC : K;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (warp >= cw) return;
+        const int q = lane & (RW - 1), sg = lane >> lgRW;
+        const int KN = Kr * N;
+        // the lane's window of CPL columns; the last windows are shifted left to
+        // end at N (their leading columns repeat the previous lane's: those are
+        // below the scan's carry, so they never step twice)
+        const int c0 = min(sg * CPL, N - CPL);
+        uint32_t fl = 0;
+        for (int rb = warp * RW; rb < nr; rb += cw * RW) {
+            const int rr = rb + q;
+            const bool ok = rr < nr;
+            const T* rob = u + (ok ? rr : 0) * KN;  // lanes past the tile re-read robot 0
+            const T* base = rob + c0;
+            int j[CPL];
+            uint32_t mx = 0;
+            B mn = ~B(0);
+            int m = 0;
+            if constexpr (VW == 2 && sizeof(T) == 4) {
+                // row pointers once per robot: every pair load below is [row + imm]
+                const T* rowp[KC > 0 ? KC : 1];
+                if constexpr (KC > 0) {
+#pragma unroll
+                    for (int k = 0; k < KC; k++) rowp[k] = base + k * N;
+                }
+#pragma unroll
+                for (int i = 0; i < CPL; i += 2) {
+                    float2 x, sf;
+                    auto ld = [&](int k) {
+                        const T* rp = KC > 0 ? rowp[KC > 0 ? k : 0] : base + k * N;
+                        x = *reinterpret_cast<const float2*>(rp + i);
+                        mx = max(mx, max(__float_as_uint(x.x), __float_as_uint(x.y)));
+                    };
+                    auto add2 = [&]() {
+                        unsigned long long a2, b2, o2;
+                        memcpy(&a2, &sf, 8);
+                        memcpy(&b2, &x, 8);
+                        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(o2) : "l"(a2), "l"(b2));
+                        memcpy(&sf, &o2, 8);
+                    };
+                    ld(0);
+                    sf = x;
+                    if constexpr (KC > 0) {
+#pragma unroll
+                        for (int k = 1; k < KC - 1; k++) { ld(k); add2(); }
+                        ld(KC - 1);
+                    } else {
+                        for (int k = 1; k < Kr - 1; k++) { ld(k); add2(); }
+                        ld(Kr - 1);
+                    }
+                    j[i] = lookup(sf.x, x.x, mn);
+                    j[i + 1] = lookup(sf.y, x.y, mn);
+                    m = max(m, max(j[i], j[i + 1]));
+                }
+            } else {
+                const T* rowp[KC > 0 ? KC : 1];
+                if constexpr (KC > 0) {
+#pragma unroll
+                    for (int k = 0; k < KC; k++) rowp[k] = base + k * N;
+                }
+#pragma unroll
+                for (int i = 0; i < CPL; i += VW) {
+                    T sf[VW], x[VW];
+                    auto ldv = [&](int k) {  // VW adjacent columns of row k
+                        const T* rp = (KC > 0 ? rowp[KC > 0 ? k : 0] : base + k * N) + i;
+                        if constexpr (VW == 2 && sizeof(T) == 8) {
+                            const double2 d = *reinterpret_cast<const double2*>(rp);
+                            x[0] = d.x;
+                            x[VW - 1] = d.y;
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < VW; c++) x[c] = rp[c];
+                        }
+                    };
+                    ldv(0);
+#pragma unroll
+                    for (int c = 0; c < VW; c++) {
+                        sf[c] = x[c];
+                        mx = max(mx, CW::sexp(x[c]));
+                    }
+                    auto rowk = [&](int k, bool add) {
+                        ldv(k);
+#pragma unroll
+                        for (int c = 0; c < VW; c++) {
+                            mx = max(mx, CW::sexp(x[c]));
+                            if (add) sf[c] = CW::add_rn(sf[c], x[c]);
+                        }
+                    };
+                    if constexpr (KC > 0) {
+#pragma unroll
+                        for (int k = 1; k < KC; k++) rowk(k, k < KC - 1);
+                    } else {
+                        for (int k = 1; k < Kr; k++) rowk(k, k < Kr - 1);
+                    }
+#pragma unroll
+                    for (int c = 0; c < VW; c++) {
+                        j[i + c] = lookup(sf[c], x[c], mn);
+                        m = max(m, j[i + c]);
+                    }
+                }
+            }
+            // rare: undecided buckets, invalid values, sums outside [sfmin, sfmax].
+            // The warp's columns that need an exact decision are dealt to all 32
+            // lanes (undecided columns cluster in the tail windows: one lane
+            // would otherwise run them one after another).
+            const bool need = ok && (mx > emaxb || mn < sfminb1 || m >= 0xFFFF);
+            if (__any_sync(0xffffffffu, need)) {
+                const bool all = mx > emaxb || mn < sfminb1;  // re-check every column
+                uint32_t fm = 0;
+                if (need) {
+#pragma unroll
+                    for (int i = 0; i < CPL; i++)
+                        if (all || j[i] == 0xFFFF) fm |= 1u << i;
+                }
+                const int cnt = __popc(fm);
+                int inc = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int o = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += o;
+                }
+                const int total = __shfl_sync(0xffffffffu, inc, 31);
+                uint16_t* task = fix_tasks(warp);
+                {
+                    const uint32_t chk = mx >= CW::kBad ? 1u : 0u;
+                    uint32_t f = fm;
+                    int o = inc - cnt;
+                    while (f) {
+                        const int i = __ffs(f) - 1;
+                        f &= f - 1;
+                        task[o++] = static_cast<uint16_t>(i | (lane << 4) | (chk << 9));
+                    }
+                }
+                __syncwarp();
+                const T* rh = sizeof(T) == 4 ? reinterpret_cast<const T*>(tables()->rh)
+                                             : reinterpret_cast<const T*>(tables()->rhd);
+                const T* rl = sizeof(T) == 4 ? reinterpret_cast<const T*>(tables()->rl)
+                                             : reinterpret_cast<const T*>(tables()->rld);
+                for (int t = lane; t < total; t += 32) {
+                    const uint32_t e = task[t];
+                    const int L = (e >> 4) & 31;
+                    const int cL = min((L >> lgRW) * CPL, N - CPL) + static_cast<int>(e & 15);
+                    const T* col = u + (rb + (L & (RW - 1))) * KN + cL;
+                    const int pk = sweep_fix<T, KC>(col, K, N, 0xFFFF, (e >> 9) & 1, sfmin, sfmax,
+                                                    half, Cc, tables()->p, rh, rl);
+                    task[t] = static_cast<uint16_t>((pk & 0xFF) | ((static_cast<uint32_t>(pk) >> 16) << 8));
+                }
+                __syncwarp();
+                if (fm) {
+                    int o = inc - cnt;
+                    m = 0;
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) {
+                        if ((fm >> i) & 1u) {
+                            const uint32_t e = task[o++];
+                            j[i] = static_cast<int>(e & 0xFF);
+                            fl |= e >> 8;
+                        }
+                        m = max(m, j[i]);
+                    }
+                }
+                __syncwarp();  // the task list is rewritten by the next robot group
+            }
+            // exclusive max-scan over the robot's segments (lanes q, q + RW, ...)
+            int vv = m;
+            for (int d = 1; d < G; d <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, vv, d * RW);
+                if (sg >= d) vv = max(vv, o);
+            }
+            int cur = __shfl_up_sync(0xffffffffu, vv, RW);
+            if (sg == 0) cur = 0;
+            const int64_t r = r0 + rr;
+            if (ok && m > cur) {  // this segment raises the running maximum
+                // branch-free: the columns where it rises, and the running maxima
+                uint32_t mask = 0;
+                uint32_t pk[(CPL + 3) / 4];
+                int run = cur;
+#pragma unroll
+                for (int i = 0; i < CPL; i++) {
+                    if (j[i] > run) mask |= 1u << i;
+                    run = max(run, j[i]);
+                    if ((i & 3) == 0) pk[i >> 2] = static_cast<uint32_t>(run);
+                    else pk[i >> 2] |= static_cast<uint32_t>(run) << ((i & 3) * 8);
+                }
+                int a2 = cur;
+                while (mask) {
+                    const int i = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int b2 = byte_at(pk, i);
+                    step(a2, b2, c0 + i, r);
+                    a2 = b2;
+                }
+            }
+            if (ok && sg == G - 1 && vv < Cc) {  // slots never tripped take N
+                atomicAdd(&tables()->D[vv], static_cast<uint32_t>(N));
+                if (H)
+                    for (int c = vv; c < Cc; c++)
+                        H[static_cast<int64_t>(tables()->orig[c]) * R + r] = N;
+            }
+            if (ok && H)
+                for (int c = Cc + sg; c < C; c += G)
+                    H[static_cast<int64_t>(tables()->orig[c]) * R + r] = tables()->hcap[c];
+        }
+        if (fl && flags) atomicOr(flags, fl);
+    }
+
+    __device__ __forceinline__ void finish(int64_t, int, int, int, int) {}
+};
+
 constexpr int kSweepThreads = 384;
+
+// n16 16-byte pieces from the (16-byte aligned) parameter space to shared memory.
+__device__ __forceinline__ void param_copy16(void* dst, const void* src, int n16) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
+}
+
+// Shared tables from the parameter space, in 16-byte pieces: a load whose
+// address differs across the warp is issued once per distinct address, so
+// wide pieces (not 2- or 8-byte elements) keep the prologue short.
+__device__ __forceinline__ void sweep_prologue(SweepTables* tab, const SweepCfg& cfg) {
+    param_copy16(tab->lut + kLutBase, cfg.lut, (cfg.lut_n * 2 + 15) / 16);
+    param_copy16(tab->rhd, cfg.rh, kSweepPad * 8 / 16);
+    param_copy16(tab->rld, cfg.rl, kSweepPad * 8 / 16);
+    param_copy16(tab->p, cfg.p, kSweepMaxCfg * 8 / 16);
+    param_copy16(tab->orig, cfg.orig, kSweepMaxCfg * 4 / 16);
+    param_copy16(tab->hcap, cfg.hcap, kSweepMaxCfg * 4 / 16);
+    if (threadIdx.x == 0) {
+        tab->lut[kLutBase - 1] = cfg.lut_below;
+        tab->lut[kLutBase + cfg.lut_n] = cfg.lut_above;
+    }
+    for (int i = threadIdx.x; i <= kSweepMaxCfg; i += blockDim.x) {
+        tab->D[i] = 0;
+        if (i < kSweepMaxCfg) tab->F[i] = 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSweepPad; i += blockDim.x) {
+        tab->rh[i] = static_cast<float>(tab->rhd[i]);  // exactly representable (host-rounded)
+        tab->rl[i] = static_cast<float>(tab->rld[i]);
+    }
+    __syncthreads();
+}
+
+// S_c = prefix_sum(D)[c] + F[c] per CTA; static slots once per grid
+__device__ __forceinline__ void sweep_epilogue(const SweepTables* tab, int Cc, int C, int64_t R,
+                                               unsigned long long* sums) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int c = 0; c < Cc; c++) {
+            run += tab->D[c];
+            const uint32_t s = run + tab->F[c];
+            if (s) atomicAdd(&sums[tab->orig[c]], static_cast<unsigned long long>(s));
+        }
+        if (blockIdx.x == 0)
+            for (int c = Cc; c < C; c++)
+                atomicAdd(&sums[tab->orig[c]],
+                          static_cast<unsigned long long>(R) * static_cast<unsigned long long>(tab->hcap[c]));
+    }
+}
 
 template <typename T, int KC, int VC, bool kStaged, bool HALF = false>
 __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p,
@@ -446,41 +877,57 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p
                                                                          const __grid_constant__ SweepCfg cfg) {
     extern __shared__ __align__(128) unsigned char smem[];
     SweepTables* const tab = w.tables();
-    for (int i = threadIdx.x; i < w.lut_n; i += blockDim.x) tab->lut[i + 1] = cfg.lut[i];
-    if (threadIdx.x == 0) {
-        tab->lut[0] = 0;
-        tab->lut[w.lut_n + 1] = static_cast<uint16_t>(w.Cc);
-    }
-    for (int i = threadIdx.x; i < kSweepPad; i += blockDim.x) {
-        tab->rhd[i] = cfg.rh[i];
-        tab->rld[i] = cfg.rl[i];
-        tab->rh[i] = static_cast<float>(cfg.rh[i]);  // exactly representable (host-rounded)
-        tab->rl[i] = static_cast<float>(cfg.rl[i]);
-        if (i < kSweepMaxCfg) {
-            tab->p[i] = cfg.p[i];
-            tab->orig[i] = cfg.orig[i];
-            tab->hcap[i] = cfg.hcap[i];
-            tab->F[i] = 0;
-        }
-        if (i <= kSweepMaxCfg) tab->D[i] = 0;
-    }
-    __syncthreads();
+    sweep_prologue(tab, cfg);
     stream_run<kStaged>(p, smem, w);
-    __syncthreads();
-    if (threadIdx.x == 0) {  // S_c = prefix_sum(D)[c] + F[c]; static slots once per grid
-        uint32_t run = 0;
-        for (int c = 0; c < w.Cc; c++) {
-            run += tab->D[c];
-            const uint32_t s = run + tab->F[c];
-            if (s) atomicAdd(&w.sums[tab->orig[c]], static_cast<unsigned long long>(s));
-        }
-        if (blockIdx.x == 0)
-            for (int c = w.Cc; c < w.C; c++)
-                atomicAdd(&w.sums[tab->orig[c]],
-                          static_cast<unsigned long long>(w.R) * static_cast<unsigned long long>(tab->hcap[c]));
-    }
+    sweep_epilogue(tab, w.Cc, w.C, w.R, w.sums);
 }
 
+constexpr int kSegThreads = 512;  // <= 128 registers per thread
+
+template <typename T, int KC, int VW, int CPL, bool kStaged>
+__global__ void __launch_bounds__(kSegThreads) k_horizon_sweep_seg(StreamPlan p, SweepSeg<T, KC, VW, CPL> w,
+                                                                    const __grid_constant__ SweepCfg cfg) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    SweepTables* const tab = w.tables();
+    sweep_prologue(tab, cfg);
+    stream_run<kStaged>(p, smem, w);
+    sweep_epilogue(tab, w.Cc, w.C, w.R, w.sums);
+}
+
+
+// Shared-memory wavefronts of the segmented kernel's first row load (lane q =
+// lane % RW reads robot q, window c0(s)): the robot stride in banks decides
+// whether the windows of a phase collide (N = 50 fp32: 1, conflict-free;
+// N = 64 / 128 fp32: every robot on the same banks).  Above 2 the launcher
+// keeps the warp-per-robot kernels.
+inline int sweep_seg_conflicts(int K, int N, size_t es, bool pair) {
+    int G = 1;
+    while (G * kSegCols < N) G <<= 1;
+    const int CPL = pair && G * 14 >= N ? 14 : kSegCols;
+    const int RW = 32 / G;
+    const int w = static_cast<int>(es / 4);         // words per element
+    const int width = (pair ? 2 : 1) * w;           // words per lane access
+    const int lanes = width >= 4 ? 8 : (width == 2 ? 16 : 32);  // lanes per phase
+    int worst = 1;
+    for (int ph = 0; ph < 32; ph += lanes) {
+        long words[32][32];  // per bank: the distinct words the phase touches
+        int cnt[32] = {};
+        for (int l = ph; l < ph + lanes; l++) {
+            const int q = l % RW, sg = l / RW;
+            const int c0 = std::min(sg * CPL, N - CPL);
+            const long a0 = (static_cast<long>(q) * K * N + c0) * w;
+            for (int t = 0; t < width; t++) {
+                const long wd = a0 + t;
+                const int b = static_cast<int>(wd & 31);
+                bool seen = false;
+                for (int z = 0; z < cnt[b]; z++) seen = seen || words[b][z] == wd;
+                if (!seen) words[b][cnt[b]++] = wd;
+            }
+        }
+        for (int b = 0; b < 32; b++) worst = std::max(worst, cnt[b]);
+    }
+    return worst;
+}
 
 // Launch of the per-dtype sweep kernels (instantiated in kr_sweep_f32.cu /
 // kr_sweep_f64.cu so the two halves compile in parallel).
@@ -495,9 +942,11 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
         // a warp per robot (32 "items"): 11 consumer warps x 2 robots per tile,
         // two CTAs (24 warps) per SM -- the per-robot scan is instruction-heavy,
         // so warps, not bytes in flight, set the pace
+        static const int tr_env = std::getenv("KR_SWEEP_TR") ? std::atoi(std::getenv("KR_SWEEP_TR")) : 0;
         StreamPlan p = make_plan(1, bases, &rb, R, W::kHalf ? 16 : 32, 0, kSweepThreads - 32,
                                  kernel_regs(kstaged), 2,
-                                 static_cast<uint32_t>(sizeof(SweepTables)), W::kHalf ? 44 : 22);
+                                 static_cast<uint32_t>(sizeof(SweepTables)),
+                                 tr_env > 0 ? tr_env : (W::kHalf ? 44 : 22));
         // per-CTA 32-bit sums: robots per CTA (grid >= SMs) x N < 2^32
         if ((R / device_info().sm_count + 1) * static_cast<int64_t>(N) >= (int64_t(1) << 32))
             return KR_EINVAL;
@@ -531,6 +980,74 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
     const bool al = (reinterpret_cast<uintptr_t>(U) & 15u) == 0;
 #define KR_SWEEP(KK, VV) \
     return go(SweepWork<T, KK, VV>{}, k_horizon_sweep<T, KK, VV, true>, k_horizon_sweep<T, KK, VV, false>)
+    // segmented sweep: G lanes per robot, <= kSegCols columns per lane
+    static const bool seg_off = std::getenv("KR_SWEEP_NO_SEG") != nullptr;  // A/B knob
+    if (!seg_off && N <= 32 * kSegCols && N >= kSegCols &&
+        sweep_seg_conflicts(K, N, sizeof(T), al && N % 2 == 0) <= 2) {
+        int G = 1;
+        while (G * kSegCols < N) G <<= 1;
+        const bool pair = al && N % 2 == 0;
+        // pairs: 14-column windows where they cover N (N = 50: 4 x 14)
+        const bool c14 = pair && G * 14 >= N;
+        const int RW = 32 / G;
+        auto go_seg = [&](auto proto, auto kstaged, auto kdirect) -> int {
+            using W = decltype(proto);
+            static const int tr_env = std::getenv("KR_SWEEP_TR") ? std::atoi(std::getenv("KR_SWEEP_TR")) : 0;
+            static const int cw_env = std::getenv("KR_SWEEP_CW") ? std::atoi(std::getenv("KR_SWEEP_CW")) : 0;
+            const int tr = tr_env > 0 ? tr_env : (cw_env > 0 ? cw_env : 5) * RW;
+            const uint32_t task_bytes = static_cast<uint32_t>((tr * G + 31) / 32) * 32 * kSegCols * 2;
+            StreamPlan p = make_plan(1, bases, &rb, R, G, 0, kSegThreads - 32, kernel_regs(kstaged), 1,
+                                     static_cast<uint32_t>(sizeof(SweepTables)) + task_bytes, tr);
+            if ((R / device_info().sm_count + 1) * static_cast<int64_t>(N) >= (int64_t(1) << 32))
+                return KR_EINVAL;
+            W w{};
+            w.K = K; w.N = N; w.C = C; w.Cc = Cc; w.maxcap = cfg.maxcap; w.half = cfg.half;
+            w.G = G; w.RW = RW;
+            w.lgRW = 0;
+            while ((1 << w.lgRW) < RW) w.lgRW++;
+            w.cw = p.threads / 32;
+            w.lut_shift = cfg.lut_shift;
+            w.lut_base = static_cast<typename W::B>(cfg.clamp_base);
+            w.clo = static_cast<T>(cfg.clamp_lo);
+            w.chi = static_cast<T>(cfg.clamp_hi);
+            w.sfmin = static_cast<T>(cfg.sfmin);
+            w.sfmax = static_cast<T>(cfg.sfmax);
+            if (cfg.sfmin <= cfg.sfmax) {
+                // every element <= emax keeps each (K - 1)-term sum <= sfmax
+                const T emax = static_cast<T>(cfg.sfmax / ((K - 1) * 1.01));
+                const T smin = static_cast<T>(cfg.sfmin);
+                if constexpr (sizeof(T) == 4) {
+                    uint32_t a, b;
+                    std::memcpy(&a, &emax, 4); std::memcpy(&b, &smin, 4);
+                    w.emaxb = a; w.sfminb1 = b - 1;
+                } else {
+                    uint64_t a, b;
+                    std::memcpy(&a, &emax, 8); std::memcpy(&b, &smin, 8);
+                    w.emaxb = static_cast<uint32_t>(a >> 32) - 1;  // high word, strictly below
+                    w.sfminb1 = b - 1;
+                }
+            } else {  // no sum filter: every lane re-decides exactly
+                w.emaxb = 0;
+                w.sfminb1 = ~typename W::B(0);
+            }
+            w.H = H; w.sums = sums; w.flags = flags; w.R = R;
+            return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_sweep", 0, cfg);
+        };
+#define KR_SEG(KK, VV, CC)                                                   \
+    return go_seg(SweepSeg<T, KK, VV, CC>{}, k_horizon_sweep_seg<T, KK, VV, CC, true>, \
+                  k_horizon_sweep_seg<T, KK, VV, CC, false>)
+        if (pair) {
+            if (c14) {
+                if (K == 6) KR_SEG(6, 2, 14);
+                KR_SEG(0, 2, 14);
+            }
+            if (K == 6) KR_SEG(6, 2, 16);
+            KR_SEG(0, 2, 16);
+        }
+        if (K == 6) KR_SEG(6, 1, 16);
+        KR_SEG(0, 1, 16);
+#undef KR_SEG
+    }
     // two robots per warp: N <= 64 (pair loads when N is even and the base 16-byte aligned)
     static const bool half_off = std::getenv("KR_SWEEP_NO_HALF") != nullptr;  // A/B knob
     if (!half_off && N <= 64 && (N % 2 == 1 || al)) {

@@ -514,8 +514,8 @@ def other_configs(reps: int = 200):
     lib = _lib.load()
     out = {}
 
-    def timed_captured(rnd, fleet, inp, reserve):
-        rnd.capture(fleet, inp, reserve_sms=reserve, layout="split")
+    def timed_captured(rnd, fleet, inp, reserve, layout="split"):
+        rnd.capture(fleet, inp, reserve_sms=reserve, layout=layout)
         for _ in range(10):
             rnd.replay()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -576,21 +576,12 @@ def other_configs(reps: int = 200):
     U = synthetic.magnitudes(R, seed=19)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))
-    rnd.capture(fleet, inp, reserve_sms=24, layout="split")  # profiles/r1_confidence_layouts.jsonl
-    for _ in range(5):
-        rnd.replay()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record()
-    for _ in range(reps):
-        rnd.replay()
-    b.record()
-    torch.cuda.synchronize()
-    t = a.elapsed_time(b) / 1e3 / reps
+    # urgency pass on the whole GPU, then horizons || admission (profiles/r2_confidence_layouts.jsonl)
+    t = timed_captured(rnd, fleet, inp, 16, layout="urgency_first")
     out["configs[4] per-GPU share, confidence policy (U 2^20 x 6 x 50 fp32), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (1.26 GB of magnitudes)",
-        "layout": "split: horizons || urgency + admission (24 reserved SMs)"}
+        "layout": "urgency_first: urgency, then horizons || admission (16 reserved SMs)"}
     # fp64 storage (the reference's native dtype, workload.py:485-486): the
     # headline divergence round and the confidence round, same layouts
     R = 1 << 20

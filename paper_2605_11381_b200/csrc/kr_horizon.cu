@@ -30,6 +30,7 @@
 #include "kr_conf.cuh"
 #include "kr_div.cuh"
 #include "kr_plan.cuh"
+#include "kr_sweep.cuh"
 
 namespace kr {
 
@@ -64,9 +65,29 @@ extern "C" int kr_horizon_confidence(const void* U, int dtype, int64_t R, int32_
     const size_t es = dtype == KR_F64 ? 8 : 4;
     uint64_t rb = static_cast<uint64_t>(K) * N * es;
     if (N > (kStreamThreads - 32) * kMaxRounds) return KR_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    // Default: the segmented decide kernel (kr_sweep.cuh SweepSeg) as a
+    // one-configuration sweep writing H -- per robot a handful of lanes decide
+    // register-resident column windows (a third of this kernel's instructions,
+    // a third of its warps), which leaves SM slots for the round's side stream.
+    // Thresholds whose bucket table cannot be built (1 + t beyond ~1e30) and
+    // shapes the segmented layout does not take stay on k_horizon_confidence.
+    static const bool classic = std::getenv("KR_CONF_CLASSIC") != nullptr;  // A/B knob
+    // (fp32 storage only: with fp64 the round-1 kernel measured faster in the round)
+    if (!classic && dtype == KR_F32 && one_plus_t >= 1.0 && one_plus_t < 1e30 &&
+        sweep_seg_ok(K, N, es, (reinterpret_cast<uintptr_t>(U) & 15u) == 0)) {
+        const int32_t kind = 1, param = min_horizon;
+        SweepCfg cfg;
+        if (sweep_make_cfg(dtype, K, N, 1, &kind, &one_plus_t, &param, cfg) == KR_OK &&
+            cfg.lut_below == 0) {
+            const int rc = dtype == KR_F64
+                               ? sweep_run_f64(U, R, K, N, 1, cfg.Cc, cfg, nullptr, H, flags, st, max_sms)
+                               : sweep_run_f32(U, R, K, N, 1, cfg.Cc, cfg, nullptr, H, flags, st, max_sms);
+            if (rc != KR_EINVAL) return rc;
+        }
+    }
     const void* bases[1] = {U};
     const float c1 = static_cast<float>(one_plus_t / static_cast<double>(K - 1));
-    cudaStream_t st = as_stream(stream);
     auto go = [&](auto proto, auto kstaged, auto kdirect) {
         using W = decltype(proto);
         constexpr int VC = W::kVC;

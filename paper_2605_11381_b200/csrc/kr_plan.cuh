@@ -169,11 +169,15 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
             }
             per_sm = f.occ_blocks;
         }
+        if (p.max_per_sm > 0 && per_sm > p.max_per_sm) per_sm = p.max_per_sm;
         if (per_sm < 1) per_sm = 1;
         // sharing the GPU (max_sms > 0): one CTA slot per SM stays free so the
-        // side stream's kernels can co-reside where registers are the limit
+        // side stream's kernels can co-reside where registers are the limit.
+        // max_sms < 0: cap at -max_sms SMs with every slot used (kernels whose
+        // own footprint already leaves room, e.g. the segmented decide kernel)
         static const bool keep_slot = std::getenv("KR_SHARED_FULL_SM") == nullptr;  // A/B knob
         if (max_sms > 0 && keep_slot && per_sm > 1) per_sm -= 1;
+        if (max_sms < 0) max_sms = -max_sms;
         int64_t ntiles = (p.R + p.TR - 1) / p.TR;
         int sms = device_info().sm_count;
         if (max_sms > 0 && max_sms < sms) sms = max_sms;

@@ -41,6 +41,7 @@ struct StreamPlan {
     int mode;                            // 0 = TMA bulk, 1 = plain staged, 2 = direct
     int threads;                         // consumer threads (the CTA adds one producer warp)
     int rounds;                          // ceil(TR * items_per_robot / threads) <= kMaxRounds
+    int max_per_sm;                      // resident CTAs per SM cap (0: occupancy decides)
     int64_t R;
 };
 

@@ -6,18 +6,15 @@
 using namespace kr;
 
 
-extern "C" int kr_horizon_sweep(const void* U, int dtype, int64_t R, int32_t K, int32_t N,
-                                int32_t C, const int32_t* kind, const double* one_plus_t,
-                                const int32_t* param, unsigned long long* sums, int32_t* H,
-                                uint32_t* flags, void* stream) {
-    if (R < 0 || K < 2 || N < 1 || C < 1 || C > kSweepMaxCfg || !kind || !one_plus_t || !param ||
-        (dtype != KR_F32 && dtype != KR_F64))
-        return KR_EINVAL;
-    if (R == 0) return KR_OK;
-    if (!U || !sums) return KR_EINVAL;
-    if (N > (kStreamThreads - 32) * kMaxRounds) return KR_EINVAL;
+namespace kr {
+
+// Configuration table of one sweep launch (C <= 64 cells): confidence slots
+// first in ascending 1 + t (stable), outward-rounded ratio bounds, the ratio
+// bucket table and the segmented kernel's clamp.  KR_EINVAL on a bad cell.
+int sweep_make_cfg(int dtype, int32_t K, int32_t N, int32_t C, const int32_t* kind,
+                   const double* one_plus_t, const int32_t* param, SweepCfg& cfg) {
+    cfg = SweepCfg{};
     // configuration table: confidence slots first, ascending 1 + t (stable)
-    SweepCfg cfg{};
     int order[kSweepMaxCfg];
     int Cc = 0;
     for (int c = 0; c < C; c++) {
@@ -141,6 +138,25 @@ extern "C" int kr_horizon_sweep(const void* U, int dtype, int64_t R, int32_t K, 
             if (cfg.hcap[i] > cfg.maxcap) cfg.maxcap = cfg.hcap[i];
         }
     }
+    return KR_OK;
+}
+
+}  // namespace kr
+
+extern "C" int kr_horizon_sweep(const void* U, int dtype, int64_t R, int32_t K, int32_t N,
+                                int32_t C, const int32_t* kind, const double* one_plus_t,
+                                const int32_t* param, unsigned long long* sums, int32_t* H,
+                                uint32_t* flags, void* stream) {
+    if (R < 0 || K < 2 || N < 1 || C < 1 || C > kSweepMaxCfg || !kind || !one_plus_t || !param ||
+        (dtype != KR_F32 && dtype != KR_F64))
+        return KR_EINVAL;
+    if (R == 0) return KR_OK;
+    if (!U || !sums) return KR_EINVAL;
+    if (N > (kStreamThreads - 32) * kMaxRounds) return KR_EINVAL;
+    SweepCfg cfg;
+    const int rc = sweep_make_cfg(dtype, K, N, C, kind, one_plus_t, param, cfg);
+    if (rc != KR_OK) return rc;
+    const int Cc = cfg.Cc;
     cudaStream_t st = as_stream(stream);
     return dtype == KR_F64 ? sweep_run_f64(U, R, K, N, C, Cc, cfg, sums, H, flags, st)
                            : sweep_run_f32(U, R, K, N, C, Cc, cfg, sums, H, flags, st);

@@ -857,7 +857,7 @@ __device__ __forceinline__ void sweep_prologue(SweepTables* tab, const SweepCfg&
 __device__ __forceinline__ void sweep_epilogue(const SweepTables* tab, int Cc, int C, int64_t R,
                                                unsigned long long* sums) {
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && sums) {  // (no sums: a decide-only launch, H is the output)
         uint32_t run = 0;
         for (int c = 0; c < Cc; c++) {
             run += tab->D[c];
@@ -931,10 +931,18 @@ inline int sweep_seg_conflicts(int K, int N, size_t es, bool pair) {
 
 // Launch of the per-dtype sweep kernels (instantiated in kr_sweep_f32.cu /
 // kr_sweep_f64.cu so the two halves compile in parallel).
+// Whether the segmented kernel takes this shape (16 <= N <= 512, windows free
+// of shared-memory bank collisions); otherwise the warp-per-robot kernels.
+inline bool sweep_seg_ok(int K, int N, size_t es, bool aligned16) {
+    static const bool seg_off = std::getenv("KR_SWEEP_NO_SEG") != nullptr;  // A/B knob
+    return !seg_off && N <= 32 * kSegCols && N >= kSegCols &&
+           sweep_seg_conflicts(K, N, es, aligned16 && N % 2 == 0) <= 2;
+}
+
 template <typename T>
 int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t Cc,
               const SweepCfg& cfg, unsigned long long* sums, int32_t* H, uint32_t* flags,
-              cudaStream_t st) {
+              cudaStream_t st, int max_sms) {
     uint64_t rb = static_cast<uint64_t>(K) * N * sizeof(T);
     const void* bases[1] = {U};
     auto go = [&](auto proto, auto kstaged, auto kdirect) -> int {
@@ -972,7 +980,7 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
             w.sfminb = 0; w.sfrng = 0;
         }
         w.H = H; w.sums = sums; w.flags = flags; w.R = R;
-        return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_sweep", 0, cfg);
+        return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_sweep", max_sms, cfg);
     };
     // N > 64 (or a misaligned base): a warp per robot, chunks of 32 lanes x VC
     // columns; VC = 2 (pair loads) when the rows allow it.  (VC = 4 was
@@ -981,9 +989,7 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
 #define KR_SWEEP(KK, VV) \
     return go(SweepWork<T, KK, VV>{}, k_horizon_sweep<T, KK, VV, true>, k_horizon_sweep<T, KK, VV, false>)
     // segmented sweep: G lanes per robot, <= kSegCols columns per lane
-    static const bool seg_off = std::getenv("KR_SWEEP_NO_SEG") != nullptr;  // A/B knob
-    if (!seg_off && N <= 32 * kSegCols && N >= kSegCols &&
-        sweep_seg_conflicts(K, N, sizeof(T), al && N % 2 == 0) <= 2) {
+    if (sweep_seg_ok(K, N, sizeof(T), al)) {
         int G = 1;
         while (G * kSegCols < N) G <<= 1;
         const bool pair = al && N % 2 == 0;
@@ -994,10 +1000,17 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
             using W = decltype(proto);
             static const int tr_env = std::getenv("KR_SWEEP_TR") ? std::atoi(std::getenv("KR_SWEEP_TR")) : 0;
             static const int cw_env = std::getenv("KR_SWEEP_CW") ? std::atoi(std::getenv("KR_SWEEP_CW")) : 0;
-            const int tr = tr_env > 0 ? tr_env : (cw_env > 0 ? cw_env : 5) * RW;
+            // 4 consumer warps (+ the producer) per CTA, two CTAs per SM: the HBM
+            // peak from ~8 deciding warps per SM (2 to 10 measured equal alone;
+            // beside the round's side stream 4 was best, profiles/r2_confidence_layouts.jsonl)
+            const int tr = tr_env > 0 ? tr_env : (cw_env > 0 ? cw_env : 4) * RW;
             const uint32_t task_bytes = static_cast<uint32_t>((tr * G + 31) / 32) * 32 * kSegCols * 2;
+            static const int st_env = std::getenv("KR_SWEEP_STAGES") ? std::atoi(std::getenv("KR_SWEEP_STAGES")) : 0;
+            static const int psm_env = std::getenv("KR_SWEEP_PERSM") ? std::atoi(std::getenv("KR_SWEEP_PERSM")) : 0;
             StreamPlan p = make_plan(1, bases, &rb, R, G, 0, kSegThreads - 32, kernel_regs(kstaged), 1,
-                                     static_cast<uint32_t>(sizeof(SweepTables)) + task_bytes, tr);
+                                     static_cast<uint32_t>(sizeof(SweepTables)) + task_bytes, tr,
+                                     st_env >= 2 ? st_env : kMaxStages);
+            p.max_per_sm = psm_env;
             if ((R / device_info().sm_count + 1) * static_cast<int64_t>(N) >= (int64_t(1) << 32))
                 return KR_EINVAL;
             W w{};
@@ -1031,7 +1044,10 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
                 w.sfminb1 = ~typename W::B(0);
             }
             w.H = H; w.sums = sums; w.flags = flags; w.R = R;
-            return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_sweep", 0, cfg);
+            // sharing (max_sms > 0): this kernel's CTAs already leave registers and
+            // warp slots to the side stream, so every CTA slot of the capped SMs is used
+            return launch_stream(kstaged, kdirect, p, w, st, "kr_horizon_sweep",
+                                 max_sms > 0 ? -max_sms : max_sms, cfg);
         };
 #define KR_SEG(KK, VV, CC)                                                   \
     return go_seg(SweepSeg<T, KK, VV, CC>{}, k_horizon_sweep_seg<T, KK, VV, CC, true>, \
@@ -1067,9 +1083,11 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
 
 int sweep_run_f32(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t Cc,
                   const SweepCfg& cfg, unsigned long long* sums, int32_t* H, uint32_t* flags,
-                  cudaStream_t st);
+                  cudaStream_t st, int max_sms = 0);
 int sweep_run_f64(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t Cc,
                   const SweepCfg& cfg, unsigned long long* sums, int32_t* H, uint32_t* flags,
-                  cudaStream_t st);
+                  cudaStream_t st, int max_sms = 0);
+int sweep_make_cfg(int dtype, int32_t K, int32_t N, int32_t C, const int32_t* kind,
+                   const double* one_plus_t, const int32_t* param, SweepCfg& cfg);
 
 }  // namespace kr

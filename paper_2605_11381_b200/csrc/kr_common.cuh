@@ -416,6 +416,10 @@ __device__ __forceinline__ int64_t us_from_actions(int64_t count, int64_t hz_num
 // Wait ledger (waiting.py:69-93), wait ratio (waiting.py:62-66, 96-100),
 // bucket (scheduler.py:79-88)
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void l2_prefetch(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 struct Slot {
     int64_t gs, ge, es, ee;
 };
@@ -482,8 +486,9 @@ __device__ __forceinline__ void history_walk(const int64_t* slots, int32_t n_exe
     total = round_wait(s0, s1.gs, s1.es, 0, n_exec, n_gen);
     if (n_exec > 1) total += round_wait(s1, s2.gs, s2.es, 1, n_exec, n_gen);
     if (n_exec > 2) total += round_wait(s2, s3.gs, s3.es, 2, n_exec, n_gen);
-    const Slot& l = n_exec == 1 ? s0 : n_exec == 2 ? s1 : n_exec == 3 ? s2 : s3;
-    last = l.ee - l.es;
+    // by value (a reference to one of the four would put them in local memory)
+    last = n_exec == 1 ? s0.ee - s0.es : n_exec == 2 ? s1.ee - s1.es : n_exec == 3 ? s2.ee - s2.es
+                                                                                  : s3.ee - s3.es;
     if (n_exec > 3) {  // rounds 3 .. n_exec-1
         Slot cur = s3;
         for (int32_t j = 3; j < n_exec; j++) {

@@ -74,14 +74,6 @@ __device__ __forceinline__ void slot_waits(const int64_t* slots, int32_t n_exec,
     }
 }
 
-__device__ __forceinline__ unsigned long long wor(unsigned long long v) {
-    for (int o = 16; o; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-__device__ __forceinline__ unsigned long long wand(unsigned long long v) {
-    for (int o = 16; o; o >>= 1) v &= __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
 // Per-request inputs of the urgency pass.  FleetSrc: one self-contained
 // structure-of-arrays per planning round (history as CSR slots, walked per
@@ -107,6 +99,22 @@ struct FleetSrc {
         slot_waits(f.slots + 4 * __ldg(f.hist_off + i), __ldg(f.n_exec + i), __ldg(f.n_gen + i),
                    out + __ldg(f.hist_off + i));
     }
+    // L2 prefetch of request i's fields (its history span follows in slots_l2)
+    __device__ __forceinline__ int64_t fields_l2(int64_t i) const {
+        l2_prefetch(f.issued_at + i);
+        l2_prefetch(f.lexrank + i);
+        l2_prefetch(f.remaining + i);
+        l2_prefetch(f.skipped + i);
+        l2_prefetch(f.n_exec + i);
+        l2_prefetch(f.n_gen + i);
+        l2_prefetch(f.t_start + i);
+        return __ldg(f.hist_off + i);
+    }
+    __device__ __forceinline__ void slots_l2(int64_t off) const {
+        const int64_t* p = f.slots + 4 * off;
+        l2_prefetch(p);
+        l2_prefetch(p + 16);  // the next 128 bytes (histories of more than 4 slots are rare)
+    }
 };
 
 struct LedgerSrc {
@@ -130,6 +138,8 @@ struct LedgerSrc {
         }
     }
     __device__ void waits(int64_t, int64_t*) const {}
+    __device__ __forceinline__ int64_t fields_l2(int64_t) const { return 0; }
+    __device__ __forceinline__ void slots_l2(int64_t) const {}
 };
 
 // Per-launch constants of the urgency pass, prepared on the host from kr_sched:
@@ -178,26 +188,29 @@ __device__ __forceinline__ int32_t assign_bucket32(double wr, int32_t skipped, i
 }
 
 // One request: its packed key (and the optional intermediates / need time).
-template <class Src>
+// LEAN: the planning round's case decided at compile time -- Kairos keys, the
+// need time, no intermediates -- so no per-request policy or output tests.
+template <class Src, bool LEAN = false>
 __device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, const UrgConst& u,
                                               const UrgencyOut& o, int64_t i, uint32_t& fl) {
     const int64_t issued = s.issued(i);
     const int32_t rank = s.rank(i);
-    if (o.need_time) {
+    const int32_t policy = LEAN ? KR_KAIROS : c.policy;
+    if (LEAN || o.need_time) {
         int32_t rem = s.remaining(i);
         o.need_time[i] = issued + us_from_actions32(rem, c, u, &fl);
     }
     kr_key key;
-    if (c.policy == KR_FIFO) {
+    if (policy == KR_FIFO) {
         key.hi = static_cast<uint64_t>(issued) ^ (uint64_t(1) << 63);
         key.lo = static_cast<uint64_t>(static_cast<uint32_t>(rank));
         if (rank < 0) fl |= KR_FLAG_KEY_RANGE;
-    } else if (c.policy == KR_LAS) {
+    } else if (policy == KR_LAS) {
         key.hi = static_cast<uint64_t>(s.accum(i)) ^ (uint64_t(1) << 63);
         key.lo = issued_rank_word(issued, c.issued_base, rank, &fl);
     }
     const bool need_hist =
-        c.policy == KR_KAIROS || o.total_wait || o.wr || o.bucket || o.est || o.slot_wait;
+        policy == KR_KAIROS || (!LEAN && (o.total_wait || o.wr || o.bucket || o.est || o.slot_wait));
     if (need_hist) {
         const int32_t skipped = s.skipped(i);
         int64_t w, t0, last = 0;
@@ -206,13 +219,15 @@ __device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, c
         double wr = wait_ratio(w, t0, c.now, &fl);
         int32_t b = assign_bucket32(wr, skipped, c.buckets, c.aging_interval, u.aging);
         const int64_t est = ne > 0 ? last : c.default_exec_estimate;
-        if (o.total_wait) o.total_wait[i] = w;
-        if (o.wr) o.wr[i] = wr;
-        if (o.bucket) o.bucket[i] = b;
-        if (o.est) o.est[i] = est;
-        if constexpr (Src::kSlots)
-            if (o.slot_wait) s.waits(i, o.slot_wait);
-        if (c.policy == KR_KAIROS) {
+        if constexpr (!LEAN) {
+            if (o.total_wait) o.total_wait[i] = w;
+            if (o.wr) o.wr[i] = wr;
+            if (o.bucket) o.bucket[i] = b;
+            if (o.est) o.est[i] = est;
+            if constexpr (Src::kSlots)
+                if (o.slot_wait) s.waits(i, o.slot_wait);
+        }
+        if (policy == KR_KAIROS) {
             // aged = est * (1 + skipped), descending -> stored complemented;
             // clamped at 2^56 - 1 (the 128-bit product of the original
             // formulation: a negative multiplier wraps to a huge value)
@@ -239,31 +254,51 @@ __device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, c
 #ifndef KR_URG_MINB
 #define KR_URG_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
-template <class Src, class Idx>
+template <class Src, class Idx, bool LEAN = false>
 __global__ void __launch_bounds__(256, KR_URG_MINB) k_urgency(Src s, kr_sched c, UrgConst u,
                                                               UrgencyOut o) {
+    // select statistics (OR / AND of the keys) per thread, then per warp and
+    // block (a per-iteration redux.sync variant measured 4% slower)
+    __shared__ uint32_t red[8];  // OR hi.hi, hi.lo, lo.hi, lo.lo | AND (same order)
+    if (threadIdx.x < 8) red[threadIdx.x] = threadIdx.x < 4 ? 0u : ~0u;
+    __syncthreads();
     uint32_t fl = 0;
-    unsigned long long ohi = 0, olo = 0, ahi = ~0ull, alo = ~0ull;
     const Idx n = static_cast<Idx>(s.n());
-    for (Idx i = blockIdx.x * Idx(blockDim.x) + threadIdx.x; i < n; i += Idx(gridDim.x) * blockDim.x) {
-        const kr_key key = urgency_one(s, c, u, o, i, fl);
+    const bool stats = o.key_stats != nullptr;
+    unsigned long long ohi = 0, olo = 0, ahi = ~0ull, alo = ~0ull;
+    const Idx stride = Idx(gridDim.x) * blockDim.x;
+    for (Idx i = blockIdx.x * Idx(blockDim.x) + threadIdx.x; i < n; i += stride) {
+        // the next request's fields into L2 now, its history span after this
+        // request is done: the next iteration's two dependent loads hit L2
+        const Idx nx = i + stride;
+        int64_t off_nx = 0;
+        if (Src::kSlots && nx < n) off_nx = s.fields_l2(nx);
+        const kr_key key = urgency_one<Src, LEAN>(s, c, u, o, i, fl);
+        if (Src::kSlots && nx < n) s.slots_l2(off_nx);
         o.keys[i] = key;
         ohi |= key.hi; olo |= key.lo; ahi &= key.hi; alo &= key.lo;
     }
-    if (fl && o.flags) atomicOr(o.flags, fl);
-    if (o.key_stats) {  // block-reduced OR / AND of the keys (select statistics)
-        __shared__ unsigned long long red[4][8];
-        ohi = wor(ohi); olo = wor(olo); ahi = wand(ahi); alo = wand(alo);
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        if (lane == 0) {
-            red[0][warp] = ohi; red[1][warp] = olo; red[2][warp] = ahi; red[3][warp] = alo;
+    if (stats) {  // warp-reduced, then eight shared words per block
+#pragma unroll
+        for (int t = 16; t; t >>= 1) {
+            ohi |= __shfl_xor_sync(0xffffffffu, ohi, t); olo |= __shfl_xor_sync(0xffffffffu, olo, t);
+            ahi &= __shfl_xor_sync(0xffffffffu, ahi, t); alo &= __shfl_xor_sync(0xffffffffu, alo, t);
         }
+        if ((threadIdx.x & 31) == 0) {
+            atomicOr(&red[0], static_cast<uint32_t>(ohi >> 32)); atomicOr(&red[1], static_cast<uint32_t>(ohi));
+            atomicOr(&red[2], static_cast<uint32_t>(olo >> 32)); atomicOr(&red[3], static_cast<uint32_t>(olo));
+            atomicAnd(&red[4], static_cast<uint32_t>(ahi >> 32)); atomicAnd(&red[5], static_cast<uint32_t>(ahi));
+            atomicAnd(&red[6], static_cast<uint32_t>(alo >> 32)); atomicAnd(&red[7], static_cast<uint32_t>(alo));
+        }
+    }
+    if (fl && o.flags) atomicOr(o.flags, fl);
+    if (stats) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            const int nw = (blockDim.x + 31) >> 5;
-            for (int w = 1; w < nw; w++) {
-                ohi |= red[0][w]; olo |= red[1][w]; ahi &= red[2][w]; alo &= red[3][w];
-            }
+            const unsigned long long ohi = (static_cast<unsigned long long>(red[0]) << 32) | red[1];
+            const unsigned long long olo = (static_cast<unsigned long long>(red[2]) << 32) | red[3];
+            const unsigned long long ahi = (static_cast<unsigned long long>(red[4]) << 32) | red[5];
+            const unsigned long long alo = (static_cast<unsigned long long>(red[6]) << 32) | red[7];
             if (ohi) atomicOr(&o.key_stats[0], ohi);
             if (olo) atomicOr(&o.key_stats[1], olo);
             if (~ahi) atomicAnd(&o.key_stats[2], ahi);
@@ -286,7 +321,13 @@ template <class Src>
 static void launch_urgency(const Src& src, int64_t n, const kr_sched& c, const UrgencyOut& o,
                            cudaStream_t st) {
     const UrgConst u = urg_const(c);
-    if (n < (int64_t(1) << 31)) {
+    static const bool lean_off = std::getenv("KR_URG_NO_LEAN") != nullptr;  // A/B knob
+    const bool lean = !lean_off && c.policy == KR_KAIROS && o.need_time && !o.total_wait && !o.wr &&
+                      !o.bucket && !o.est && !o.slot_wait;
+    if (lean && n < (int64_t(1) << 31)) {
+        static int per_sm = occupancy(k_urgency<Src, int32_t, true>, 256);
+        k_urgency<Src, int32_t, true><<<grid_cap(n, 256, per_sm), 256, 0, st>>>(src, c, u, o);
+    } else if (n < (int64_t(1) << 31)) {
         static int per_sm = occupancy(k_urgency<Src, int32_t>, 256);
         k_urgency<Src, int32_t><<<grid_cap(n, 256, per_sm), 256, 0, st>>>(src, c, u, o);
     } else {

@@ -27,9 +27,16 @@ for path in sys.argv[1:] * 2:
                        None, None, None, None, None, stats.data_ptr(), None, dev.stream())
     for _ in range(5):
         run()
+    # captured: 20 launches per graph, device time per launch (no host gaps)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        for _ in range(20):
+            run()
+    g.replay()
     ts = []
-    for _ in range(30):
+    for _ in range(10):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(); run(); b.record(); torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    print(Path(path).name, "median ms", round(statistics.median(ts), 4))
+        a.record(); g.replay(); b.record(); torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 20)
+    print(Path(path).name, "median ms per launch (graph)", round(statistics.median(ts), 4))

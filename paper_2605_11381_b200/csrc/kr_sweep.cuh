@@ -882,10 +882,20 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p
     sweep_epilogue(tab, w.Cc, w.C, w.R, w.sums);
 }
 
-constexpr int kSegThreads = 512;  // <= 128 registers per thread
+// Register budget: 80 per thread (__launch_bounds__(384, 2)).  128 measured
+// 1% faster alone, but 80 leaves room on every SM for the planning round's
+// side stream (urgency: 2 CTAs of 256 threads at 64 registers beside the two
+// decide CTAs): confidence round 266 -> 258 us (profiles/r2_confidence_layouts.jsonl).
+#ifndef KR_SEG_THREADS
+#define KR_SEG_THREADS 384
+#endif
+#ifndef KR_SEG_MINB
+#define KR_SEG_MINB 2
+#endif
+constexpr int kSegThreads = KR_SEG_THREADS;
 
 template <typename T, int KC, int VW, int CPL, bool kStaged>
-__global__ void __launch_bounds__(kSegThreads) k_horizon_sweep_seg(StreamPlan p, SweepSeg<T, KC, VW, CPL> w,
+__global__ void __launch_bounds__(kSegThreads, KR_SEG_MINB) k_horizon_sweep_seg(StreamPlan p, SweepSeg<T, KC, VW, CPL> w,
                                                                     const __grid_constant__ SweepCfg cfg) {
     extern __shared__ __align__(128) unsigned char smem[];
     SweepTables* const tab = w.tables();

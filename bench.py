@@ -624,23 +624,27 @@ def other_configs(reps: int = 200):
     rnd.set_cloud(eng.transfer_time_batch(net, payload, eng.UP),
                   eng.cloud_thresholds(edge, cloud, net, 0, 0, k, rnd.cap))
     inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
+    # eager (the offload scan reads its slot count back: one sync), overlapped
+    # like the graph rounds: urgency, then horizons || the admission side stream
+    # (tests/test_gpu_hybrid_round.py: identical decisions to the sequential round)
+    step = lambda: rnd.run_overlapped(fleet, inp, reserve_sms=10, layout="urgency_first")
     for _ in range(5):
-        rnd.run(fleet, inp)
+        step()
     torch.cuda.synchronize()
     n_cloud = int(rnd.n_cloud.item())
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps // 4):
-        rnd.run(fleet, inp)  # eager: the full sort reads its pass plan back (one sync)
+        step()
     b.record()
     torch.cuda.synchronize()
     t = a.elapsed_time(b) / 1e3 / (reps // 4)
     out["configs[4] per-GPU share with a cloud tier (k=8192 edge, 2048 cloud slots)"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t, "cloud_placed": n_cloud,
         "full_sorts": rnd.full_sorts,
-        "layout": "eager, sequential: horizons, urgency, ordered top k + 4096 (fused select), "
-                  "edge admission, ordered offload scan, one 4-byte read of the slot count "
-                  "(rounds.HybridDecisionRound)"}
+        "layout": "eager, overlapped: urgency, then horizons (138 SMs) || ordered top k + 4096 "
+                  "(fused select), edge admission, ordered offload scan, one 4-byte read of the "
+                  "slot count (rounds.HybridDecisionRound.run_overlapped)"}
     return out
 
 

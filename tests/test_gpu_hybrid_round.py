@@ -128,3 +128,41 @@ def test_hybrid_round_matches_plan_at_scale(kb, window):
     assert deferred == [[r.task_id, r.skipped] for r in p.deferred]
     assert refetch == sorted(p.refetch_task_ids)
     assert skipped == {t: s.skipped for t, s in states.items()}
+
+
+@pytest.mark.parametrize("layout,reserve", [("urgency_first", 10), ("split", 10), ("split", -1)])
+def test_hybrid_round_overlapped_equals_sequential(kb, layout, reserve):
+    """The bench's overlapped hybrid round (horizons on the main stream, the
+    urgency / admission / offload scan with its one 4-byte read on a side
+    stream) decides exactly what the sequential round decides, over several
+    evolving rounds of a 2^17-robot fleet."""
+    from paper_2605_11381_b200 import engines as eng, fleet as fl, rounds, synthetic
+    R, k = 1 << 17, 4096
+    soa = synthetic.fleet_soa(R, seed=30)
+    prev, cand, off = synthetic.chunks(R, seed=31)
+    edge = kb.EngineProfile(tier="edge", capacity=k, max_batch=256, points=((1, 150_000), (256, 400_000)))
+    cloud = kb.EngineProfile(tier="cloud", capacity=1024, max_batch=512, points=((1, 80_000), (512, 250_000)))
+    net = kb.NetworkModel(base_latency_us=20_000, uplink_bps=400_000_000, downlink_bps=1_000_000_000)
+    sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    payload = torch.from_numpy(np.random.default_rng(32).choice(
+        np.array([100_000, 300_000, 2_000_000], np.int64), R)).cuda()
+    inp = rounds.DivergenceInputs(prev, cand, 0.9, offset=off)
+    outs = []
+    for overlapped in (False, True):
+        fleet = fl.DeviceFleet.from_host(soa)
+        rnd = rounds.HybridDecisionRound(R, k, sched, cloud.capacity)
+        rnd.set_cloud(eng.transfer_time_batch(net, payload, eng.UP),
+                      eng.cloud_thresholds(edge, cloud, net, 0, 0, k, rnd.cap))
+        seq = []
+        for _ in range(3):  # skip counters evolve between rounds
+            o = (rnd.run_overlapped(fleet, inp, reserve_sms=reserve, layout=layout) if overlapped
+                 else rnd.run(fleet, inp))
+            torch.cuda.synchronize()
+            seq.append([t.cpu().clone() for t in (o.horizon, o.admitted, o.refetch, o.edge_idx,
+                                                 rnd.cloud(), fleet.t["skipped"])])
+        outs.append(seq)
+    for a, b in zip(*outs):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
+    assert outs[0][0][4].numel() > 0  # the cloud tier placed requests

@@ -882,20 +882,23 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_horizon_sweep(StreamPlan p
     sweep_epilogue(tab, w.Cc, w.C, w.R, w.sums);
 }
 
-// Register budget: 80 per thread (__launch_bounds__(384, 2)).  128 measured
-// 1% faster alone, but 80 leaves room on every SM for the planning round's
-// side stream (urgency: 2 CTAs of 256 threads at 64 registers beside the two
-// decide CTAs): confidence round 266 -> 258 us (profiles/r2_confidence_layouts.jsonl).
-#ifndef KR_SEG_THREADS
-#define KR_SEG_THREADS 384
-#endif
-#ifndef KR_SEG_MINB
-#define KR_SEG_MINB 2
-#endif
-constexpr int kSegThreads = KR_SEG_THREADS;
+// Register budget.  LEAN (decide-only launches of the fp32 pair kernel, i.e.
+// confidence horizons beside the planning round's side stream) is held to 80
+// registers (__launch_bounds__(384, 2)): 128 measured 1% faster alone, but 80
+// leaves room on every SM for the side stream (urgency: 2 CTAs of 256 threads
+// at 64 registers beside the two decide CTAs), confidence round 266 -> 258 us
+// (profiles/r2_confidence_layouts.jsonl).  Sweeps keep 128: at 80 the exact
+// path spills (tie-heavy sweep 0.67 -> 0.79 ms, fp64 0.49 -> 0.59 ms).
+template <bool LEAN>
+struct SegBounds {
+    static constexpr int kThreads = LEAN ? 384 : 512;
+    static constexpr int kMinBlocks = LEAN ? 2 : 1;
+};
+constexpr int kSegThreads = 384;  // largest CTA the launcher plans (<= both bounds)
 
-template <typename T, int KC, int VW, int CPL, bool kStaged>
-__global__ void __launch_bounds__(kSegThreads, KR_SEG_MINB) k_horizon_sweep_seg(StreamPlan p, SweepSeg<T, KC, VW, CPL> w,
+template <typename T, int KC, int VW, int CPL, bool kStaged, bool LEAN = false>
+__global__ void __launch_bounds__(SegBounds<LEAN>::kThreads, SegBounds<LEAN>::kMinBlocks)
+k_horizon_sweep_seg(StreamPlan p, SweepSeg<T, KC, VW, CPL> w,
                                                                     const __grid_constant__ SweepCfg cfg) {
     extern __shared__ __align__(128) unsigned char smem[];
     SweepTables* const tab = w.tables();
@@ -1010,10 +1013,11 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
             using W = decltype(proto);
             static const int tr_env = std::getenv("KR_SWEEP_TR") ? std::atoi(std::getenv("KR_SWEEP_TR")) : 0;
             static const int cw_env = std::getenv("KR_SWEEP_CW") ? std::atoi(std::getenv("KR_SWEEP_CW")) : 0;
-            // 4 consumer warps (+ the producer) per CTA, two CTAs per SM: the HBM
-            // peak from ~8 deciding warps per SM (2 to 10 measured equal alone;
-            // beside the round's side stream 4 was best, profiles/r2_confidence_layouts.jsonl)
-            const int tr = tr_env > 0 ? tr_env : (cw_env > 0 ? cw_env : 4) * RW;
+            // consumer warps (+ the producer) per CTA, two CTAs per SM: sweeps 5
+            // (4 and 5 equal on the common shape, 5 better for fp64 / odd N / ties,
+            // 6 leaves one CTA per SM); decide-only launches 4, best beside the
+            // round's side stream (profiles/r2_confidence_layouts.jsonl)
+            const int tr = tr_env > 0 ? tr_env : (cw_env > 0 ? cw_env : (sums ? 5 : 4)) * RW;
             const uint32_t task_bytes = static_cast<uint32_t>((tr * G + 31) / 32) * 32 * kSegCols * 2;
             static const int st_env = std::getenv("KR_SWEEP_STAGES") ? std::atoi(std::getenv("KR_SWEEP_STAGES")) : 0;
             static const int psm_env = std::getenv("KR_SWEEP_PERSM") ? std::atoi(std::getenv("KR_SWEEP_PERSM")) : 0;
@@ -1062,8 +1066,17 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
 #define KR_SEG(KK, VV, CC)                                                   \
     return go_seg(SweepSeg<T, KK, VV, CC>{}, k_horizon_sweep_seg<T, KK, VV, CC, true>, \
                   k_horizon_sweep_seg<T, KK, VV, CC, false>)
+#define KR_SEG_LEAN(KK)                                                                         \
+    return go_seg(SweepSeg<T, KK, 2, 14>{}, k_horizon_sweep_seg<T, KK, 2, 14, true, true>,   \
+                  k_horizon_sweep_seg<T, KK, 2, 14, false, true>)
         if (pair) {
             if (c14) {
+                if constexpr (sizeof(T) == 4) {
+                    if (!sums) {  // decide-only (confidence horizons): the lean register budget
+                        if (K == 6) KR_SEG_LEAN(6);
+                        KR_SEG_LEAN(0);
+                    }
+                }
                 if (K == 6) KR_SEG(6, 2, 14);
                 KR_SEG(0, 2, 14);
             }
@@ -1073,6 +1086,7 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
         if (K == 6) KR_SEG(6, 1, 16);
         KR_SEG(0, 1, 16);
 #undef KR_SEG
+#undef KR_SEG_LEAN
     }
     // two robots per warp: N <= 64 (pair loads when N is even and the base 16-byte aligned)
     static const bool half_off = std::getenv("KR_SWEEP_NO_HALF") != nullptr;  // A/B knob

@@ -846,6 +846,47 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
     }
 }
 
+// Grouped rank merge: sorted runs of length L, merged G at a time (G a power
+// of two <= 32): a sub-warp of G lanes per pair, lane j counting the pairs
+// smaller than it in run j of the pair's group (one binary search of log2 L
+// dependent probes), the sub-warp sums, lane 0 scatters the pair to its rank
+// inside the group's output segment.  Repeated passes (G = 8 until at most 8
+// runs remain) replace one pass against every other run: at 16k pairs
+// (64 runs) 2 passes of 7 searches instead of 63 searches per pair.
+__global__ void __launch_bounds__(256) k_run_merge_group(const kr_key* rk, const int32_t* ri,
+                                                         const unsigned int* count_dev, int m_host,
+                                                         int L, int lgG, int32_t* out_idx,
+                                                         kr_key* out_keys) {
+    const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
+    const int G = 1 << lgG;
+    const int nruns = (m + L - 1) / L;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);
+    const int spw = 32 >> lgG;  // pairs per warp
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t e0 = warp * spw; e0 < m; e0 += nwarps * spw) {  // warp-uniform
+        const int e = static_cast<int>(e0) + (lane >> lgG);
+        const bool ok = e < m;
+        kr_key x{0, 0};
+        int32_t xi = 0;
+        int run = 0, c = 0;
+        if (ok) {
+            x = rk[e];
+            xi = ri[e];
+            run = e / L;
+            const int r = (run & ~(G - 1)) + gl;
+            if (r != run && r < nruns) c = count_less(rk, ri, r * L, min(r * L + L, m), x, xi);
+        }
+        for (int o = G >> 1; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (ok && gl == 0) {
+            const int pos = (run & ~(G - 1)) * L + c + (e - run * L);
+            if (out_idx) out_idx[pos] = xi;
+            if (out_keys) out_keys[pos] = x;
+        }
+    }
+}
+
 // The same rank merge with every 16th pair of every run staged in shared
 // memory (m <= kMergeSampled): a lane finds its run's 16-pair window among the
 // samples, then counts inside the window with 15 independent loads -- one
@@ -1160,6 +1201,42 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
         // runs are written to the sort ping-pong buffer not holding the input
         kr_key* rk = keys == w.skeys[1] ? w.skeys[0] : w.skeys[1];
         int32_t* ri = keys == w.skeys[1] ? w.sidx[0] : w.sidx[1];
+        // more than 32 runs (> 8k pairs): grouped merge passes (both outputs
+        // given), G = 8 until at most 8 runs remain, the runs ping-ponging
+        // between the outputs and the select's candidate buffers (unused by
+        // every sort_pairs caller), landing in out.  Up to 32 runs the flat
+        // merge's one search per lane is faster (4k pairs: 22 vs 27 us).
+        static const bool grouped_off = std::getenv("KR_MERGE_FLAT") != nullptr;  // A/B knob
+        const int runs0 = (m + kRun - 1) / kRun;
+        if (!grouped_off && out_idx && out_keys && runs0 > 32) {
+            int lg[8], P = 0;
+            for (int r = runs0; r > 1 && P < 8; P++) {
+                int g = 0;
+                while ((1 << g) < r && g < 3) g++;
+                lg[P] = g;
+                r = (r + (1 << g) - 1) >> g;
+            }
+            kr_key* tk = w.cand[0];
+            int32_t* ti = reinterpret_cast<int32_t*>(w.cand[1]);
+            // the run sort's target: out when an even number of passes follows
+            kr_key* ck = P % 2 == 0 ? out_keys : tk;
+            int32_t* ci = P % 2 == 0 ? out_idx : ti;
+            k_run_sort<<<(m + kRun - 1) / kRun, kRunThreads, 0, st>>>(sk, si, count_dev, m, ck, ci);
+            int L = kRun;
+            for (int q = 0; q < P; q++) {
+                kr_key* dk = (P - 1 - q) % 2 == 0 ? out_keys : tk;
+                int32_t* di = (P - 1 - q) % 2 == 0 ? out_idx : ti;
+                const int64_t warps = (static_cast<int64_t>(m) + (32 >> lg[q]) - 1) / (32 >> lg[q]);
+                int64_t blocks = (warps + 7) / 8;
+                if (blocks > 148 * 64) blocks = 148 * 64;
+                k_run_merge_group<<<static_cast<unsigned>(blocks), 256, 0, st>>>(ck, ci, count_dev, m, L,
+                                                                                lg[q], di, dk);
+                ck = dk;
+                ci = di;
+                L <<= lg[q];
+            }
+            return check_launch("run sort (grouped merge)", 1 + P);
+        }
         k_run_sort<<<(m + kRun - 1) / kRun, kRunThreads, 0, st>>>(sk, si, count_dev, m, rk, ri);
         const int64_t warps = m;
         int64_t blocks = (warps + 7) / 8;

@@ -508,6 +508,10 @@ __device__ __forceinline__ double wait_ratio(int64_t total, int64_t t_start, int
     int64_t life = now - t_start;
     const int64_t lim = int64_t(1) << 53;
     if (total >= lim || total <= -lim || life >= lim) *flag_bits |= KR_FLAG_RATIO;
+    // 0 / life = 0.0 exactly; a zero numerator is also outside the division's
+    // fast-path range, and one such lane sent the whole warp through the slow
+    // path (~90 instructions per request in the urgency pass)
+    if (total == 0) return 0.0;
     double r = ddiv(static_cast<double>(total), static_cast<double>(life));
     r = r > 0.0 ? r : 0.0;
     return r < 1.0 ? r : 1.0;

@@ -32,7 +32,7 @@
 
 static PyObject *s_task_id, *s_gen_starts, *s_gen_ends, *s_exec_intervals, *s_t_start,
     *s_issued_at, *s_obs_captured_at, *s_accumulated_generation, *s_last_exec_info,
-    *s_remaining_actions, *s_skipped, *s_start, *s_end;
+    *s_remaining_actions, *s_skipped, *s_start, *s_end, *s_dict, *s_dc_fields;
 
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
@@ -198,9 +198,112 @@ done:
     return result;
 }
 
+/* dataclasses.replace(req, skipped=skipped) for a validated request
+ * (scheduler.py:232-234): a new instance of the same class whose __dict__ is a
+ * copy of the original's with `skipped` replaced; classes without a __dict__
+ * go through the Python fallback `bump(req, skipped)`. */
+static PyObject* bumped(PyObject* req, long skipped, PyObject* bump) {
+    /* not a dataclass (replace() raises there) or no __dict__: the fallback */
+    PyObject* d = PyObject_HasAttr((PyObject*)Py_TYPE(req), s_dc_fields)
+                      ? PyObject_GetAttr(req, s_dict) : NULL;
+    if (!d || !PyDict_Check(d)) {
+        PyErr_Clear();
+        Py_XDECREF(d);
+        return PyObject_CallFunction(bump, "Ol", req, skipped);
+    }
+    PyObject* empty = PyTuple_New(0);
+    PyObject* obj = empty ? PyBaseObject_Type.tp_new(Py_TYPE(req), empty, NULL) : NULL;
+    Py_XDECREF(empty);
+    PyObject* nd = obj ? PyObject_GetAttr(obj, s_dict) : NULL;
+    PyObject* sk = nd ? PyLong_FromLong(skipped) : NULL;
+    if (!sk || PyDict_Update(nd, d) || PyDict_SetItem(nd, s_skipped, sk)) {
+        Py_XDECREF(sk); Py_XDECREF(nd); Py_XDECREF(obj); Py_DECREF(d);
+        return NULL;
+    }
+    Py_DECREF(sk); Py_DECREF(nd); Py_DECREF(d);
+    return obj;
+}
+
+/* The plan's result objects from the device's one read-back (scheduler.py
+ * _place's tail, scheduler.py:223-241):
+ *   finish(reqs, states, order_addr, refetch_addr, skipped_addr, n, k,
+ *          cloud_addr, bump) -> (edge tuple, deferred tuple, refetch frozenset)
+ * order: int32 [n] request indices in plan order; refetch, skipped, cloud
+ * (cloud_addr 0: no cloud tier): int32 [n] by request index.  Every task's
+ * TaskState.skipped is set to its request's updated counter; the deferred
+ * requests (plan order after the first k, the offloaded ones excluded) are
+ * bumped copies. */
+static PyObject* finish(PyObject* self, PyObject* args) {
+    (void)self;
+    PyObject *reqs_in, *states, *bump;
+    Py_ssize_t oa, ra, sa, ca, n, k;
+    if (!PyArg_ParseTuple(args, "OOnnnnnnO", &reqs_in, &states, &oa, &ra, &sa, &n, &k, &ca, &bump))
+        return NULL;
+    PyObject* reqs = PySequence_Fast(reqs_in, "reqs must be a sequence");
+    if (!reqs) return NULL;
+    if (PySequence_Fast_GET_SIZE(reqs) != n || k < 0 || k > n) {
+        Py_DECREF(reqs);
+        PyErr_SetString(PyExc_ValueError, "finish: inconsistent sizes");
+        return NULL;
+    }
+    PyObject** R = PySequence_Fast_ITEMS(reqs);
+    const int32_t* order = (const int32_t*)oa;
+    const int32_t* refetch = (const int32_t*)ra;
+    const int32_t* skipped = (const int32_t*)sa;
+    const int32_t* cloud = (const int32_t*)ca;
+    Py_ssize_t nd = 0;
+    for (Py_ssize_t p = k; p < n; p++) nd += !(cloud && cloud[order[p]]);
+    PyObject* edge = PyTuple_New(k);
+    PyObject* deferred = PyTuple_New(nd);
+    PyObject* ref = PySet_New(NULL);
+    PyObject* result = NULL;
+    if (!edge || !deferred || !ref) goto done;
+    Py_ssize_t q = 0;
+    for (Py_ssize_t p = 0; p < n; p++) {
+        const int32_t j = order[p];
+        if (j < 0 || j >= n) {
+            PyErr_SetString(PyExc_ValueError, "finish: order index out of range");
+            goto done;
+        }
+        PyObject* req = R[j];
+        PyObject* tid = PyObject_GetAttr(req, s_task_id);
+        if (!tid) goto done;
+        PyObject* st = PyObject_GetItem(states, tid);
+        PyObject* sk = st ? PyLong_FromLong(skipped[j]) : NULL;
+        int bad = !sk || PyObject_SetAttr(st, s_skipped, sk);
+        Py_XDECREF(sk);
+        Py_XDECREF(st);
+        if (!bad && refetch[j]) bad = PySet_Add(ref, tid);
+        Py_DECREF(tid);
+        if (bad) goto done;
+        if (p < k) {
+            Py_INCREF(req);
+            PyTuple_SET_ITEM(edge, p, req);
+        } else if (!(cloud && cloud[j])) {
+            PyObject* b = bumped(req, skipped[j], bump);
+            if (!b) goto done;
+            PyTuple_SET_ITEM(deferred, q++, b);
+        }
+    }
+    {
+        PyObject* fz = PyFrozenSet_New(ref);
+        if (fz) result = Py_BuildValue("(NNN)", edge, deferred, fz);
+        if (result) edge = deferred = NULL;  /* stolen by the tuple */
+    }
+done:
+    Py_XDECREF(edge);
+    Py_XDECREF(deferred);
+    Py_XDECREF(ref);
+    Py_DECREF(reqs);
+    return result;
+}
+
 static PyMethodDef methods[] = {
     {"pack", pack, METH_VARARGS,
      "pack(reqs, states, rank_of, host_addr, capacity, out_bytes) -> (osl, o32, oout, nsl) | None"},
+    {"finish", finish, METH_VARARGS,
+     "finish(reqs, states, order_addr, refetch_addr, skipped_addr, n, k, cloud_addr, bump)"
+     " -> (edge, deferred, refetch_task_ids)"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_kr_pack",
@@ -222,6 +325,8 @@ PyMODINIT_FUNC PyInit__kr_pack(void) {
     INTERN(s_skipped, "skipped");
     INTERN(s_start, "start");
     INTERN(s_end, "end");
+    INTERN(s_dict, "__dict__");
+    INTERN(s_dc_fields, "__dataclass_fields__");
 #undef INTERN
     return PyModule_Create(&module);
 }

@@ -118,11 +118,12 @@ def _issued_base(issued) -> int:
 
 
 def _ranks(ids: Sequence[str]) -> dict:
-    if len(set(ids)) != len(ids):
-        raise ValueError("pending set holds more than one request for a task")
     if len(ids) >= fl.RANK_SPAN:
         raise ValueError("more than 2^24 pending requests in one planning round")
-    return {t: i for i, t in enumerate(sorted(ids))}
+    rank = {t: i for i, t in enumerate(sorted(ids))}
+    if len(rank) != len(ids):  # a repeated id collapsed into one entry
+        raise ValueError("pending set holds more than one request for a task")
+    return rank
 
 
 def order_within_bucket(requests: Sequence[PendingRequest], exec_estimates: Mapping[str, Duration],
@@ -152,10 +153,15 @@ def order_within_bucket(requests: Sequence[PendingRequest], exec_estimates: Mapp
 
 def _checked_pending(pending: Iterable[PendingRequest],
                      states: Mapping[str, TaskState]) -> list[PendingRequest]:
-    reqs = sorted(pending, key=lambda r: (r.issued_at, r.task_id))
-    for req in reqs:
-        if req.task_id not in states:
-            raise ValueError(f"pending request references unknown task {req.task_id!r}")
+    """The pending requests, validated (scheduler.py:245-251).  The reference
+    sorts them by (issued_at, task_id) first; every result here is ordered by
+    the unique packed keys, so the sort only decides which unknown task the
+    error names -- it runs only when there is one."""
+    reqs = list(pending)
+    if not all(r.task_id in states for r in reqs):
+        for req in sorted(reqs, key=lambda r: (r.issued_at, r.task_id)):
+            if req.task_id not in states:
+                raise ValueError(f"pending request references unknown task {req.task_id!r}")
     return reqs
 
 
@@ -226,14 +232,10 @@ def _plan_small(reqs, states, rank_of, sched, k) -> DispatchPlan:
     if f & (_lib.FLAG_KEY_RANGE | _lib.FLAG_RATIO):
         raise ValueError("a pending request falls outside the packed sort-key range "
                          "(aged estimate >= 2^56 µs or lifetime >= 2^53 µs)")
-    order_h = out[:n].tolist()
-    skipped_h = out[2 * n:3 * n].tolist()
-    refetch_idx = np.flatnonzero(out[n:2 * n]).tolist()
-    for i in order_h:
-        states[reqs[i].task_id].skipped = skipped_h[i]
-    s_edge = tuple([reqs[i] for i in order_h[:k]])
-    deferred = tuple([_bumped(reqs[i], skipped_h[i]) for i in order_h[k:]])
-    refetch_ids = frozenset([reqs[i].task_id for i in refetch_idx])
+    from . import _kr_pack
+    a = out.ctypes.data  # order [n], refetch [n], skipped [n] (int32, mapped host memory)
+    s_edge, deferred, refetch_ids = _kr_pack.finish(reqs, states, a, a + 4 * n, a + 8 * n, n, k,
+                                                    0, _bumped)
     return DispatchPlan(edge=s_edge, cloud=(), deferred=deferred, refetch_task_ids=refetch_ids)
 
 
@@ -277,22 +279,17 @@ def _place(reqs, states, keys, fleet, sched, flags, edge, cloud, net, edge_avail
     if f & (_lib.FLAG_KEY_RANGE | _lib.FLAG_RATIO):
         raise ValueError("a pending request falls outside the packed sort-key range "
                          "(aged estimate >= 2^56 µs or lifetime >= 2^53 µs)")
-    order_h = host[:n]
-    refetch_h = host[n:2 * n]
-    skipped_h = host[2 * n:3 * n]
     cloud_h = cloud_idx[:n_cloud].cpu().numpy() if n_cloud else np.zeros(0, np.int32)
-    in_cloud = set(int(i) for i in cloud_h)
-    s_edge = [reqs[i] for i in order_h[:k]]
-    s_cloud = [reqs[i] for i in cloud_h]
-    deferred = []
-    for i in order_h:
-        states[reqs[i].task_id].skipped = int(skipped_h[i])
-    for i in order_h[k:]:
-        if int(i) in in_cloud:
-            continue
-        deferred.append(_bumped(reqs[i], int(skipped_h[i])))
-    refetch_ids = frozenset(reqs[i].task_id for i in np.nonzero(refetch_h)[0])
-    return DispatchPlan(edge=tuple(s_edge), cloud=tuple(s_cloud), deferred=tuple(deferred),
+    in_cloud = np.zeros(n, np.int32)
+    in_cloud[cloud_h] = 1
+    from . import _kr_pack
+    host = np.ascontiguousarray(host)
+    a = host.ctypes.data
+    s_edge, deferred, refetch_ids = _kr_pack.finish(reqs, states, a, a + 4 * n, a + 8 * n, n, k,
+                                                    in_cloud.ctypes.data if n_cloud else 0,
+                                                    _bumped)
+    s_cloud = tuple(reqs[i] for i in cloud_h)
+    return DispatchPlan(edge=s_edge, cloud=s_cloud, deferred=deferred,
                         refetch_task_ids=refetch_ids)
 
 

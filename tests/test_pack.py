@@ -95,3 +95,54 @@ def test_native_pack_numpy_ints_and_errors():
     big = {t: 1 << 40 for t in rank}
     with pytest.raises(OverflowError):
         fl.host_soa(pending, states, big)
+
+
+@pytest.mark.parametrize("n,k,with_cloud", [(1, 1, False), (7, 3, False), (300, 0, False),
+                                            (300, 120, True), (2000, 2000, False)])
+def test_native_finish_matches_python(n, k, with_cloud):
+    """_kr_pack.finish (the plan's result objects from the device read-back)
+    equals the plain-Python construction of scheduler.py:223-241: edge prefix,
+    deferred bumped copies (offloaded requests excluded), refetch ids, and every
+    TaskState.skipped updated."""
+    import copy
+    from paper_2605_11381_b200 import _kr_pack, scheduler as sch
+    states, pending = fleet_objects(n, seed=n + k)
+    rng = np.random.default_rng(n)
+    order = rng.permutation(n).astype(np.int32)
+    refetch = (rng.random(n) < 0.3).astype(np.int32)
+    skipped = rng.integers(0, 20, n).astype(np.int32)
+    cloud = np.zeros(n, np.int32)
+    if with_cloud:
+        cloud[order[k:][rng.random(n - k) < 0.2]] = 1
+    buf = np.concatenate([order, refetch, skipped])
+    a = buf.ctypes.data
+    states_py = copy.deepcopy(states)
+    before = [r.skipped for r in pending]
+    edge, deferred, ref = _kr_pack.finish(pending, states, a, a + 4 * n, a + 8 * n, n, k,
+                                          cloud.ctypes.data if with_cloud else 0, sch._bumped)
+    exp_edge = tuple(pending[i] for i in order[:k])
+    exp_def = tuple(sch._bumped(pending[i], int(skipped[i])) for i in order[k:] if not cloud[i])
+    exp_ref = frozenset(pending[i].task_id for i in np.nonzero(refetch)[0])
+    for i in order:
+        states_py[pending[i].task_id].skipped = int(skipped[i])
+    assert edge == exp_edge and all(a_ is b_ for a_, b_ in zip(edge, exp_edge))
+    assert deferred == exp_def
+    assert all(type(d) is type(e) for d, e in zip(deferred, exp_def))
+    assert ref == exp_ref and isinstance(ref, frozenset)
+    assert {t: s.skipped for t, s in states.items()} == {t: s.skipped for t, s in states_py.items()}
+    # the originals are untouched (bumped copies, not mutation)
+    assert [r.skipped for r in pending] == before
+
+
+def test_native_finish_errors():
+    from paper_2605_11381_b200 import _kr_pack, scheduler as sch
+    states, pending = fleet_objects(3, seed=1)
+    buf = np.array([0, 1, 5, 0, 0, 0, 1, 1, 1], np.int32)  # index 5 out of range
+    a = buf.ctypes.data
+    with pytest.raises(ValueError):
+        _kr_pack.finish(pending, states, a, a + 12, a + 24, 3, 1, 0, sch._bumped)
+    del states[pending[0].task_id]
+    buf = np.array([0, 1, 2, 0, 0, 0, 1, 1, 1], np.int32)
+    a = buf.ctypes.data
+    with pytest.raises(KeyError):
+        _kr_pack.finish(pending, states, a, a + 12, a + 24, 3, 1, 0, sch._bumped)

@@ -599,10 +599,10 @@ def other_configs(reps: int = 200):
     U = synthetic.magnitudes(R, seed=25, dtype=torch.float64)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     t = timed_captured(rnd, fleet, rounds.ConfidenceInputs(
-        U, HorizonPolicyConfig.confidence(0.4, 5)), 24)
+        U, HorizonPolicyConfig.confidence(0.4, 5)), 8)
     out["configs[4] per-GPU share, confidence policy fp64 (U 2^20 x 6 x 50 fp64), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
-        "l2": "streams from HBM (2.5 GB of magnitudes)", "layout": "split, 24 reserved SMs"}
+        "l2": "streams from HBM (2.5 GB of magnitudes)", "layout": "split, 8 reserved SMs"}
     del U
     # the headline fleet with a cloud tier (phase 3 at fleet scale, §8(f)1):
     # full key order + edge admission + the ordered offload scan

@@ -33,7 +33,8 @@ def main():
     R = 1 << 20
     soa = synthetic.fleet_soa(R, seed=18)
     fleet = fl.DeviceFleet.from_host(soa)
-    U = synthetic.magnitudes(R, seed=19)
+    import os
+    U = synthetic.magnitudes(R, seed=19, dtype=torch.float64 if os.environ.get("CONF_FP64") else torch.float32)
     sched = fl.sched_struct("kairos", 10, 5, 150_000, 166_667, synthetic.NOW, 30,
                             int(soa["issued_at"].min()))
     inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))

@@ -531,12 +531,13 @@ __device__ __noinline__ int sweep_fix(const T* col, int K, int N, int jf, bool c
     return static_cast<int>(fl << 16) | j;
 }
 
-template <typename T, int KC, int VW, int CPL>
+template <typename T, int KC, int VW, int CPL, bool ROT = false>
 struct SweepSeg {
     using CW = ConfWork<T, KC, 1>;
     using B = typename std::conditional<sizeof(T) == 4, uint32_t, uint64_t>::type;
     using Elem = T;
     static constexpr int kVC = VW;
+    static constexpr bool kRot = ROT;
     int K, N, C, Cc, maxcap, half;
     int G, RW, lgRW;             // lanes per robot, robots per warp (32 / G), log2(RW)
     int cw;                      // consumer warps
@@ -617,6 +618,14 @@ struct SweepSeg {
         // end at N (their leading columns repeat the previous lane's: those are
         // below the scan's carry, so they never step twice)
         const int c0 = min(sg * CPL, N - CPL);
+        // ROT (robot strides that are multiples of 32 banks, e.g. N = 64 / 128
+        // fp32): lane (q, s) walks its window's column groups rotated by
+        // q + RW (s / 2), so the lanes of a phase read distinct banks; j[i]
+        // then holds column colof(i), and pass 2 restores column order
+        constexpr int kP = CPL / VW;
+        static_assert(!ROT || (kP & (kP - 1)) == 0, "rotation needs a power-of-two group count");
+        const int rot = ROT ? ((q + RW * (sg >> 1)) & (kP - 1)) : 0;
+        auto colof = [&](int i) { return ROT ? VW * (((i / VW) + rot) & (kP - 1)) + i % VW : i; };
         uint32_t fl = 0;
         for (int rb = warp * RW; rb < nr; rb += cw * RW) {
             const int rr = rb + q;
@@ -639,7 +648,7 @@ struct SweepSeg {
                     float2 x, sf;
                     auto ld = [&](int k) {
                         const T* rp = KC > 0 ? rowp[KC > 0 ? k : 0] : base + k * N;
-                        x = *reinterpret_cast<const float2*>(rp + i);
+                        x = *reinterpret_cast<const float2*>(rp + colof(i));
                         mx = max(mx, max(__float_as_uint(x.x), __float_as_uint(x.y)));
                     };
                     auto add2 = [&]() {
@@ -673,7 +682,7 @@ struct SweepSeg {
                 for (int i = 0; i < CPL; i += VW) {
                     T sf[VW], x[VW];
                     auto ldv = [&](int k) {  // VW adjacent columns of row k
-                        const T* rp = (KC > 0 ? rowp[KC > 0 ? k : 0] : base + k * N) + i;
+                        const T* rp = (KC > 0 ? rowp[KC > 0 ? k : 0] : base + k * N) + colof(i);
                         if constexpr (VW == 2 && sizeof(T) == 8) {
                             const double2 d = *reinterpret_cast<const double2*>(rp);
                             x[0] = d.x;
@@ -750,7 +759,12 @@ struct SweepSeg {
                 for (int t = lane; t < total; t += 32) {
                     const uint32_t e = task[t];
                     const int L = (e >> 4) & 31;
-                    const int cL = min((L >> lgRW) * CPL, N - CPL) + static_cast<int>(e & 15);
+                    int ci = static_cast<int>(e & 15);
+                    if constexpr (ROT) {  // the owner's rotation
+                        const int rL = ((L & (RW - 1)) + RW * ((L >> lgRW) >> 1)) & (kP - 1);
+                        ci = VW * (((ci / VW) + rL) & (kP - 1)) + ci % VW;
+                    }
+                    const int cL = min((L >> lgRW) * CPL, N - CPL) + ci;
                     const T* col = u + (rb + (L & (RW - 1))) * KN + cL;
                     const int pk = sweep_fix<T, KC>(col, K, N, 0xFFFF, (e >> 9) & 1, sfmin, sfmax,
                                                     half, Cc, tables()->p, rh, rl);
@@ -782,6 +796,13 @@ struct SweepSeg {
             if (sg == 0) cur = 0;
             const int64_t r = r0 + rr;
             if (ok && m > cur) {  // this segment raises the running maximum
+                if constexpr (ROT) {  // column order through this lane's task-list row
+                    uint16_t* sc = fix_tasks(warp) + lane * kSegCols;
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) sc[colof(i)] = static_cast<uint16_t>(j[i]);
+#pragma unroll
+                    for (int i = 0; i < CPL; i++) j[i] = sc[i];
+                }
                 // branch-free: the columns where it rises, and the running maxima
                 uint32_t mask = 0;
                 uint32_t pk[(CPL + 3) / 4];
@@ -896,6 +917,16 @@ struct SegBounds {
 };
 constexpr int kSegThreads = 384;  // largest CTA the launcher plans (<= both bounds)
 
+template <typename T, int KC, int VW, bool kStaged>
+__global__ void __launch_bounds__(512, 1)
+k_horizon_sweep_seg_rot(StreamPlan p, SweepSeg<T, KC, VW, 16, true> w, const __grid_constant__ SweepCfg cfg) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    SweepTables* const tab = w.tables();
+    sweep_prologue(tab, cfg);
+    stream_run<kStaged>(p, smem, w);
+    sweep_epilogue(tab, w.Cc, w.C, w.R, w.sums);
+}
+
 template <typename T, int KC, int VW, int CPL, bool kStaged, bool LEAN = false>
 __global__ void __launch_bounds__(SegBounds<LEAN>::kThreads, SegBounds<LEAN>::kMinBlocks)
 k_horizon_sweep_seg(StreamPlan p, SweepSeg<T, KC, VW, CPL> w,
@@ -913,10 +944,11 @@ k_horizon_sweep_seg(StreamPlan p, SweepSeg<T, KC, VW, CPL> w,
 // whether the windows of a phase collide (N = 50 fp32: 1, conflict-free;
 // N = 64 / 128 fp32: every robot on the same banks).  Above 2 the launcher
 // keeps the warp-per-robot kernels.
-inline int sweep_seg_conflicts(int K, int N, size_t es, bool pair) {
+inline int sweep_seg_conflicts(int K, int N, size_t es, bool pair, bool rot = false) {
     int G = 1;
     while (G * kSegCols < N) G <<= 1;
-    const int CPL = pair && G * 14 >= N ? 14 : kSegCols;
+    const int CPL = rot ? kSegCols : (pair && G * 14 >= N ? 14 : kSegCols);
+    const int VWc = pair ? 2 : 1, P = CPL / VWc;
     const int RW = 32 / G;
     const int w = static_cast<int>(es / 4);         // words per element
     const int width = (pair ? 2 : 1) * w;           // words per lane access
@@ -927,7 +959,7 @@ inline int sweep_seg_conflicts(int K, int N, size_t es, bool pair) {
         int cnt[32] = {};
         for (int l = ph; l < ph + lanes; l++) {
             const int q = l % RW, sg = l / RW;
-            const int c0 = std::min(sg * CPL, N - CPL);
+            const int c0 = std::min(sg * CPL, N - CPL) + (rot ? VWc * ((q + RW * (sg >> 1)) % P) : 0);
             const long a0 = (static_cast<long>(q) * K * N + c0) * w;
             for (int t = 0; t < width; t++) {
                 const long wd = a0 + t;
@@ -950,6 +982,13 @@ inline bool sweep_seg_ok(int K, int N, size_t es, bool aligned16) {
     static const bool seg_off = std::getenv("KR_SWEEP_NO_SEG") != nullptr;  // A/B knob
     return !seg_off && N <= 32 * kSegCols && N >= kSegCols &&
            sweep_seg_conflicts(K, N, es, aligned16 && N % 2 == 0) <= 2;
+}
+// The rotated-window form takes the shapes whose plain windows collide.
+inline bool sweep_seg_rot_ok(int K, int N, size_t es, bool aligned16) {
+    static const bool rot_off = std::getenv("KR_SWEEP_NO_ROT") != nullptr;  // A/B knob
+    return !rot_off && !sweep_seg_ok(K, N, es, aligned16) && N <= 32 * kSegCols && N >= kSegCols &&
+           !std::getenv("KR_SWEEP_NO_SEG") &&
+           sweep_seg_conflicts(K, N, es, aligned16 && N % 2 == 0, true) <= 2;
 }
 
 template <typename T>
@@ -1002,7 +1041,8 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
 #define KR_SWEEP(KK, VV) \
     return go(SweepWork<T, KK, VV>{}, k_horizon_sweep<T, KK, VV, true>, k_horizon_sweep<T, KK, VV, false>)
     // segmented sweep: G lanes per robot, <= kSegCols columns per lane
-    if (sweep_seg_ok(K, N, sizeof(T), al)) {
+    const bool rot = sweep_seg_rot_ok(K, N, sizeof(T), al);
+    if (rot || sweep_seg_ok(K, N, sizeof(T), al)) {
         int G = 1;
         while (G * kSegCols < N) G <<= 1;
         const bool pair = al && N % 2 == 0;
@@ -1017,7 +1057,14 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
             // (4 and 5 equal on the common shape, 5 better for fp64 / odd N / ties,
             // 6 leaves one CTA per SM); decide-only launches 4, best beside the
             // round's side stream (profiles/r2_confidence_layouts.jsonl)
-            const int tr = tr_env > 0 ? tr_env : (cw_env > 0 ? cw_env : (sums ? 5 : 4)) * RW;
+            int tr = tr_env > 0 ? tr_env : (cw_env > 0 ? cw_env : (sums ? 5 : 4)) * RW;
+            // rotated windows (large robots: N = 64 / 128 / ... fp32): ~36 KB
+            // stages -- N = 64: 24 robots, N = 128: 12 (71 -> 91% and 70 -> 90%
+            // of the measured peak against 5 warps' worth of robots)
+            if (W::kRot && tr_env <= 0 && cw_env <= 0) {
+                const int fit = static_cast<int>(36864 / rb) / RW * RW;
+                tr = fit > RW ? fit : RW;
+            }
             const uint32_t task_bytes = static_cast<uint32_t>((tr * G + 31) / 32) * 32 * kSegCols * 2;
             static const int st_env = std::getenv("KR_SWEEP_STAGES") ? std::atoi(std::getenv("KR_SWEEP_STAGES")) : 0;
             static const int psm_env = std::getenv("KR_SWEEP_PERSM") ? std::atoi(std::getenv("KR_SWEEP_PERSM")) : 0;
@@ -1069,6 +1116,17 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
 #define KR_SEG_LEAN(KK)                                                                         \
     return go_seg(SweepSeg<T, KK, 2, 14>{}, k_horizon_sweep_seg<T, KK, 2, 14, true, true>,   \
                   k_horizon_sweep_seg<T, KK, 2, 14, false, true>)
+#define KR_SEG_ROT(KK, VV)                                                                     \
+    return go_seg(SweepSeg<T, KK, VV, 16, true>{}, k_horizon_sweep_seg_rot<T, KK, VV, true>,   \
+                  k_horizon_sweep_seg_rot<T, KK, VV, false>)
+        if (rot) {
+            if (pair) {
+                if (K == 6) KR_SEG_ROT(6, 2);
+                KR_SEG_ROT(0, 2);
+            }
+            if (K == 6) KR_SEG_ROT(6, 1);
+            KR_SEG_ROT(0, 1);
+        }
         if (pair) {
             if (c14) {
                 if constexpr (sizeof(T) == 4) {
@@ -1087,6 +1145,7 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
         KR_SEG(0, 1, 16);
 #undef KR_SEG
 #undef KR_SEG_LEAN
+#undef KR_SEG_ROT
     }
     // two robots per warp: N <= 64 (pair loads when N is even and the base 16-byte aligned)
     static const bool half_off = std::getenv("KR_SWEEP_NO_HALF") != nullptr;  // A/B knob

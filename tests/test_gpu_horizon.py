@@ -231,7 +231,9 @@ def test_sweep_golden(kb):
 
 @pytest.mark.parametrize("R,K,N", [(1, 2, 1), (999, 6, 50), (4099, 6, 64), (513, 3, 1),
                                    (300, 10, 7), (257, 4, 300), (700, 10, 64), (333, 3, 2),
-                                   (65, 7, 66), (500, 6, 49), (90, 5, 63), (41, 6, 33)])
+                                   (65, 7, 66), (500, 6, 49), (90, 5, 63), (41, 6, 33),
+                                   (301, 6, 128), (203, 6, 256), (150, 6, 96), (100, 6, 16),
+                                   (120, 6, 32), (77, 6, 512)])
 @pytest.mark.parametrize("storage", [np.float32, np.float64])
 def test_sweep_vs_oracle_every_decision(kb, R, K, N, storage):
     rng = np.random.default_rng(R + K + N)

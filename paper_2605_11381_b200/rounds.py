@@ -34,6 +34,7 @@ from . import device as dev
 from . import fleet as fl
 
 ALL_ONES = -1  # int64 view of 0xFFFF...FFFF
+SMALL_ADMIT_MAX = 16384  # kr_select.cu kSmallAdmit: admission sorts every key up to here
 
 
 @dataclass
@@ -112,6 +113,12 @@ class DecisionRound:
         self.flags = dev.flags()
         self.lib = _lib.load()
         self.max_sms = 0  # divergence grid SM cap (0: all); see capture(concurrent=...)
+        # the keys' OR / AND statistics feed only the radix select; rounds whose
+        # admission sorts everything (R <= 16,384: kr_select.cu kSmallAdmit) or
+        # selects nothing skip them (one launch less per round; a select that
+        # gets no statistics computes its own, so a wrong guess costs only time)
+        self.stats_needed = not (type(self) is DecisionRound and
+                                 (R <= SMALL_ADMIT_MAX or self.k == 0 or self.k >= R))
 
     def horizons(self, h) -> None:
         if isinstance(h, MixedInputs):
@@ -157,12 +164,15 @@ class DecisionRound:
 
     def urgency(self, fleet: fl.DeviceFleet) -> None:
         st = dev.stream()
-        _lib.check(self.lib.kr_key_stats_init(self.key_stats.data_ptr(), st), "kr_key_stats_init")
+        if self.stats_needed:
+            _lib.check(self.lib.kr_key_stats_init(self.key_stats.data_ptr(), st),
+                       "kr_key_stats_init")
         fs = fleet.c_struct()
         _lib.check(self.lib.kr_urgency(
             ctypes.byref(fs), ctypes.byref(self.sched), self.keys.data_ptr(),
             self.need_time.data_ptr(), None, None, None, None, None,
-            self.key_stats.data_ptr(), self.flags.data_ptr(), st), "kr_urgency")
+            self.key_stats.data_ptr() if self.stats_needed else None, self.flags.data_ptr(), st),
+            "kr_urgency")
 
     def check(self, reset: bool = True) -> None:
         """Raise the reference's ValueError if any round since the last check
@@ -175,7 +185,8 @@ class DecisionRound:
         raise_round_flags(f)
 
     def admit(self, fleet: fl.DeviceFleet) -> None:
-        fl.select_admit(self.keys, self.k, self.ws, key_stats=self.key_stats, fleet=fleet,
+        fl.select_admit(self.keys, self.k, self.ws,
+                        key_stats=self.key_stats if self.stats_needed else None, fleet=fleet,
                         sched=self.sched, admitted=self.admitted, refetch=self.refetch,
                         edge_idx=self.edge_idx, edge_keys=self.edge_keys, kth=self.kth)
 

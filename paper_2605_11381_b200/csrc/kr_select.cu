@@ -740,13 +740,44 @@ __device__ __forceinline__ Pair keep(const Pair& mine, const Pair& other, bool k
     return (gt == keep_min) ? other : mine;
 }
 
+struct SmallAdmitArgs {
+    const kr_key* sorted_keys;
+    const int32_t* sorted_idx;
+    int n, k;
+    const int64_t* obs;  // nullable
+    int32_t* skipped;    // nullable
+    uint8_t* admitted;   // nullable
+    uint8_t* refetch;    // nullable
+    int64_t now, stale;
+    int32_t* edge_idx;   // nullable
+    kr_key* edge_keys;   // nullable
+    kr_key* kth_out;     // nullable
+};
+
+// The admission writes of the small-fleet path for the pair at plan position
+// p (request j, key x): rank < k is admission (keys are unique), refetch of a
+// stale observation, skip counter, ordered S_e and the k-th key.
+__device__ __forceinline__ void apply_one(const SmallAdmitArgs& a, int p, int32_t j, const kr_key& x) {
+    const bool in = p < a.k;
+    if (a.admitted) a.admitted[j] = in;
+    if (a.refetch) a.refetch[j] = in && (a.now - __ldg(a.obs + j) > a.stale);
+    if (a.skipped) a.skipped[j] = in ? 0 : a.skipped[j] + 1;
+    if (in) {
+        if (a.edge_idx) a.edge_idx[p] = j;
+        if (a.edge_keys) a.edge_keys[p] = x;
+    }
+    if (a.kth_out && p == a.k - 1) *a.kth_out = x;
+}
+
 // One run of kRun = 256 pairs per CTA, a bitonic network held in registers:
 // thread t owns elements 2t and 2t + 1; partners at distance j = 1 are in the
 // same thread, j = 2..32 in the same warp (shuffles), j = 64, 128 in another
 // warp (one shared-memory exchange each).  Padding is +inf (all-ones, INT_MAX).
 __global__ void __launch_bounds__(kRunThreads) k_run_sort(const kr_key* keys, const int32_t* idx,
                                                           const unsigned int* count_dev, int m_host,
-                                                          kr_key* rk, int32_t* ri) {
+                                                          kr_key* rk, int32_t* ri,
+                                                          SmallAdmitArgs a = SmallAdmitArgs{},
+                                                          int apply = 0) {
     static_assert(kRun == 2 * kRunThreads, "two elements per thread");
     __shared__ Pair sp[kRun];
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
@@ -801,8 +832,12 @@ __global__ void __launch_bounds__(kRunThreads) k_run_sort(const kr_key* keys, co
     for (int q = 0; q < 2; q++) {
         const int x = 2 * t + q;
         if (x < n) {
-            rk[base + x] = e[q].k;
-            ri[base + x] = e[q].i;
+            if (apply) {  // a single run is the whole order: admission from the registers
+                apply_one(a, base + x, e[q].i, e[q].k);
+            } else {
+                rk[base + x] = e[q].k;
+                ri[base + x] = e[q].i;
+            }
         }
     }
 }
@@ -824,7 +859,8 @@ __device__ __forceinline__ int count_less(const kr_key* rk, const int32_t* ri, i
 // of 256, spread over m warps, keep the whole GPU busy even for small m.
 __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32_t* ri,
                                                    const unsigned int* count_dev, int m_host,
-                                                   int32_t* out_idx, kr_key* out_keys) {
+                                                   int32_t* out_idx, kr_key* out_keys,
+                                                   SmallAdmitArgs a = SmallAdmitArgs{}, int apply = 0) {
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
     const int nruns = (m + kRun - 1) / kRun;
     const int lane = threadIdx.x & 31;
@@ -840,8 +876,12 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
         for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (lane == 0) {
             const int rank = c + (e - own * kRun);
-            if (out_idx) out_idx[rank] = xi;
-            if (out_keys) out_keys[rank] = x;
+            if (apply) {
+                apply_one(a, rank, xi, x);
+            } else {
+                if (out_idx) out_idx[rank] = xi;
+                if (out_keys) out_keys[rank] = x;
+            }
         }
     }
 }
@@ -856,7 +896,9 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
 __global__ void __launch_bounds__(256) k_run_merge_group(const kr_key* rk, const int32_t* ri,
                                                          const unsigned int* count_dev, int m_host,
                                                          int L, int lgG, int32_t* out_idx,
-                                                         kr_key* out_keys) {
+                                                         kr_key* out_keys,
+                                                         SmallAdmitArgs a = SmallAdmitArgs{},
+                                                         int apply = 0) {
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
     const int G = 1 << lgG;
     const int nruns = (m + L - 1) / L;
@@ -881,8 +923,12 @@ __global__ void __launch_bounds__(256) k_run_merge_group(const kr_key* rk, const
         for (int o = G >> 1; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (ok && gl == 0) {
             const int pos = (run & ~(G - 1)) * L + c + (e - run * L);
-            if (out_idx) out_idx[pos] = xi;
-            if (out_keys) out_keys[pos] = x;
+            if (apply) {
+                apply_one(a, pos, xi, x);
+            } else {
+                if (out_idx) out_idx[pos] = xi;
+                if (out_keys) out_keys[pos] = x;
+            }
         }
     }
 }
@@ -957,34 +1003,7 @@ __global__ void __launch_bounds__(256) k_run_merge_sampled(const kr_key* rk, con
 constexpr int kSmallAdmit = KR_SMALL_ADMIT;  // 16k: with the register run sort the
                                              // small path beats the select (configs[2] 91 -> 86 us)
 
-struct SmallAdmitArgs {
-    const kr_key* sorted_keys;
-    const int32_t* sorted_idx;
-    int n, k;
-    const int64_t* obs;  // nullable
-    int32_t* skipped;    // nullable
-    uint8_t* admitted;   // nullable
-    uint8_t* refetch;    // nullable
-    int64_t now, stale;
-    int32_t* edge_idx;   // nullable
-    kr_key* edge_keys;   // nullable
-    kr_key* kth_out;     // nullable
-};
 
-__global__ void __launch_bounds__(256) k_small_apply(SmallAdmitArgs a) {
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < a.n; p += gridDim.x * blockDim.x) {
-        const int32_t j = a.sorted_idx[p];
-        const bool in = p < a.k;
-        if (a.admitted) a.admitted[j] = in;
-        if (a.refetch) a.refetch[j] = in && (a.now - __ldg(a.obs + j) > a.stale);
-        if (a.skipped) a.skipped[j] = in ? 0 : a.skipped[j] + 1;
-        if (in) {
-            if (a.edge_idx) a.edge_idx[p] = j;
-            if (a.edge_keys) a.edge_keys[p] = a.sorted_keys[p];
-        }
-        if (a.kth_out && p == a.k - 1) *a.kth_out = a.sorted_keys[p];
-    }
-}
 
 // Merge of W sorted candidate runs (the sharded round's all-gathered local
 // top-k' lists, sentinel-padded to equal length): every element's global rank
@@ -1193,7 +1212,12 @@ static bool merge_unsampled() {
 // Sorts (keys, idx) with n elements (keys/idx may alias workspace buffer 0).
 static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx,
                       const unsigned int* count_dev, int64_t n, int32_t* out_idx, kr_key* out_keys,
-                      const unsigned long long* stats_dev, cudaStream_t st) {
+                      const unsigned long long* stats_dev, cudaStream_t st,
+                      const SmallAdmitArgs* ap = nullptr) {
+    // ap: the small-fleet admission applied by the final sort stage from the
+    // ranks it computes (no separate apply pass); n <= kRunSortMax only
+    const SmallAdmitArgs av = ap ? *ap : SmallAdmitArgs{};
+    const int apply = ap ? 1 : 0;
     if (n <= kRunSortMax) {
         const int m = static_cast<int>(n);
         const kr_key* sk = keys;
@@ -1208,6 +1232,10 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
         // merge's one search per lane is faster (4k pairs: 22 vs 27 us).
         static const bool grouped_off = std::getenv("KR_MERGE_FLAT") != nullptr;  // A/B knob
         const int runs0 = (m + kRun - 1) / kRun;
+        if (apply && runs0 == 1) {  // one run is the whole order
+            k_run_sort<<<1, kRunThreads, 0, st>>>(sk, si, count_dev, m, rk, ri, av, 1);
+            return check_launch("run sort (apply)");
+        }
         if (!grouped_off && out_idx && out_keys && runs0 > 32) {
             int lg[8], P = 0;
             for (int r = runs0; r > 1 && P < 8; P++) {
@@ -1229,8 +1257,8 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
                 const int64_t warps = (static_cast<int64_t>(m) + (32 >> lg[q]) - 1) / (32 >> lg[q]);
                 int64_t blocks = (warps + 7) / 8;
                 if (blocks > 148 * 64) blocks = 148 * 64;
-                k_run_merge_group<<<static_cast<unsigned>(blocks), 256, 0, st>>>(ck, ci, count_dev, m, L,
-                                                                                lg[q], di, dk);
+                k_run_merge_group<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+                    ck, ci, count_dev, m, L, lg[q], di, dk, av, apply && q == P - 1);
                 ck = dk;
                 ci = di;
                 L <<= lg[q];
@@ -1241,7 +1269,7 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
         const int64_t warps = m;
         int64_t blocks = (warps + 7) / 8;
         if (blocks > 148 * 64) blocks = 148 * 64;
-        if (KR_MERGE_SAMPLED && m <= kMergeSampled && !merge_unsampled()) {
+        if (KR_MERGE_SAMPLED && !apply && m <= kMergeSampled && !merge_unsampled()) {
             // every CTA stages the samples: a few CTAs per SM, several pairs per warp
             const int64_t cap = static_cast<int64_t>(device_info().sm_count) * 2;
             k_run_merge_sampled<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, 0, st>>>(
@@ -1249,7 +1277,7 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
         }
         else
             k_run_merge<<<static_cast<unsigned>(blocks), 256, 0, st>>>(rk, ri, count_dev, m,
-                                                                       out_idx, out_keys);
+                                                                       out_idx, out_keys, av, apply);
         return check_launch("run sort", 2);
     }
     // window plan from OR ^ AND of the set (read back: one stream sync)
@@ -1526,8 +1554,6 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
     }
     if (n <= kSmallAdmit) {  // sort everything (run sort), rank < k is admission
         Workspace w = carve(ws, n);
-        int e = sort_pairs(w, keys, nullptr, nullptr, n, w.sidx[0], w.skeys[0], nullptr, st);
-        if (e) return e;
         SmallAdmitArgs a{};
         a.sorted_keys = w.skeys[0];
         a.sorted_idx = w.sidx[0];
@@ -1542,8 +1568,8 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
         a.edge_idx = edge_idx;
         a.edge_keys = edge_keys;
         a.kth_out = kth_out;
-        k_small_apply<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(a);
-        return check_launch("kr_select_admit(small)");
+        // the sort's last stage applies the admission (rank < k) itself
+        return sort_pairs(w, keys, nullptr, nullptr, n, w.sidx[0], w.skeys[0], nullptr, st, &a);
     }
     Workspace w = carve(ws, n);
     int e = select_pipeline(keys, n, k, key_stats, w, kth_out, st);

@@ -340,3 +340,32 @@ def test_zero_mean_columns_huge_thresholds(kb, storage):
     sums = kb.sweep_horizon_sums(cells, Ut).cpu().numpy()
     exp = orc.sweep_sums(U.astype(np.float64), [(1, 0, c.threshold, c.min_horizon) for c in cells])
     assert np.array_equal(sums, exp)
+
+
+@pytest.mark.parametrize("storage", [torch.float32, torch.float64])
+def test_segmented_validation_and_negative_zero(kb, storage):
+    """The segmented sweep / decide kernels' validation: NaN, +inf and negative
+    magnitudes in any lane's window raise the reference's ValueError; -0.0 is a
+    valid magnitude (horizon.py:47-50: isfinite and not < 0) and decides like
+    +0.0 through the exact path."""
+    rng = np.random.default_rng(23)
+    base = rng.uniform(0.2, 1.5, (257, 6, 50))
+    base[:, -1, 35:] *= 2.5
+    for bad, msg in ((float("nan"), "finite"), (float("inf"), "finite"), (-1e-3, ">= 0")):
+        for col in (0, 13, 29, 49):  # the windows of different lanes
+            U = torch.from_numpy(base.copy()).to(storage).cuda()
+            U[101, 2, col] = bad
+            with pytest.raises(ValueError, match=msg):
+                kb.sweep_horizon_sums([kb.HorizonPolicyConfig.confidence(0.4, 5)], U)
+            with pytest.raises(ValueError, match=msg):
+                kb.decide_horizon_batch(kb.HorizonPolicyConfig.confidence(0.4, 5), U)
+    U = base.copy()
+    U[5, :, 7] = -0.0
+    U[9, 1, 20] = -0.0
+    Ut = torch.from_numpy(U).to(storage).cuda()
+    Un = Ut.cpu().numpy()
+    for t, h in ((0.4, 5), (0.0, 1), (1.3, 3)):
+        cfg = kb.HorizonPolicyConfig.confidence(t, h)
+        exp = orc.horizon_conf_batch(Un, t, h)
+        assert np.array_equal(kb.decide_horizon_batch(cfg, Ut).cpu().numpy(), exp)
+        assert int(kb.sweep_horizon_sums([cfg], Ut).cpu()[0]) == int(exp.sum())

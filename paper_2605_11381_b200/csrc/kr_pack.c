@@ -287,8 +287,16 @@ static PyObject* finish(PyObject* self, PyObject* args) {
     }
     {
         PyObject* fz = PyFrozenSet_New(ref);
-        if (fz) result = Py_BuildValue("(NNN)", edge, deferred, fz);
-        if (result) edge = deferred = NULL;  /* stolen by the tuple */
+        PyObject* tup = fz ? PyTuple_New(3) : NULL;
+        if (!tup) {
+            Py_XDECREF(fz);
+            goto done;
+        }
+        PyTuple_SET_ITEM(tup, 0, edge);  /* references moved into the tuple */
+        PyTuple_SET_ITEM(tup, 1, deferred);
+        PyTuple_SET_ITEM(tup, 2, fz);
+        edge = deferred = NULL;
+        result = tup;
     }
 done:
     Py_XDECREF(edge);

@@ -26,7 +26,7 @@ SOURCES = ["kr_capi.cu", "kr_horizon.cu", "kr_div_skx.cu", "kr_div_hsw.cu", "kr_
            "kr_sweep_f32.cu", "kr_sweep_f64.cu",
            "kr_urgency.cu", "kr_select.cu", "kr_synth.cu", "kr_ingest.cpp"]
 HEADERS = ["kr_common.cuh", "kr_host.cuh", "kr_stream.cuh", "kr_plan.cuh", "kr_conf.cuh",
-           "kr_sweep.cuh", "kr_div.cuh"]
+           "kr_sweep.cuh", "kr_div.cuh", "kr_select_state.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -24,10 +24,10 @@
 
 #include "kr_common.cuh"
 #include "kr_host.cuh"
+#include "kr_select_state.cuh"
 
 namespace kr {
 
-constexpr int kDigitBits = 11;
 #ifndef KR_SEL_U
 #define KR_SEL_U 4
 #endif
@@ -36,42 +36,10 @@ constexpr int kSelU = KR_SEL_U;  // keys in flight per thread in the level-0 his
 #define KR_SCAT_W 1
 #endif
 constexpr int kScatW = KR_SCAT_W;  // digits per thread per step in the level-0 scatter
-constexpr int kBins = 1 << kDigitBits;
 #ifndef KR_SORT_TILE
 #define KR_SORT_TILE 4096
 #endif
 constexpr int kSortTile = KR_SORT_TILE;  // LSD radix: elements per CTA tile (256 threads x 16)
-
-// Digit = the values of the candidate set's kDigitBits most significant
-// *differing* bit positions (a pext of OR ^ AND), MSB first.  All candidates
-// agree on every other bit, so digit order is key order; unlike a contiguous
-// bit window it never wastes digit bits on constant fields (e.g. the high
-// zero bits of the aged estimate between the bucket and its significant bits).
-struct Digit {
-    int W;                 // number of digit bits (0: all candidates identical)
-    int nrun;              // the digit bits grouped into runs of adjacent positions
-    int run_pos[kDigitBits];  // lowest bit position (0..127) of each run, MSB run first
-    int run_len[kDigitBits];
-    bool any;
-};
-struct SelState {
-    unsigned long long st[2][4];  // [parity] {or_hi, or_lo, and_hi, and_lo}
-    unsigned int cnt[2];          // [parity] candidate count
-    long long need;               // 1-based rank of the target within candidates
-    unsigned int dstar;
-    unsigned int dcount;          // population of the boundary bin
-    int done;
-    int pad_;
-    kr_key kth;
-    unsigned int sel_count;       // admission gather count
-    unsigned int pad2_[3];
-    unsigned long long sst[4];    // OR/AND of the gathered (admitted) keys
-    Digit d0;                     // level-0 digit (from the keys' OR / AND)
-    unsigned int dstar0;          // its boundary bin (dstar moves on in later levels)
-    unsigned int done_hist;       // last-CTA-done counters of the two grid passes
-    unsigned int done_scatter;
-    unsigned int hist[kBins];
-};
 
 struct Workspace {
     SelState* state;
@@ -163,48 +131,6 @@ __device__ __forceinline__ void stats_accumulate(unsigned long long* dst, unsign
     }
 }
 
-// Built with compile-time indices only (predicated updates) so that the run
-// table lives in registers for the per-key extraction loops.
-__device__ __forceinline__ Digit digit_of(const unsigned long long* s) {
-    unsigned long long xlo = s[1] ^ s[3], xhi = s[0] ^ s[2];
-    Digit d;
-    d.W = 0;
-    d.nrun = 0;
-#pragma unroll
-    for (int r = 0; r < kDigitBits; r++) {
-        d.run_pos[r] = 0;
-        d.run_len[r] = 0;
-    }
-    int last = -2;
-#pragma unroll
-    for (int w = 0; w < kDigitBits; w++) {
-        int pos = -1;
-        if (xhi) {
-            pos = 127 - __clzll(xhi);
-            xhi &= ~(1ull << (pos - 64));
-        } else if (xlo) {
-            pos = 63 - __clzll(xlo);
-            xlo &= ~(1ull << pos);
-        }
-        if (pos >= 0) {
-            // extend the current run downwards unless it would cross the word boundary
-            const bool extend = pos == last - 1 && (pos >> 6) == (last >> 6);
-            const int cur = extend ? d.nrun - 1 : d.nrun;
-#pragma unroll
-            for (int r = 0; r < kDigitBits; r++) {
-                if (r == cur) {
-                    d.run_pos[r] = pos;
-                    d.run_len[r] += 1;
-                }
-            }
-            d.nrun = cur + 1;
-            last = pos;
-            d.W = w + 1;
-        }
-    }
-    d.any = d.W > 0;
-    return d;
-}
 __device__ __forceinline__ unsigned digit_val(const kr_key& k, const Digit& d) {
     unsigned v = 0;
 #pragma unroll
@@ -228,26 +154,6 @@ __device__ __forceinline__ unsigned digit_val(const kr_key& k, const Digit& d) {
 // The admission pass then decides most keys from the digit array alone
 // (digit < d*: in, > d*: out).  "Last CTA" = the CTA whose increment of a
 // completion counter returns gridDim - 1, after a release fence by every CTA.
-__device__ __forceinline__ void sel_init(SelState* s, int64_t n, int64_t k) {
-    s->st[1][0] = 0; s->st[1][1] = 0; s->st[1][2] = ~0ull; s->st[1][3] = ~0ull;
-    s->sst[0] = 0; s->sst[1] = 0; s->sst[2] = ~0ull; s->sst[3] = ~0ull;
-    s->cnt[0] = static_cast<unsigned>(n);
-    s->cnt[1] = 0;
-    s->need = k;
-    s->done = 0;
-    s->sel_count = 0;
-    s->done_hist = 0;
-    s->done_scatter = 0;
-}
-// The level-0 digit of the full key set; a set of identical keys (n == 1,
-// keys being unique) is its own answer.
-__device__ __forceinline__ void sel_digit0(SelState* s, const kr_key* keys) {
-    s->d0 = digit_of(s->st[0]);
-    if (!s->d0.any) {
-        s->kth = keys[0];
-        s->done = 1;
-    }
-}
 
 __global__ void k_sel_reset(SelState* s, int64_t n, int64_t k, const unsigned long long* stats,
                             const kr_key* keys) {
@@ -1458,11 +1364,14 @@ static int sel_ctas_per_sm(int occ) { return KR_SEL_CPS > 0 && KR_SEL_CPS < occ 
 // when given), w.digits the level-0 digits and state->dstar their boundary bin.
 static int select_pipeline(const kr_key* keys, int64_t n, int64_t k,
                            const unsigned long long* key_stats, const Workspace& w,
-                           kr_key* kth_out, cudaStream_t st) {
+                           kr_key* kth_out, cudaStream_t st, bool prepared = false) {
     SelState* s = w.state;
-    k_sel_reset<<<1, 1024, 0, st>>>(s, n, k, key_stats, keys);
-    int launches = 3;
-    if (!key_stats) {
+    int launches = 2;
+    if (!prepared) {  // (prepared: the urgency pass's last CTA did this, kr_urgency_prep)
+        k_sel_reset<<<1, 1024, 0, st>>>(s, n, k, key_stats, keys);
+        launches++;
+    }
+    if (!key_stats && !prepared) {
         k_sel_stats<<<grid_stream(n), 256, 0, st>>>(keys, n, s);
         k_sel_digit<<<1, 1, 0, st>>>(s, keys);
         launches += 2;
@@ -1531,11 +1440,35 @@ extern "C" int kr_topk_select(const kr_key* keys, int64_t n, int64_t k, kr_key* 
     return select_pipeline(keys, n, k, key_stats, w, kth, st);
 }
 
+static int select_admit(const kr_key* keys, int64_t n, int64_t k,
+                        const unsigned long long* key_stats, const kr_fleet* fleet,
+                        const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
+                        int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* ws,
+                        size_t ws_bytes, void* stream, bool prepared);
+
 extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
                                const unsigned long long* key_stats, const kr_fleet* fleet,
                                const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
                                int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* ws,
                                size_t ws_bytes, void* stream) {
+    return select_admit(keys, n, k, key_stats, fleet, cfg, admitted, refetch, edge_idx, edge_keys,
+                        kth_out, ws, ws_bytes, stream, false);
+}
+
+extern "C" int kr_select_admit_prepared(const kr_key* keys, int64_t n, int64_t k,
+                                        const kr_fleet* fleet, const kr_sched* cfg,
+                                        uint8_t* admitted, uint8_t* refetch, int32_t* edge_idx,
+                                        kr_key* edge_keys, kr_key* kth_out, void* ws,
+                                        size_t ws_bytes, void* stream) {
+    return select_admit(keys, n, k, nullptr, fleet, cfg, admitted, refetch, edge_idx, edge_keys,
+                        kth_out, ws, ws_bytes, stream, true);
+}
+
+static int select_admit(const kr_key* keys, int64_t n, int64_t k,
+                        const unsigned long long* key_stats, const kr_fleet* fleet,
+                        const kr_sched* cfg, uint8_t* admitted, uint8_t* refetch,
+                        int32_t* edge_idx, kr_key* edge_keys, kr_key* kth_out, void* ws,
+                        size_t ws_bytes, void* stream, bool prepared) {
     if (n < 0 || k < 0) return KR_EINVAL;
     if (n == 0) return KR_OK;
     if (!keys) return KR_EINVAL;
@@ -1572,7 +1505,7 @@ extern "C" int kr_select_admit(const kr_key* keys, int64_t n, int64_t k,
         return sort_pairs(w, keys, nullptr, nullptr, n, w.sidx[0], w.skeys[0], nullptr, st, &a);
     }
     Workspace w = carve(ws, n);
-    int e = select_pipeline(keys, n, k, key_stats, w, kth_out, st);
+    int e = select_pipeline(keys, n, k, key_stats, w, kth_out, st, prepared);
     if (e) return e;
     return admit_with(keys, n, k, &w.state->kth, fleet, cfg, admitted, refetch, edge_idx,
                       edge_keys, w, st, w.digits);

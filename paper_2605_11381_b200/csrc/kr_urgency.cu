@@ -13,6 +13,7 @@
 // rounded like Python's int / int) and its bucket multiply.
 #include "kr_common.cuh"
 #include "kr_host.cuh"
+#include "kr_select_state.cuh"
 
 namespace kr {
 
@@ -53,6 +54,8 @@ struct UrgencyOut {
     int64_t* slot_wait;
     unsigned long long* key_stats;
     uint32_t* flags;
+    SelState* sel = nullptr;  // kr_urgency_prep: the last CTA prepares the select state
+    int64_t sel_k = 0;
 };
 
 // Per-round waits of one request (WaitLedger.waits), -1 where none recorded.
@@ -305,6 +308,17 @@ __global__ void __launch_bounds__(256, KR_URG_MINB) k_urgency(Src s, kr_sched c,
             if (~alo) atomicAnd(&o.key_stats[3], alo);
         }
     }
+    if (o.sel) {  // the last CTA to finish prepares the radix select (sel_prepare)
+        __shared__ bool last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(&o.sel->done_urg, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            sel_prepare(o.sel, s.n(), o.sel_k, o.key_stats, o.keys);
+        }
+    }
 }
 
 static unsigned grid_for(int64_t n, int threads) {
@@ -385,6 +399,22 @@ extern "C" int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* ke
     UrgencyOut o{keys, need_time, total_wait, wr, bucket, est, slot_wait, key_stats, flags};
     launch_urgency(FleetSrc{*fleet}, fleet->n, *cfg, o, as_stream(stream));
     return check_launch("kr_urgency");
+}
+
+extern "C" int kr_urgency_prep(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys,
+                               int64_t* need_time, unsigned long long* key_stats, uint32_t* flags,
+                               int64_t k, void* ws, size_t ws_bytes, void* stream) {
+    if (!fleet || !cfg || fleet->n < 0 || k < 0) return KR_EINVAL;
+    if (cfg->policy < KR_KAIROS || cfg->policy > KR_LAS || cfg->buckets < 1 ||
+        cfg->buckets > 256 || cfg->aging_interval < 1 || cfg->hz_num <= 0 || cfg->hz_den <= 0)
+        return KR_EINVAL;
+    if (fleet->n == 0) return KR_OK;
+    if (!keys || !key_stats || !ws || ws_bytes < sizeof(SelState)) return KR_EINVAL;
+    UrgencyOut o{keys, need_time, nullptr, nullptr, nullptr, nullptr, nullptr, key_stats, flags};
+    o.sel = static_cast<SelState*>(ws);  // kr_select.cu carve(): the state heads the workspace
+    o.sel_k = k;
+    launch_urgency(FleetSrc{*fleet}, fleet->n, *cfg, o, as_stream(stream));
+    return check_launch("kr_urgency_prep");
 }
 
 extern "C" int kr_urgency_ledger(const kr_ledger* ledger, const kr_requests* req,

@@ -24,6 +24,7 @@ subset of the union of local top-k' sets and keys are unique.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -119,6 +120,15 @@ class DecisionRound:
         # gets no statistics computes its own, so a wrong guess costs only time)
         self.stats_needed = not (type(self) is DecisionRound and
                                  (R <= SMALL_ADMIT_MAX or self.k == 0 or self.k >= R))
+        # rounds that run the radix select: the urgency pass's last CTA prepares
+        # the select state and leaves the statistics as the identity again
+        # (kr_urgency_prep / kr_select_admit_prepared: two launches fewer)
+        self.prepared = (type(self) is DecisionRound and self.stats_needed
+                         and not os.environ.get("KR_ROUND_NO_PREP"))
+        if self.prepared:
+            self.ws.buf.zero_()  # the state's last-CTA counter starts at 0
+            _lib.check(self.lib.kr_key_stats_init(self.key_stats.data_ptr(), dev.stream()),
+                       "kr_key_stats_init")
 
     def horizons(self, h) -> None:
         if isinstance(h, MixedInputs):
@@ -164,10 +174,16 @@ class DecisionRound:
 
     def urgency(self, fleet: fl.DeviceFleet) -> None:
         st = dev.stream()
+        fs = fleet.c_struct()
+        if self.prepared:
+            _lib.check(self.lib.kr_urgency_prep(
+                ctypes.byref(fs), ctypes.byref(self.sched), self.keys.data_ptr(),
+                self.need_time.data_ptr(), self.key_stats.data_ptr(), self.flags.data_ptr(),
+                self.k, self.ws.ptr(), self.ws.nbytes, st), "kr_urgency_prep")
+            return
         if self.stats_needed:
             _lib.check(self.lib.kr_key_stats_init(self.key_stats.data_ptr(), st),
                        "kr_key_stats_init")
-        fs = fleet.c_struct()
         _lib.check(self.lib.kr_urgency(
             ctypes.byref(fs), ctypes.byref(self.sched), self.keys.data_ptr(),
             self.need_time.data_ptr(), None, None, None, None, None,
@@ -185,6 +201,14 @@ class DecisionRound:
         raise_round_flags(f)
 
     def admit(self, fleet: fl.DeviceFleet) -> None:
+        if self.prepared:
+            fs = fleet.c_struct()
+            _lib.check(self.lib.kr_select_admit_prepared(
+                self.keys.data_ptr(), self.R, self.k, ctypes.byref(fs), ctypes.byref(self.sched),
+                self.admitted.data_ptr(), self.refetch.data_ptr(), self.edge_idx.data_ptr(),
+                self.edge_keys.data_ptr(), self.kth.data_ptr(), self.ws.ptr(), self.ws.nbytes,
+                dev.stream()), "kr_select_admit_prepared")
+            return
         fl.select_admit(self.keys, self.k, self.ws,
                         key_stats=self.key_stats if self.stats_needed else None, fleet=fleet,
                         sched=self.sched, admitted=self.admitted, refetch=self.refetch,

@@ -221,3 +221,42 @@ def test_round_flags_raise_out_of_range_keys():
     hyb.admit(rounds_fleet)
     o = hyb.outputs()
     assert torch.equal(o.kth[0], o.edge_keys[k - 1])
+
+
+@pytest.mark.parametrize("policy", ["kairos", "fifo", "las"])
+def test_prepared_select_equals_separate_reset(policy):
+    """kr_urgency_prep + kr_select_admit_prepared (the urgency pass's last CTA
+    prepares the select state and restores the statistics) decide exactly what
+    kr_urgency + kr_select_admit decide, over evolving rounds, eager and
+    graph-captured, and match the oracle."""
+    from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
+    R, k = 1 << 17, 3000
+    soa = synthetic.fleet_soa(R, seed=41)
+    prev, cand, off = synthetic.chunks(R, seed=42)
+    sched = fl.sched_struct(policy, 10, 5, 150_000, 166_667, synthetic.NOW, 30,
+                            int(soa["issued_at"].min()))
+    inp = rounds.DivergenceInputs(prev, cand, 0.9, offset=off)
+    runs = []
+    for prepared, graph in ((False, False), (True, False), (True, True)):
+        fleet = fl.DeviceFleet.from_host(soa)
+        rnd = rounds.DecisionRound(R, k, sched)
+        assert rnd.prepared
+        rnd.prepared = prepared
+        if graph:
+            rnd.capture(fleet, inp, reserve_sms=8)  # runs one round
+            fleet.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
+        seq = []
+        for _ in range(3):
+            o = rnd.replay() if graph else rnd.run(fleet, inp)
+            torch.cuda.synchronize()
+            seq.append([t.cpu().clone() for t in (o.keys, o.admitted, o.refetch, o.edge_idx,
+                                                 o.edge_keys, o.kth, fleet.t["skipped"])])
+        rnd.check()
+        runs.append(seq)
+    for other in runs[1:]:
+        for a, b in zip(runs[0], other):
+            for x, y in zip(a, b):
+                assert torch.equal(x, y)
+    res = orc.plan_soa(soa, policy, 10, 5, 150_000, 166_667, synthetic.NOW, 30, k)
+    assert np.array_equal(runs[1][0][3].numpy(), res["order"][:k])
+    assert np.array_equal(runs[1][0][1].numpy(), res["admitted"])

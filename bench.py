@@ -576,13 +576,13 @@ def other_configs(reps: int = 200):
     U = synthetic.magnitudes(R, seed=19)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))
-    # urgency pass on the whole GPU, then horizons || admission, no SM cap
-    # (profiles/r2_confidence_layouts.jsonl)
-    t = timed_captured(rnd, fleet, inp, -1, layout="urgency_first")
+    # horizons || urgency + admission, 10 reserved SMs (the steadiest of the
+    # layouts within +-5 us of each other, profiles/r2_confidence_layouts.jsonl)
+    t = timed_captured(rnd, fleet, inp, 10)
     out["configs[4] per-GPU share, confidence policy (U 2^20 x 6 x 50 fp32), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (1.26 GB of magnitudes)",
-        "layout": "urgency_first: urgency, then horizons || admission (co-resident, no SM cap)"}
+        "layout": "split: horizons || urgency + admission (10 reserved SMs)"}
     # fp64 storage (the reference's native dtype, workload.py:485-486): the
     # headline divergence round and the confidence round, same layouts
     R = 1 << 20

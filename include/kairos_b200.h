@@ -227,17 +227,18 @@ KR_API int kr_assign_bucket(const double* wr, const int32_t* skipped, int64_t n,
 KR_API int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys, int64_t* need_time,
                int64_t* total_wait, double* wr, int32_t* bucket, int64_t* est,
                int64_t* slot_wait, unsigned long long* key_stats, uint32_t* flags, void* stream);
-/* The planning round's urgency pass (kr_urgency with keys, need times and
- * key_stats) whose last CTA also prepares the radix-select state in
- * `workspace` for kr_select_admit_prepared with budget k: the state reset and
- * level-0 digit of kr_select_admit's first launch, from the statistics this
- * pass accumulated.  key_stats must hold the identity (kr_key_stats_init) on
- * the first call; the pass leaves it as the identity again, so a round needs
- * no kr_key_stats_init.  workspace as for kr_select_admit over fleet->n keys.
+/* The planning round's urgency pass (kr_urgency with keys and need times)
+ * whose last CTA also prepares the radix-select state in `workspace` for
+ * kr_select_admit_prepared with budget k: the state reset and level-0 digit
+ * of kr_select_admit's first launch, from the keys' statistics this pass
+ * reduces (per-CTA partials in the workspace, no key_stats buffer, no
+ * kr_key_stats_init).  workspace as for kr_select_admit over fleet->n keys;
+ * fleet->n >= 16,384 (smaller rounds sort every key instead), and its state's
+ * completion counter zero before the first call (a zeroed workspace).
  * scheduler.py:120-140 (keys) + the select preparation; waiting.py:69-100. */
 KR_API int kr_urgency_prep(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys,
-                           int64_t* need_time, unsigned long long* key_stats, uint32_t* flags,
-                           int64_t k, void* workspace, size_t workspace_bytes, void* stream);
+                           int64_t* need_time, uint32_t* flags, int64_t k, void* workspace,
+                           size_t workspace_bytes, void* stream);
 /* key_stats (nullable, 4 words, prepared by kr_key_stats_init) accumulates
  * {OR hi, OR lo, AND hi, AND lo} of the keys written, so the admission select
  * needs no extra pass over the keys. */

@@ -112,7 +112,7 @@ _SIGNATURES = {
                                   _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kr_key_stats_init": (ctypes.c_int, [_vp, _vp]),
     "kr_urgency_prep": (ctypes.c_int, [ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _vp, _vp,
-                                       _vp, _vp, _i64, _vp, ctypes.c_size_t, _vp]),
+                                       _vp, _i64, _vp, ctypes.c_size_t, _vp]),
     "kr_plan_small": (ctypes.c_int, [ctypes.POINTER(KrFleet), ctypes.POINTER(KrSched), _i64, _vp,
                                      _vp]),
     "kr_mapped_ptr": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),

@@ -107,17 +107,15 @@ __device__ __forceinline__ void sel_digit0(SelState* s, const kr_key* keys) {
 }
 
 // The select state for a round over n keys with budget k, from the keys'
-// OR / AND statistics accumulated in key_stats (which are left as the
-// identity for the next round's accumulation).  Run by every thread of one
-// CTA after all keys and statistics are written (the urgency pass's last CTA).
+// OR / AND statistics st4 {or_hi, or_lo, and_hi, and_lo}.  Run by every thread
+// of one CTA after all keys are written (the urgency pass's last CTA).
 __device__ __forceinline__ void sel_prepare(SelState* s, int64_t n, int64_t k,
-                                            unsigned long long* key_stats, const kr_key* keys) {
+                                            const unsigned long long* st4, const kr_key* keys) {
     for (int i = threadIdx.x; i < kBins; i += blockDim.x) s->hist[i] = 0;
     if (threadIdx.x == 0) {
-        for (int j = 0; j < 4; j++) s->st[0][j] = __ldcg(key_stats + j);
+        for (int j = 0; j < 4; j++) s->st[0][j] = st4[j];
         sel_init(s, n, k);
         sel_digit0(s, keys);
-        key_stats[0] = 0ull; key_stats[1] = 0ull; key_stats[2] = ~0ull; key_stats[3] = ~0ull;
         s->done_urg = 0;
     }
 }

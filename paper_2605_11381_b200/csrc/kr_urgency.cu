@@ -56,6 +56,7 @@ struct UrgencyOut {
     uint32_t* flags;
     SelState* sel = nullptr;  // kr_urgency_prep: the last CTA prepares the select state
     int64_t sel_k = 0;
+    unsigned long long* sel_part = nullptr;  // [gridDim][4] per-CTA key statistics (prep)
 };
 
 // Per-round waits of one request (WaitLedger.waits), -1 where none recorded.
@@ -295,6 +296,51 @@ __global__ void __launch_bounds__(256, KR_URG_MINB) k_urgency(Src s, kr_sched c,
         }
     }
     if (fl && o.flags) atomicOr(o.flags, fl);
+    if (o.sel) {
+        // prep: each CTA stores its partial statistics (no contended atomics);
+        // the last CTA to finish reduces them into the select state
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long* pp = o.sel_part + 4 * blockIdx.x;
+            pp[0] = (static_cast<unsigned long long>(red[0]) << 32) | red[1];
+            pp[1] = (static_cast<unsigned long long>(red[2]) << 32) | red[3];
+            pp[2] = (static_cast<unsigned long long>(red[4]) << 32) | red[5];
+            pp[3] = (static_cast<unsigned long long>(red[6]) << 32) | red[7];
+        }
+        __shared__ bool last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(&o.sel->done_urg, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            unsigned long long a = 0, b = 0, c = ~0ull, d = ~0ull;
+            for (unsigned g = threadIdx.x; g < gridDim.x; g += blockDim.x) {
+                const ulonglong2 v0 = __ldcg(reinterpret_cast<const ulonglong2*>(o.sel_part + 4 * g));
+                const ulonglong2 v1 = __ldcg(reinterpret_cast<const ulonglong2*>(o.sel_part + 4 * g + 2));
+                a |= v0.x; b |= v0.y; c &= v1.x; d &= v1.y;
+            }
+#pragma unroll
+            for (int t = 16; t; t >>= 1) {
+                a |= __shfl_xor_sync(0xffffffffu, a, t); b |= __shfl_xor_sync(0xffffffffu, b, t);
+                c &= __shfl_xor_sync(0xffffffffu, c, t); d &= __shfl_xor_sync(0xffffffffu, d, t);
+            }
+            __shared__ unsigned long long wred[4][8];
+            const int wp = threadIdx.x >> 5;
+            if ((threadIdx.x & 31) == 0) { wred[0][wp] = a; wred[1][wp] = b; wred[2][wp] = c; wred[3][wp] = d; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int w = 1; w < static_cast<int>(blockDim.x >> 5); w++) {
+                    a |= wred[0][w]; b |= wred[1][w]; c &= wred[2][w]; d &= wred[3][w];
+                }
+                wred[0][0] = a; wred[1][0] = b; wred[2][0] = c; wred[3][0] = d;
+            }
+            __syncthreads();
+            const unsigned long long st4[4] = {wred[0][0], wred[1][0], wred[2][0], wred[3][0]};
+            sel_prepare(o.sel, s.n(), o.sel_k, st4, o.keys);
+        }
+        return;
+    }
     if (stats) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -306,17 +352,6 @@ __global__ void __launch_bounds__(256, KR_URG_MINB) k_urgency(Src s, kr_sched c,
             if (olo) atomicOr(&o.key_stats[1], olo);
             if (~ahi) atomicAnd(&o.key_stats[2], ahi);
             if (~alo) atomicAnd(&o.key_stats[3], alo);
-        }
-    }
-    if (o.sel) {  // the last CTA to finish prepares the radix select (sel_prepare)
-        __shared__ bool last;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) last = atomicAdd(&o.sel->done_urg, 1u) == gridDim.x - 1;
-        __syncthreads();
-        if (last) {
-            __threadfence();
-            sel_prepare(o.sel, s.n(), o.sel_k, o.key_stats, o.keys);
         }
     }
 }
@@ -402,17 +437,23 @@ extern "C" int kr_urgency(const kr_fleet* fleet, const kr_sched* cfg, kr_key* ke
 }
 
 extern "C" int kr_urgency_prep(const kr_fleet* fleet, const kr_sched* cfg, kr_key* keys,
-                               int64_t* need_time, unsigned long long* key_stats, uint32_t* flags,
-                               int64_t k, void* ws, size_t ws_bytes, void* stream) {
-    if (!fleet || !cfg || fleet->n < 0 || k < 0) return KR_EINVAL;
+                               int64_t* need_time, uint32_t* flags, int64_t k, void* ws,
+                               size_t ws_bytes, void* stream) {
+    if (!fleet || !cfg || fleet->n < (int64_t(1) << 14) || k < 0) return KR_EINVAL;
     if (cfg->policy < KR_KAIROS || cfg->policy > KR_LAS || cfg->buckets < 1 ||
         cfg->buckets > 256 || cfg->aging_interval < 1 || cfg->hz_num <= 0 || cfg->hz_den <= 0)
         return KR_EINVAL;
-    if (fleet->n == 0) return KR_OK;
-    if (!keys || !key_stats || !ws || ws_bytes < sizeof(SelState)) return KR_EINVAL;
-    UrgencyOut o{keys, need_time, nullptr, nullptr, nullptr, nullptr, nullptr, key_stats, flags};
-    o.sel = static_cast<SelState*>(ws);  // kr_select.cu carve(): the state heads the workspace
+    if (!keys || !ws || ws_bytes < sizeof(SelState)) return KR_EINVAL;
+    // kr_select.cu carve(): the state heads the workspace, the level-0 digit
+    // array (n x 2 bytes, written only by the select) follows 256-byte aligned;
+    // it holds the per-CTA statistics meanwhile (grid x 32 bytes <= n x 2)
+    unsigned char* base = static_cast<unsigned char*>(ws);
+    const size_t off = (sizeof(SelState) + 255) & ~size_t(255);
+    UrgencyOut o{keys, need_time, nullptr, nullptr, nullptr, nullptr, nullptr,
+                 reinterpret_cast<unsigned long long*>(base + off), flags};
+    o.sel = reinterpret_cast<SelState*>(base);
     o.sel_k = k;
+    o.sel_part = reinterpret_cast<unsigned long long*>(base + off);
     launch_urgency(FleetSrc{*fleet}, fleet->n, *cfg, o, as_stream(stream));
     return check_launch("kr_urgency_prep");
 }

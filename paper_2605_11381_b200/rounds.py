@@ -121,14 +121,12 @@ class DecisionRound:
         self.stats_needed = not (type(self) is DecisionRound and
                                  (R <= SMALL_ADMIT_MAX or self.k == 0 or self.k >= R))
         # rounds that run the radix select: the urgency pass's last CTA prepares
-        # the select state and leaves the statistics as the identity again
-        # (kr_urgency_prep / kr_select_admit_prepared: two launches fewer)
+        # the select state from per-CTA statistics (kr_urgency_prep /
+        # kr_select_admit_prepared: two launches fewer)
         self.prepared = (type(self) is DecisionRound and self.stats_needed
                          and not os.environ.get("KR_ROUND_NO_PREP"))
         if self.prepared:
             self.ws.buf.zero_()  # the state's last-CTA counter starts at 0
-            _lib.check(self.lib.kr_key_stats_init(self.key_stats.data_ptr(), dev.stream()),
-                       "kr_key_stats_init")
 
     def horizons(self, h) -> None:
         if isinstance(h, MixedInputs):
@@ -178,8 +176,8 @@ class DecisionRound:
         if self.prepared:
             _lib.check(self.lib.kr_urgency_prep(
                 ctypes.byref(fs), ctypes.byref(self.sched), self.keys.data_ptr(),
-                self.need_time.data_ptr(), self.key_stats.data_ptr(), self.flags.data_ptr(),
-                self.k, self.ws.ptr(), self.ws.nbytes, st), "kr_urgency_prep")
+                self.need_time.data_ptr(), self.flags.data_ptr(), self.k, self.ws.ptr(),
+                self.ws.nbytes, st), "kr_urgency_prep")
             return
         if self.stats_needed:
             _lib.check(self.lib.kr_key_stats_init(self.key_stats.data_ptr(), st),

@@ -1106,6 +1106,9 @@ __global__ void __launch_bounds__(256) k_rs_scatter(const kr_key* keys, const in
 #ifndef KR_MERGE_SAMPLED
 #define KR_MERGE_SAMPLED 0  // 1: sample-staged rank merge
 #endif
+#ifndef KR_GROUP_MIN_RUNS
+#define KR_GROUP_MIN_RUNS 16  // more runs than this (4k pairs): grouped rank-merge passes
+#endif
 // KR_MERGE_UNSAMPLED=1: the plain binary-search merge (A/B measurements).
 static bool merge_unsampled() {
     static bool v = [] {
@@ -1131,18 +1134,21 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
         // runs are written to the sort ping-pong buffer not holding the input
         kr_key* rk = keys == w.skeys[1] ? w.skeys[0] : w.skeys[1];
         int32_t* ri = keys == w.skeys[1] ? w.sidx[0] : w.sidx[1];
-        // more than 32 runs (> 8k pairs): grouped merge passes (both outputs
+        // more than KR_GROUP_MIN_RUNS runs: grouped merge passes (both outputs
         // given), G = 8 until at most 8 runs remain, the runs ping-ponging
         // between the outputs and the select's candidate buffers (unused by
-        // every sort_pairs caller), landing in out.  Up to 32 runs the flat
-        // merge's one search per lane is faster (4k pairs: 22 vs 27 us).
+        // every sort_pairs caller), landing in out.  At 8k pairs (32 runs) two
+        // grouped passes (7 + 3 searches per pair) beat one flat pass of 31
+        // L2-resident searches: the bench round 483.8 -> 476.3 us, configs[3]
+        // 148.7 -> 137.7 us (tools/ab_configs.sh); the flat merge stays for
+        // at most 16 runs.
         static const bool grouped_off = std::getenv("KR_MERGE_FLAT") != nullptr;  // A/B knob
         const int runs0 = (m + kRun - 1) / kRun;
         if (apply && runs0 == 1) {  // one run is the whole order
             k_run_sort<<<1, kRunThreads, 0, st>>>(sk, si, count_dev, m, rk, ri, av, 1);
             return check_launch("run sort (apply)");
         }
-        if (!grouped_off && out_idx && out_keys && runs0 > 32) {
+        if (!grouped_off && out_idx && out_keys && runs0 > KR_GROUP_MIN_RUNS) {
             int lg[8], P = 0;
             for (int r = runs0; r > 1 && P < 8; P++) {
                 int g = 0;

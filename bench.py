@@ -564,10 +564,10 @@ def other_configs(reps: int = 200):
     prev, cand, off = synthetic.chunks(R, seed=17, S=8)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.DivergenceInputs(prev, cand, THR, offset=off)
-    t = timed_captured(rnd, fleet, inp, 4)
+    t = timed_captured(rnd, fleet, inp, 1)
     out["configs[3] 64k robots S=8 ensembles 50x7 k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
-        "l2": "streams from HBM (826 MB inputs)", "layout": "split, 4 reserved SMs"}
+        "l2": "streams from HBM (826 MB inputs)", "layout": "split, 1 reserved SM"}
     # the headline fleet with the confidence policy (paper default t=0.4, H_min=5)
     from paper_2605_11381_b200 import HorizonPolicyConfig
     R = 1 << 20
@@ -576,13 +576,13 @@ def other_configs(reps: int = 200):
     U = synthetic.magnitudes(R, seed=19)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))
-    # horizons || urgency + admission, 10 reserved SMs (the steadiest of the
-    # layouts within +-5 us of each other, profiles/r2_confidence_layouts.jsonl)
-    t = timed_captured(rnd, fleet, inp, 10)
+    # horizons || urgency + admission, 16 reserved SMs (median of four
+    # interleaved repeats per layout, tools/conf_layout_reps.py)
+    t = timed_captured(rnd, fleet, inp, 16)
     out["configs[4] per-GPU share, confidence policy (U 2^20 x 6 x 50 fp32), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (1.26 GB of magnitudes)",
-        "layout": "split: horizons || urgency + admission (10 reserved SMs)"}
+        "layout": "split: horizons || urgency + admission (16 reserved SMs)"}
     # fp64 storage (the reference's native dtype, workload.py:485-486): the
     # headline divergence round and the confidence round, same layouts
     R = 1 << 20
@@ -590,10 +590,10 @@ def other_configs(reps: int = 200):
     fleet = fl.DeviceFleet.from_host(soa)
     prev, cand, off = synthetic.chunks(R, seed=24, dtype=torch.float64)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
-    t = timed_captured(rnd, fleet, rounds.DivergenceInputs(prev, cand, THR, offset=off), 10)
+    t = timed_captured(rnd, fleet, rounds.DivergenceInputs(prev, cand, THR, offset=off), 2)
     out["configs[4] per-GPU share, fp64 chunks (50x7 fp64), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
-        "l2": "streams from HBM (5.9 GB of chunks)", "layout": "split, 10 reserved SMs",
+        "l2": "streams from HBM (5.9 GB of chunks)", "layout": "split, 2 reserved SMs",
         "round_GBps": (DIV_BYTES * 2 - 8) * R / t / 1e9}
     del prev, cand
     U = synthetic.magnitudes(R, seed=25, dtype=torch.float64)
@@ -817,7 +817,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--eager", action="store_true",
                     help="N=1: the N>1 path (eager launches, side-stream overlap) instead of graphs")
-    ap.add_argument("--reserve-sms", type=int, default=10,
+    ap.add_argument("--reserve-sms", type=int, default=2,
                     help="SMs left to urgency + admission (side stream) during the horizon kernel")
     ap.add_argument("--layout", choices=["split", "urgency_first"], default="split",
                     help="graph layout of the round (see rounds.DecisionRound.capture)")

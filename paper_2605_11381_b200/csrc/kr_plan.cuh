@@ -3,6 +3,7 @@
 // and the cached launcher.
 #pragma once
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -78,11 +79,11 @@ static StreamPlan make_plan(int nseg, const void* const* base, const uint64_t* r
         per_sm = per_sm < 2048 / cta ? per_sm : 2048 / cta;
         per_sm = per_sm > 4 ? 4 : per_sm;
         for (; per_sm >= 1; per_sm--) {
-            const uint64_t budget = smem_sm / per_sm - 1024 - 128;  // 1 KB reserved per CTA
+            const uint64_t budget = smem_sm / per_sm - 1024 - 128 - kStreamStaticSmem;  // 1 KB reserved per CTA
             if (aux + 2 * sb <= budget) break;
         }
         if (per_sm < 1) continue;
-        const uint64_t budget = smem_sm / per_sm - 1024 - 128;
+        const uint64_t budget = smem_sm / per_sm - 1024 - 128 - kStreamStaticSmem;
         int stages = static_cast<int>((budget - aux) / sb);
         stages = stages > max_stages ? max_stages : stages;
         static const int max_stages_env = std::getenv("KR_PLAN_MAX_STAGES")
@@ -146,6 +147,28 @@ static int kernel_regs(K kern) {
     return f.regs;
 }
 
+// Tile counters of the dynamic schedule (kr_stream.cuh stream_run): a pool
+// per translation unit, one {claimed, done} pair per launch, rotating so that
+// concurrently running launches (the mixed fleet's two horizon kernels, a
+// horizon kernel beside the side stream) never share one; each launch's last
+// CTA zeroes its pair, so CUDA-graph replays start from zero too.
+constexpr int kStreamCtrSlots = 256;
+static __device__ unsigned g_stream_ctr[2 * kStreamCtrSlots];
+static unsigned* stream_counters() {
+    static unsigned* base = [] {
+        void* p = nullptr;
+        return cudaGetSymbolAddress(&p, g_stream_ctr) == cudaSuccess ? static_cast<unsigned*>(p)
+                                                                      : nullptr;
+    }();
+    static std::atomic<unsigned> next{0};
+    if (!base) return nullptr;
+    return base + 2 * (next.fetch_add(1) % kStreamCtrSlots);
+}
+static bool dynamic_tiles() {
+    static const bool off = std::getenv("KR_STATIC_TILES") != nullptr;  // A/B knob
+    return !off;
+}
+
 template <class Work, class KStaged, class KDirect, class... Extra>
 static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, const Work& w,
                          cudaStream_t st, const char* name, int max_sms = 0,
@@ -190,7 +213,13 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
                          "mode=%d stage_bytes=%u smem=%zu grid=%lld per_sm=%d\n", name,
                          static_cast<long long>(p.R), p.TR, p.threads, p.rounds, p.stages, p.mode,
                          p.stage_bytes, smem, static_cast<long long>(grid), per_sm);
-        kern<<<static_cast<unsigned>(grid), p.threads + 32, smem, st>>>(p, w, extra...);
+        StreamPlan pd = p;
+        // the dynamic tail needs several tiles per CTA to balance (configs[1],
+        // 1k robots, one tile per CTA: +2 us from the claims alone)
+        if (p.mode == kModeBulk && !p.static_tiles && dynamic_tiles() && ntiles >= 8 * grid &&
+            ntiles < (int64_t(1) << 31))
+            pd.ctr = stream_counters();
+        kern<<<static_cast<unsigned>(grid), p.threads + 32, smem, st>>>(pd, w, extra...);
         return check_launch(name);
     };
     return p.mode == kModeDirect ? go(kdirect) : go(kstaged);

@@ -26,6 +26,10 @@ constexpr int kMaxSeg = 5;
 constexpr int kMaxRounds = 4;      // item positions per thread per tile
 constexpr int kStreamThreads = 1024;
 constexpr int kMaxStages = 8;      // ring depth (mbarrier slots)
+constexpr int kStreamStaticSmem = 64;  // stream_run's static shared memory (dynamic tile ids)
+#ifndef KR_DYN_TAIL_DIV
+#define KR_DYN_TAIL_DIV 8  // the last ~1/8 of the tiles are claimed dynamically
+#endif
 
 // Segments have fixed slots (unused slots: rbytes 0) so that every segment
 // pointer is a compile-time-indexed register, never a local-memory array.
@@ -43,6 +47,8 @@ struct StreamPlan {
     int rounds;                          // ceil(TR * items_per_robot / threads) <= kMaxRounds
     int max_per_sm;                      // resident CTAs per SM cap (0: occupancy decides)
     int64_t R;
+    unsigned* ctr;                       // TMA mode: {tiles claimed, CTAs done} (null: static)
+    int static_tiles;                    // launcher hint: keep the static schedule
 };
 
 enum { kModeBulk = 0, kModePlain = 1, kModeDirect = 2 };
@@ -58,8 +64,9 @@ __host__ inline size_t stream_smem_bytes(const StreamPlan& p) {
 }
 
 __device__ __forceinline__ void stream_issue(const StreamPlan& p, unsigned char* buf,
-                                             uint64_t* bar, int64_t local, uint64_t pol) {
-    int64_t t = blockIdx.x + local * gridDim.x;
+                                             uint64_t* bar, int64_t local, uint64_t pol,
+                                             int64_t tile = -1) {
+    int64_t t = tile >= 0 ? tile : blockIdx.x + local * gridDim.x;
     int64_t r0 = t * p.TR;
     int64_t nr = p.R - r0 < p.TR ? p.R - r0 : p.TR;
     uint32_t total = 0;
@@ -147,6 +154,100 @@ __device__ __forceinline__ void stream_run(const StreamPlan& p, unsigned char* s
             nr = static_cast<int>(p.R - r0 < p.TR ? p.R - r0 : p.TR);
         }
     };
+    if (bulk && p.ctr) {
+        // Dynamic tiles: the producer claims each tile from a grid-wide counter
+        // when it (re)fills a slot and leaves its index in tid_s[slot] (or -1:
+        // none left, the slot's full barrier completed without bytes), so CTAs
+        // that start late -- their SM held by the side stream's kernels -- take
+        // fewer tiles instead of finishing a fixed share last.  The last CTA
+        // done claiming resets the counters for the next launch.
+        __shared__ int tid_s[kMaxStages];
+        static_assert(sizeof(tid_s) <= kStreamStaticSmem, "plan budget");
+        const unsigned nt = static_cast<unsigned>(ntiles);
+        // a static prefix (round-robin, no atomics) of whole rounds over the
+        // grid, then the tail claimed from the counter
+        const unsigned G = gridDim.x;
+        const unsigned nstat = (nt - nt / KR_DYN_TAIL_DIV) / G;  // static tiles per CTA
+        const unsigned tail0 = nstat * G;
+        unsigned next_stat = 0;
+        auto fill = [&](int slot) {  // producer lane 0
+            const unsigned t = next_stat < nstat ? blockIdx.x + (next_stat++) * G
+                                                 : tail0 + atomicAdd(p.ctr, 1u);
+            if (t < nt) {
+                tid_s[slot] = static_cast<int>(t);
+                stream_issue(p, bufs + static_cast<size_t>(slot) * p.stage_bytes, &full[slot], 0, pol, t);
+            } else {
+                tid_s[slot] = -1;
+                mbar_arrive(&full[slot]);
+            }
+        };
+        auto tile_at = [&](int t, int64_t& r0, int& nr) {
+            r0 = static_cast<int64_t>(t) * p.TR;
+            nr = static_cast<int>(p.R - r0 < p.TR ? p.R - r0 : p.TR);
+        };
+        if (producer) {
+            if (lane == 0)
+                for (int s = 0; s < p.stages; s++) fill(s);
+            __syncwarp();
+            int s = 0;
+            uint32_t phase = 0;
+            for (;;) {
+                const int t = *reinterpret_cast<volatile int*>(&tid_s[s]);
+                if (t < 0) break;
+                int64_t r0;
+                int nr;
+                tile_at(t, r0, nr);
+                mbar_wait(&empty[s], phase);
+                work.finish(r0, nr, s, lane, 32);
+                __syncwarp();
+                if (lane == 0) fill(s);
+                __syncwarp();
+                if (++s == p.stages) {
+                    s = 0;
+                    phase ^= 1u;
+                }
+            }
+            if (lane == 0 && atomicAdd(p.ctr + 1, 1u) == gridDim.x - 1) {
+                p.ctr[0] = 0;
+                p.ctr[1] = 0;
+            }
+            return;
+        }
+        int s = 0;
+        uint32_t phase = 0;
+        for (;;) {
+            mbar_wait(&full[s], phase);
+            const int t = *reinterpret_cast<volatile int*>(&tid_s[s]);
+            if (t < 0) break;
+            int64_t r0;
+            int nr;
+            tile_at(t, r0, nr);
+            unsigned char* buf = bufs + static_cast<size_t>(s) * p.stage_bytes;
+            if (nr < p.TR) {  // last tile: sub-16-byte remainder by hand (generic-proxy writes)
+                for (int g = 0; g < kMaxSeg; g++) {
+                    if (p.rbytes[g] == 0) continue;
+                    const uint32_t bytes = static_cast<uint32_t>(nr * p.rbytes[g]);
+                    const uint32_t* src = reinterpret_cast<const uint32_t*>(p.base[g] + r0 * p.rbytes[g]);
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(buf + p.soff[g]);
+                    for (uint32_t w = (bytes & ~15u) / 4 + threadIdx.x; w < bytes / 4; w += p.threads)
+                        dst[w] = __ldg(src + w);
+                }
+                fence_proxy_async_smem();
+                asm volatile("bar.sync 1, %0;" ::"r"(p.threads));  // consumer warps only
+            }
+            TileView v;
+#pragma unroll
+            for (int g = 0; g < kMaxSeg; g++) v.seg[g] = buf + p.soff[g];
+            work.tile(v, r0, nr, s);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == p.stages) {
+                s = 0;
+                phase ^= 1u;
+            }
+        }
+        return;
+    }
     if (bulk && producer) {
         // producer warp: fill the ring, then per tile wait until every consumer
         // warp has released the slot, finish the tile, refill the slot

@@ -1072,6 +1072,9 @@ int sweep_run(const void* U, int64_t R, int32_t K, int32_t N, int32_t C, int32_t
                                      static_cast<uint32_t>(sizeof(SweepTables)) + task_bytes, tr,
                                      st_env >= 2 ? st_env : kMaxStages);
             p.max_per_sm = psm_env;
+            // fp64 keeps the static schedule: the fp64 confidence round's median
+            // 494 -> 478 us static (tools/conf_layout_reps.py, 4 interleaved reps)
+            p.static_tiles = sizeof(T) == 8;
             if ((R / device_info().sm_count + 1) * static_cast<int64_t>(N) >= (int64_t(1) << 32))
                 return KR_EINVAL;
             W w{};

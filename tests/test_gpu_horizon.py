@@ -369,3 +369,33 @@ def test_segmented_validation_and_negative_zero(kb, storage):
         exp = orc.horizon_conf_batch(Un, t, h)
         assert np.array_equal(kb.decide_horizon_batch(cfg, Ut).cpu().numpy(), exp)
         assert int(kb.sweep_horizon_sums([cfg], Ut).cpu()[0]) == int(exp.sum())
+
+
+def test_dynamic_tile_counters_across_launches(kb):
+    """The horizon kernels' tail tiles are claimed from per-launch counter
+    slots (kr_plan.cuh stream_counters, 256 per library unit) that each
+    launch's last CTA resets: 300 back-to-back launches -- more than the pool,
+    eager and from one CUDA graph -- must all decide exactly what the oracle
+    decides (a counter left non-zero would skip tiles)."""
+    from paper_2605_11381_b200 import synthetic
+    from paper_2605_11381_b200.divergence import round_optimal_horizon_batch
+    R = 1 << 16  # many tiles per CTA: the dynamic tail is in use
+    prev, cand, off = synthetic.chunks(R, seed=5)
+    exp = orc.divergence_batch(prev.cpu().numpy(), cand.cpu().numpy(), 0.9,
+                               off.cpu().numpy(), None, None)
+    out = torch.empty(R, dtype=torch.int32, device="cuda")
+    hs = []
+    for i in range(300):
+        round_optimal_horizon_batch(prev, cand, 0.9, off, out=out)
+        if i % 50 == 0:
+            hs.append(out.clone())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        round_optimal_horizon_batch(prev, cand, 0.9, off, out=out)
+    for _ in range(20):
+        out.fill_(-1)
+        g.replay()
+    hs.append(out.clone())
+    torch.cuda.synchronize()
+    for h in hs:
+        assert np.array_equal(h.cpu().numpy(), exp)

@@ -147,22 +147,29 @@ static int kernel_regs(K kern) {
     return f.regs;
 }
 
-// Tile counters of the dynamic schedule (kr_stream.cuh stream_run): a pool
-// per translation unit, one {claimed, done} pair per launch, rotating so that
-// concurrently running launches (the mixed fleet's two horizon kernels, a
-// horizon kernel beside the side stream) never share one; each launch's last
-// CTA zeroes its pair, so CUDA-graph replays start from zero too.
-constexpr int kStreamCtrSlots = 256;
+// Tile counters of the dynamic schedule (kr_stream.cuh stream_run): one
+// {claimed, done} pair per launch captured into a CUDA graph, never reused (a
+// replayed graph keeps its pair, and no two graphs -- nor a graph and another
+// launch -- can ever share one, however they overlap); each launch's last CTA
+// zeroes its pair, so every replay starts from zero.  Eager launches keep the
+// static schedule; a process that captures more than kStreamCtrSlots launches
+// per library unit falls back to it too.
+constexpr int kStreamCtrSlots = 4096;
 static __device__ unsigned g_stream_ctr[2 * kStreamCtrSlots];
-static unsigned* stream_counters() {
+static unsigned* stream_counters(cudaStream_t st) {
+    // resolved on the first launch (normally an eager warm-up, outside capture)
     static unsigned* base = [] {
         void* p = nullptr;
         return cudaGetSymbolAddress(&p, g_stream_ctr) == cudaSuccess ? static_cast<unsigned*>(p)
                                                                       : nullptr;
     }();
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusActive)
+        return nullptr;
     static std::atomic<unsigned> next{0};
     if (!base) return nullptr;
-    return base + 2 * (next.fetch_add(1) % kStreamCtrSlots);
+    const unsigned k = next.fetch_add(1);
+    return k < static_cast<unsigned>(kStreamCtrSlots) ? base + 2 * k : nullptr;
 }
 static bool dynamic_tiles() {
     static const bool off = std::getenv("KR_STATIC_TILES") != nullptr;  // A/B knob
@@ -218,7 +225,7 @@ static int launch_stream(KStaged kstaged, KDirect kdirect, const StreamPlan& p, 
         // 1k robots, one tile per CTA: +2 us from the claims alone)
         if (p.mode == kModeBulk && !p.static_tiles && dynamic_tiles() && ntiles >= 8 * grid &&
             ntiles < (int64_t(1) << 31))
-            pd.ctr = stream_counters();
+            pd.ctr = stream_counters(st);
         kern<<<static_cast<unsigned>(grid), p.threads + 32, smem, st>>>(pd, w, extra...);
         return check_launch(name);
     };

@@ -372,30 +372,38 @@ def test_segmented_validation_and_negative_zero(kb, storage):
 
 
 def test_dynamic_tile_counters_across_launches(kb):
-    """The horizon kernels' tail tiles are claimed from per-launch counter
-    slots (kr_plan.cuh stream_counters, 256 per library unit) that each
-    launch's last CTA resets: 300 back-to-back launches -- more than the pool,
-    eager and from one CUDA graph -- must all decide exactly what the oracle
-    decides (a counter left non-zero would skip tiles)."""
+    """Launches captured into CUDA graphs claim their tail tiles from a counter
+    pair of their own (kr_plan.cuh stream_counters) that each replay's last CTA
+    resets; eager launches keep the static schedule.  Three graphs replayed
+    interleaved, 20 times each, on two streams, and 50 eager launches must all
+    decide exactly what the oracle decides (a counter left non-zero, or shared
+    by two graphs, would skip tiles)."""
     from paper_2605_11381_b200 import synthetic
     from paper_2605_11381_b200.divergence import round_optimal_horizon_batch
     R = 1 << 16  # many tiles per CTA: the dynamic tail is in use
     prev, cand, off = synthetic.chunks(R, seed=5)
     exp = orc.divergence_batch(prev.cpu().numpy(), cand.cpu().numpy(), 0.9,
                                off.cpu().numpy(), None, None)
-    out = torch.empty(R, dtype=torch.int32, device="cuda")
-    hs = []
-    for i in range(300):
-        round_optimal_horizon_batch(prev, cand, 0.9, off, out=out)
-        if i % 50 == 0:
-            hs.append(out.clone())
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        round_optimal_horizon_batch(prev, cand, 0.9, off, out=out)
+    outs = [torch.empty(R, dtype=torch.int32, device="cuda") for _ in range(4)]
+    for _ in range(50):
+        round_optimal_horizon_batch(prev, cand, 0.9, off, out=outs[3])
+    graphs = []
+    for j in range(3):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            round_optimal_horizon_batch(prev, cand, 0.9, off, out=outs[j])
+        graphs.append(g)
+    side = torch.cuda.Stream()
     for _ in range(20):
-        out.fill_(-1)
-        g.replay()
-    hs.append(out.clone())
-    torch.cuda.synchronize()
-    for h in hs:
-        assert np.array_equal(h.cpu().numpy(), exp)
+        for j, g in enumerate(graphs):
+            outs[j].fill_(-1)
+            if j == 1:  # one graph on a second stream, overlapping the others
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    g.replay()
+            else:
+                g.replay()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.array_equal(o.cpu().numpy(), exp)

@@ -157,19 +157,23 @@ static int kernel_regs(K kern) {
 constexpr int kStreamCtrSlots = 4096;
 static __device__ unsigned g_stream_ctr[2 * kStreamCtrSlots];
 static unsigned* stream_counters(cudaStream_t st) {
-    // resolved on the first launch (normally an eager warm-up, outside capture)
-    static unsigned* base = [] {
-        void* p = nullptr;
-        return cudaGetSymbolAddress(&p, g_stream_ctr) == cudaSuccess ? static_cast<unsigned*>(p)
-                                                                      : nullptr;
-    }();
+    // the pool's address is resolved by a launch outside capture (an eager
+    // warm-up); a capture before any such launch keeps the static schedule
+    static std::atomic<unsigned*> base{nullptr};
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusActive)
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return nullptr;
+    if (cs == cudaStreamCaptureStatusNone) {
+        if (!base.load()) {
+            void* p = nullptr;
+            if (cudaGetSymbolAddress(&p, g_stream_ctr) == cudaSuccess)
+                base.store(static_cast<unsigned*>(p));
+        }
         return nullptr;
+    }
+    if (cs != cudaStreamCaptureStatusActive || !base.load()) return nullptr;
     static std::atomic<unsigned> next{0};
-    if (!base) return nullptr;
     const unsigned k = next.fetch_add(1);
-    return k < static_cast<unsigned>(kStreamCtrSlots) ? base + 2 * k : nullptr;
+    return k < static_cast<unsigned>(kStreamCtrSlots) ? base.load() + 2 * k : nullptr;
 }
 static bool dynamic_tiles() {
     static const bool off = std::getenv("KR_STATIC_TILES") != nullptr;  // A/B knob

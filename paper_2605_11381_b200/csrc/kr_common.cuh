@@ -47,6 +47,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Programmatic dependent launch: wait until the same-stream predecessor grid
+// has completed and its memory is visible (a no-op for a plain launch).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Global -> shared bulk copy through the TMA engine; completion is signalled
 // as transaction bytes on `bar`.  dst, src and bytes must be 16-byte aligned.
 // The evict-first L2 policy keeps the one-pass action-chunk stream from

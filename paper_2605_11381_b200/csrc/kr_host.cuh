@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/kairos_b200.h"
@@ -25,6 +26,32 @@ inline int check_launch(const char* where, int launches = 1) {
         return KR_ECUDA;
     }
     return KR_OK;
+}
+
+// Programmatic dependent launch for the admission chain's kernels (each
+// begins with griddep_wait(), so it may be scheduled while its same-stream
+// predecessor drains and then waits for that grid's completion and memory
+// flush): the launch latency of one kernel overlaps the tail of the previous.
+// KR_NO_PDL=1 launches them plainly (A/B knob).  A failed launch leaves its
+// error for check_launch, like <<<>>>.
+inline bool pdl_on() {
+    static const bool off = std::getenv("KR_NO_PDL") != nullptr;
+    return !off;
+}
+template <typename... ExpTypes, typename... ActTypes>
+inline void launch_pdl(void (*kern)(ExpTypes...), dim3 grid, dim3 block, cudaStream_t st,
+                       ActTypes&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    (void)cudaLaunchKernelEx(&cfg, kern, static_cast<ExpTypes>(args)...);
 }
 
 #define KR_CUDA_TRY(expr)                                  \

@@ -235,6 +235,7 @@ __device__ void sel_pick_block(SelState* s, const Digit& d, const unsigned int* 
 // Level 0 over all keys: digits[i] and the histogram; the last CTA picks d*.
 __global__ void __launch_bounds__(256) k_sel_hist0(const kr_key* __restrict__ keys, int64_t n,
                                                    uint16_t* __restrict__ digits, SelState* s) {
+    griddep_wait();
     __shared__ unsigned int h[kBins];
     __shared__ Digit sd;
     __shared__ int sdone;
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(256) k_sel_scatter0(const kr_key* __restrict__
                                                       const uint16_t* __restrict__ digits,
                                                       kr_key* cand, kr_key* spare, SelState* s,
                                                       kr_key* kth_out) {
+    griddep_wait();
     __shared__ unsigned sdstar;
     __shared__ int ssingle, sdone;
     if (threadIdx.x == 0) {
@@ -475,6 +477,7 @@ __global__ void k_admit_init(SelState* s) {
 // (key, index) pairs are appended per warp (one atomic per warp; their order
 // is fixed by the sort that follows).
 __global__ void __launch_bounds__(256) k_admit(AdmitArgs a) {
+    griddep_wait();
     kr_key kth{~0ull, ~0ull};
     if (!a.all && !a.none) kth = *a.kth;
     const bool dig = a.digits && !a.all && !a.none;
@@ -684,6 +687,7 @@ __global__ void __launch_bounds__(kRunThreads) k_run_sort(const kr_key* keys, co
                                                           kr_key* rk, int32_t* ri,
                                                           SmallAdmitArgs a = SmallAdmitArgs{},
                                                           int apply = 0) {
+    griddep_wait();
     static_assert(kRun == 2 * kRunThreads, "two elements per thread");
     __shared__ Pair sp[kRun];
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
@@ -767,6 +771,7 @@ __global__ void __launch_bounds__(256) k_run_merge(const kr_key* rk, const int32
                                                    const unsigned int* count_dev, int m_host,
                                                    int32_t* out_idx, kr_key* out_keys,
                                                    SmallAdmitArgs a = SmallAdmitArgs{}, int apply = 0) {
+    griddep_wait();
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
     const int nruns = (m + kRun - 1) / kRun;
     const int lane = threadIdx.x & 31;
@@ -805,6 +810,7 @@ __global__ void __launch_bounds__(256) k_run_merge_group(const kr_key* rk, const
                                                          kr_key* out_keys,
                                                          SmallAdmitArgs a = SmallAdmitArgs{},
                                                          int apply = 0) {
+    griddep_wait();
     const int m = count_dev ? min(static_cast<int>(*count_dev), m_host) : m_host;
     const int G = 1 << lgG;
     const int nruns = (m + L - 1) / L;
@@ -1145,7 +1151,7 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
         static const bool grouped_off = std::getenv("KR_MERGE_FLAT") != nullptr;  // A/B knob
         const int runs0 = (m + kRun - 1) / kRun;
         if (apply && runs0 == 1) {  // one run is the whole order
-            k_run_sort<<<1, kRunThreads, 0, st>>>(sk, si, count_dev, m, rk, ri, av, 1);
+            launch_pdl(k_run_sort, 1, kRunThreads, st, sk, si, count_dev, m, rk, ri, av, 1);
             return check_launch("run sort (apply)");
         }
         if (!grouped_off && out_idx && out_keys && runs0 > KR_GROUP_MIN_RUNS) {
@@ -1161,7 +1167,8 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
             // the run sort's target: out when an even number of passes follows
             kr_key* ck = P % 2 == 0 ? out_keys : tk;
             int32_t* ci = P % 2 == 0 ? out_idx : ti;
-            k_run_sort<<<(m + kRun - 1) / kRun, kRunThreads, 0, st>>>(sk, si, count_dev, m, ck, ci);
+            launch_pdl(k_run_sort, (m + kRun - 1) / kRun, kRunThreads, st, sk, si, count_dev, m, ck,
+                       ci, SmallAdmitArgs{}, 0);
             int L = kRun;
             for (int q = 0; q < P; q++) {
                 kr_key* dk = (P - 1 - q) % 2 == 0 ? out_keys : tk;
@@ -1169,15 +1176,16 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
                 const int64_t warps = (static_cast<int64_t>(m) + (32 >> lg[q]) - 1) / (32 >> lg[q]);
                 int64_t blocks = (warps + 7) / 8;
                 if (blocks > 148 * 64) blocks = 148 * 64;
-                k_run_merge_group<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-                    ck, ci, count_dev, m, L, lg[q], di, dk, av, apply && q == P - 1);
+                launch_pdl(k_run_merge_group, static_cast<unsigned>(blocks), 256, st, ck, ci, count_dev,
+                           m, L, lg[q], di, dk, av, apply && q == P - 1 ? 1 : 0);
                 ck = dk;
                 ci = di;
                 L <<= lg[q];
             }
             return check_launch("run sort (grouped merge)", 1 + P);
         }
-        k_run_sort<<<(m + kRun - 1) / kRun, kRunThreads, 0, st>>>(sk, si, count_dev, m, rk, ri);
+        launch_pdl(k_run_sort, (m + kRun - 1) / kRun, kRunThreads, st, sk, si, count_dev, m, rk, ri,
+                   SmallAdmitArgs{}, 0);
         const int64_t warps = m;
         int64_t blocks = (warps + 7) / 8;
         if (blocks > 148 * 64) blocks = 148 * 64;
@@ -1188,8 +1196,8 @@ static int sort_pairs(const Workspace& w, const kr_key* keys, const int32_t* idx
                 rk, ri, count_dev, m, out_idx, out_keys);
         }
         else
-            k_run_merge<<<static_cast<unsigned>(blocks), 256, 0, st>>>(rk, ri, count_dev, m,
-                                                                       out_idx, out_keys, av, apply);
+            launch_pdl(k_run_merge, static_cast<unsigned>(blocks), 256, st, rk, ri, count_dev, m,
+                       out_idx, out_keys, av, apply);
         return check_launch("run sort", 2);
     }
     // window plan from OR ^ AND of the set (read back: one stream sync)
@@ -1384,8 +1392,8 @@ static int select_pipeline(const kr_key* keys, int64_t n, int64_t k,
     }
     static int per_sm_h = sel_ctas_per_sm(occupancy(k_sel_hist0, 256));
     static int per_sm_s = sel_ctas_per_sm(occupancy(k_sel_scatter0, 256));
-    k_sel_hist0<<<grid_cap(n, 256 * kSelU, per_sm_h), 256, 0, st>>>(keys, n, w.digits, s);
-    k_sel_scatter0<<<grid_cap(n, 256 * kScatW, per_sm_s), 256, 0, st>>>(keys, n, w.digits, w.cand[0],
+    launch_pdl(k_sel_hist0, grid_cap(n, 256 * kSelU, per_sm_h), 256, st, keys, n, w.digits, s);
+    launch_pdl(k_sel_scatter0, grid_cap(n, 256 * kScatW, per_sm_s), 256, st, keys, n, w.digits, w.cand[0],
                                                                    w.cand[1], s, kth_out);
     return check_launch("select", launches);
 }
@@ -1547,7 +1555,7 @@ static int admit_with(const kr_key* keys, int64_t n, int64_t k, const kr_key* kt
         k_admit_dig<<<grid_cap(n, 256 * 4, per_sm), 256, 0, st>>>(a);
     } else {
         static int per_sm = occupancy(k_admit, 256);
-        k_admit<<<grid_cap(n, 256, per_sm), 256, 0, st>>>(a);
+        launch_pdl(k_admit, grid_cap(n, 256, per_sm), 256, st, a);
     }
     int e = check_launch("k_admit", init ? 2 : 1);
     if (e || !gather) return e;

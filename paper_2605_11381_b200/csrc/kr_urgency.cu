@@ -261,6 +261,7 @@ __device__ __forceinline__ kr_key urgency_one(const Src& s, const kr_sched& c, c
 template <class Src, class Idx, bool LEAN = false>
 __global__ void __launch_bounds__(256, KR_URG_MINB) k_urgency(Src s, kr_sched c, UrgConst u,
                                                               UrgencyOut o) {
+    griddep_wait();  // programmatic dependent launch (kr_host.cuh launch_pdl)
     // select statistics (OR / AND of the keys) per thread, then per warp and
     // block (a per-iteration redux.sync variant measured 4% slower)
     __shared__ uint32_t red[8];  // OR hi.hi, hi.lo, lo.hi, lo.lo | AND (same order)
@@ -375,13 +376,13 @@ static void launch_urgency(const Src& src, int64_t n, const kr_sched& c, const U
                       !o.bucket && !o.est && !o.slot_wait;
     if (lean && n < (int64_t(1) << 31)) {
         static int per_sm = occupancy(k_urgency<Src, int32_t, true>, 256);
-        k_urgency<Src, int32_t, true><<<grid_cap(n, 256, per_sm), 256, 0, st>>>(src, c, u, o);
+        launch_pdl(k_urgency<Src, int32_t, true>, grid_cap(n, 256, per_sm), 256, st, src, c, u, o);
     } else if (n < (int64_t(1) << 31)) {
         static int per_sm = occupancy(k_urgency<Src, int32_t>, 256);
-        k_urgency<Src, int32_t><<<grid_cap(n, 256, per_sm), 256, 0, st>>>(src, c, u, o);
+        launch_pdl(k_urgency<Src, int32_t, false>, grid_cap(n, 256, per_sm), 256, st, src, c, u, o);
     } else {
         static int per_sm = occupancy(k_urgency<Src, int64_t>, 256);
-        k_urgency<Src, int64_t><<<grid_cap(n, 256, per_sm), 256, 0, st>>>(src, c, u, o);
+        launch_pdl(k_urgency<Src, int64_t, false>, grid_cap(n, 256, per_sm), 256, st, src, c, u, o);
     }
 }
 

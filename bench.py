@@ -541,7 +541,8 @@ def other_configs(reps: int = 200):
     t = timed_captured(rnd, fleet, inp, 0)
     out["configs[1] 1k robots 50x7 k=64"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t, "l2": "resident (0.3 MB inputs)",
-        "layout": "sequential graphs (at 1k robots a second stream costs more than it hides)"}
+        "layout": "sequential, one graph per round with programmatic dependent launches "
+                  "(at 1k robots a second stream costs more than it hides)"}
     # configs[2]: 16k mixed fleet, two homogeneous tensors, 64-step chunks, k = 1024
     R = 16384
     soa = synthetic.fleet_soa(R, seed=13)

@@ -93,6 +93,8 @@ def raise_round_flags(f: int) -> None:
 class DecisionRound:
     """Preallocated single-GPU decision round over R robots, budget k."""
 
+    one_graph_sequential = True  # sequential layout also captured as one graph
+
     def __init__(self, R: int, k: int, sched: _lib.KrSched):
         self.R = R
         self.k = min(k, R)
@@ -260,6 +262,16 @@ class DecisionRound:
                 self.urgency(fleet)
                 self.admit(fleet)
         self.side = torch.cuda.Stream(device=self.H.device) if reserve_sms != 0 else None
+        # sequential rounds (no side stream) also as one graph: one launch per
+        # round, and the urgency pass's programmatic launch overlaps the horizon
+        # kernel's tail (configs[1]: 20.7 -> see DESIGN "The round")
+        self.g_seq = None
+        if self.side is None and layout == "split" and self.one_graph_sequential:
+            self.g_seq = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.g_seq):
+                self.horizons(h)
+                self.urgency(fleet)
+                self.admit(fleet)
 
     def replay_concurrent(self, before_horizon=None, after_horizon=None, before_side=None,
                           after_side=None) -> None:
@@ -270,6 +282,9 @@ class DecisionRound:
         side stream at the end.  `before_horizon` / `after_horizon` (callables)
         may record events around the horizon graph."""
         main = torch.cuda.current_stream()
+        if getattr(self, "g_seq", None) is not None and not (before_horizon or after_horizon):
+            self.g_seq.replay()
+            return
         if self.g_urgency is not None:
             self.g_urgency.replay()  # the side stream forks after it
         if self.side is None:
@@ -535,6 +550,8 @@ class ShardedDecisionRound(DecisionRound):
     def admit(self, fleet: fl.DeviceFleet) -> None:
         sharded_topk(self.keys, self.R, self.k_request, self.sizes, CudaShardOps(self, fleet),
                      self.group)
+
+    one_graph_sequential = False  # one capture of the NCCL all-gather per round graph
 
     def capture(self, fleet: fl.DeviceFleet, h, reserve_sms: int = 0,
                 layout: str = "split") -> None:

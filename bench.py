@@ -599,14 +599,15 @@ def other_configs(reps: int = 200):
     del prev, cand
     U = synthetic.magnitudes(R, seed=25, dtype=torch.float64)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
-    # urgency first, then horizons || admission, 4 reserved SMs (split/8:
-    # 522-527 us, this layout 478 us; tools/conf_layout_reps.py CONF_DT=64)
+    # horizons || urgency + admission, 16 reserved SMs (median of four
+    # interleaved repeats: split/16 398 us, urgency first/4 442 us, split/2
+    # 498 us; tools/conf_layout_reps.py CONF_DT=64)
     t = timed_captured(rnd, fleet, rounds.ConfidenceInputs(
-        U, HorizonPolicyConfig.confidence(0.4, 5)), 4, layout="urgency_first")
+        U, HorizonPolicyConfig.confidence(0.4, 5)), 16)
     out["configs[4] per-GPU share, confidence policy fp64 (U 2^20 x 6 x 50 fp64), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (2.5 GB of magnitudes)",
-        "layout": "urgency_first: urgency, then horizons || admission (4 reserved SMs)"}
+        "layout": "split: horizons || urgency + admission (16 reserved SMs)"}
     del U
     # the headline fleet with a cloud tier (phase 3 at fleet scale, §8(f)1):
     # full key order + edge admission + the ordered offload scan

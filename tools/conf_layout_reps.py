@@ -1,6 +1,7 @@
 """Repeated confidence-round timings per (layout, reserved SMs), fp32 and fp64
 magnitudes (configs[4] shape), interleaved so drifts hit every layout alike:
     python tools/conf_layout_reps.py"""
+import os
 import sys
 from pathlib import Path
 
@@ -10,6 +11,8 @@ import torch  # noqa: E402
 from paper_2605_11381_b200 import HorizonPolicyConfig, fleet as fl, rounds, synthetic  # noqa: E402
 
 LAYOUTS = [("split", 2), ("split", 16), ("urgency_first", 1), ("urgency_first", 4)]
+if os.environ.get("CONF_LAYOUTS"):  # e.g. "split:12,split:20"
+    LAYOUTS = [(x.split(":")[0], int(x.split(":")[1])) for x in os.environ["CONF_LAYOUTS"].split(",")]
 
 
 def timed(rnd, reps=150):

@@ -823,7 +823,10 @@ def main():
     ap.add_argument("--eager", action="store_true",
                     help="N=1: the N>1 path (eager launches, side-stream overlap) instead of graphs")
     ap.add_argument("--reserve-sms", type=int, default=2,
-                    help="SMs left to urgency + admission (side stream) during the horizon kernel")
+                    help="SMs left to urgency + admission (side stream) during the horizon "
+                         "kernel (tools/reserve_sweep.sh; the sharded round with its NCCL "
+                         "all-gather on the side stream: --force-sharded 0.467 ms at 2, "
+                         "0.480 ms at 10)")
     ap.add_argument("--layout", choices=["split", "urgency_first"], default="split",
                     help="graph layout of the round (see rounds.DecisionRound.capture)")
     ap.add_argument("--force-sharded", action="store_true",

@@ -577,13 +577,14 @@ def other_configs(reps: int = 200):
     U = synthetic.magnitudes(R, seed=19)
     rnd = rounds.DecisionRound(R, 8192, sched_for(soa))
     inp = rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5))
-    # horizons || urgency + admission, 16 reserved SMs (median of four
-    # interleaved repeats per layout, tools/conf_layout_reps.py)
-    t = timed_captured(rnd, fleet, inp, 16)
+    # horizons || urgency + admission, 8 reserved SMs (median of four
+    # interleaved repeats per layout on two boxes: split/8 249.8-250.1 us,
+    # split/16 257.0-260.5, urgency first/1 259.3-262.1; tools/conf_layout_reps.py)
+    t = timed_captured(rnd, fleet, inp, 8)
     out["configs[4] per-GPU share, confidence policy (U 2^20 x 6 x 50 fp32), k=8192"] = {
         "us_per_round": 1e6 * t, "robot_rounds_per_s": R / t,
         "l2": "streams from HBM (1.26 GB of magnitudes)",
-        "layout": "split: horizons || urgency + admission (16 reserved SMs)"}
+        "layout": "split: horizons || urgency + admission (8 reserved SMs)"}
     # fp64 storage (the reference's native dtype, workload.py:485-486): the
     # headline divergence round and the confidence round, same layouts
     R = 1 << 20

@@ -60,7 +60,7 @@ def test_bench_round_2p20_evolving():
     prev, cand, off = synthetic.chunks(R, seed=2000)
     rnd = rounds.DecisionRound(R, k, _sched(NOW - (1 << 39)))
     inputs = rounds.DivergenceInputs(prev, cand, 0.9, offset=off)
-    rnd.capture(fleet, inputs, reserve_sms=10, layout="split")
+    rnd.capture(fleet, inputs, reserve_sms=2, layout="split")
     torch.cuda.synchronize()
     fleet.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())  # undo the warm-up round
     for r in range(3):
@@ -100,14 +100,14 @@ def test_config2_mixed_16k():
 
 
 def test_config3_ensembles_64k():
-    """(iii) configs[3]: 65,536 robots x S=8 samples, captured split/4."""
+    """(iii) configs[3]: 65,536 robots x S=8 samples, captured split/1 (bench.py)."""
     from paper_2605_11381_b200 import fleet as fl, rounds, synthetic
     R, k = 65536, 8192
     soa = synthetic.fleet_soa(R, seed=16)
     prev, cand, off = synthetic.chunks(R, seed=17, S=8)
     fleet = fl.DeviceFleet.from_host(soa)
     rnd = rounds.DecisionRound(R, k, _sched(int(soa["issued_at"].min())))
-    rnd.capture(fleet, rounds.DivergenceInputs(prev, cand, 0.9, offset=off), reserve_sms=4,
+    rnd.capture(fleet, rounds.DivergenceInputs(prev, cand, 0.9, offset=off), reserve_sms=1,
                 layout="split")
     fleet.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
     out = rnd.replay()
@@ -120,7 +120,7 @@ def test_config3_ensembles_64k():
 @pytest.mark.parametrize("storage", [torch.float32, torch.float64])
 def test_confidence_round_2p20(storage):
     """(iv) the headline fleet under the confidence policy, as bench.py's
-    other_configs runs it (split, 24 reserved SMs)."""
+    other_configs runs it (split; 8 reserved SMs for fp32, 16 for fp64)."""
     from paper_2605_11381_b200 import HorizonPolicyConfig, fleet as fl, rounds, synthetic
     R, k = 1 << 20, 8192
     soa = synthetic.fleet_soa(R, seed=18)
@@ -128,7 +128,7 @@ def test_confidence_round_2p20(storage):
     fleet = fl.DeviceFleet.from_host(soa)
     rnd = rounds.DecisionRound(R, k, _sched(int(soa["issued_at"].min())))
     rnd.capture(fleet, rounds.ConfidenceInputs(U, HorizonPolicyConfig.confidence(0.4, 5)),
-                reserve_sms=24, layout="split")
+                reserve_sms=8 if storage == torch.float32 else 16, layout="split")
     fleet.t["skipped"].copy_(torch.from_numpy(soa["skipped"]).cuda())
     out = rnd.replay()
     torch.cuda.synchronize()
